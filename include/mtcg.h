@@ -1,0 +1,236 @@
+/*
+ * mtcg.h — C ABI of the B200-native multi-tensor contraction engine.
+ *
+ * Drop-in boundary for the reference's hot path (arXiv 2108.05665 `mtc`):
+ *
+ *   mtcg_eval          replaces  EvalResult eval_all(const Plan&,
+ *                                  const NetworkDiagram&, const AssignmentSet&,
+ *                                  const EvalOptions&)      multieval.hpp:62-63
+ *                          and   EvalResult eval_sliced(...) multieval.hpp:69-70
+ *                     (the CLI's choice `plan.sliced.empty() ? eval_all :
+ *                      eval_sliced` is MTCG_EVAL_AUTO, tools/main.cpp:159-160)
+ *   mtcg_linear_xeb    replaces  double linear_xeb(int n,
+ *                                  const std::vector<double>& probs)  xeb.hpp:38
+ *   mtcg_linear_xeb_amplitudes
+ *                      replaces  linear_xeb(n, probs_from_amplitudes(amps))
+ *                                                            xeb.hpp:38,42-43
+ *
+ * (paths relative to /root/reference/proj/include/mtc and proj/tools.)
+ *
+ * The staged API (mtcg_compile / mtcg_run / mtcg_fetch / mtcg_xeb_device)
+ * splits mtcg_eval so callers can keep the compiled problem resident in HBM,
+ * shard slice ranges over one process per GPU and combine the per-rank
+ * partial amplitudes with one NCCL collective.
+ *
+ * Conventions
+ *  - No function throws. Every call returns an mtcg_status; on failure a
+ *    NUL-terminated message is written to err[0..errlen) when err != NULL.
+ *    Status codes mirror the reference's exception classes:
+ *      MTCG_ERR_DATA        mtc::DataError     (CLI exit 2)
+ *      MTCG_ERR_MEMORY_CAP  mtc::MemoryCapError (CLI exit 3); the offending
+ *                           plan node is returned in mtcg_result.cap_node /
+ *                           the cap_node out-parameter
+ *      MTCG_ERR_INTERNAL    std::logic_error    (CLI exit 1)
+ *  - All input arrays are borrowed for the duration of the call and copied
+ *    to the device; the caller owns every output buffer. No device pointer
+ *    owned by the library escapes; device pointers passed IN (mtcg_run's
+ *    accumulator) belong to the caller.
+ *  - Calls on one handle are not reentrant; separate handles are
+ *    independent.
+ *  - Complex numbers cross the boundary as interleaved (re, im) doubles, the
+ *    layout of std::complex<double> (tensor.hpp:26).
+ */
+#ifndef MTCG_H
+#define MTCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MTCG_ABI_VERSION 1
+
+typedef enum mtcg_status {
+  MTCG_OK = 0,
+  MTCG_ERR_INTERNAL = 1,
+  MTCG_ERR_DATA = 2,
+  MTCG_ERR_MEMORY_CAP = 3,
+  MTCG_ERR_CUDA = 5,
+  MTCG_ERR_ARGUMENT = 6
+} mtcg_status;
+
+/* Arithmetic of the device path.
+ *  MTCG_C64   complex64 (fp32 pairs) — the production mode; amplitudes agree
+ *             with the complex128 reference within 1e-4 relative.
+ *  MTCG_C128  complex128 with every multiply/add individually rounded
+ *             (no FMA contraction) and closed legs summed in the reference's
+ *             ascending-id row-major order (tensor.cpp:186-245): per-slice
+ *             values are bit-identical to the reference, and so is the
+ *             slice fold on one device. */
+typedef enum mtcg_precision { MTCG_C64 = 0, MTCG_C128 = 1 } mtcg_precision;
+
+typedef enum mtcg_eval_mode {
+  MTCG_EVAL_AUTO = 0,   /* sliced plan ? eval_sliced : eval_all */
+  MTCG_EVAL_ALL = 1,    /* eval_all: rejects sliced plans (DataError) */
+  MTCG_EVAL_SLICED = 2  /* eval_sliced: rejects unsliced plans (DataError) */
+} mtcg_eval_mode;
+
+/* The engine's inputs, as POD arrays. Field groups mirror the reference
+ * types the engine reads; nothing else of them is needed. */
+typedef struct mtcg_problem {
+  /* Plan (plan.hpp:33-45): binary tree over slots + sliced legs. Leaves have
+   * slot >= 0 and left = right = -1; internal nodes have slot = -1. */
+  int32_t n_nodes;
+  const int32_t* node_left;
+  const int32_t* node_right;
+  const int32_t* node_slot;
+  int32_t root;
+  int32_t n_sliced;
+  const uint32_t* sliced; /* in plan order: slice enumeration is mixed radix
+                             with the LAST listed leg fastest
+                             (multieval.cpp:322-329) */
+  /* NetworkDiagram (diagram.hpp:32-45): legs [0, n_closed) are closed, legs
+   * [n_closed, n_legs) open (the open leg of qubit q is n_closed + q). */
+  uint32_t n_legs;
+  uint32_t n_closed;
+  const uint32_t* leg_dims; /* [n_legs]; this engine supports dim 2 */
+  int32_t n_slots;
+  /* AssignmentSet (diagram.hpp:61-68). Slot j has slot_n_values[j] value
+   * tensors sharing one leg list slot_legs[slot_leg_begin[j] ..
+   * slot_leg_begin[j+1]) (listed order = row-major order). `values` holds
+   * all of them, slot-major then value-major, each row-major. */
+  const int32_t* slot_n_values;   /* [n_slots] */
+  const int32_t* slot_leg_begin;  /* [n_slots + 1] */
+  const uint32_t* slot_legs;
+  const double* values;           /* complex128 interleaved */
+  uint64_t n_requests;
+  const uint32_t* tuples;         /* [n_requests][n_slots] value indices */
+  int32_t n_batch_legs;           /* '*' legs kept open, ascending */
+  const uint32_t* batch_legs;
+} mtcg_problem;
+
+typedef struct mtcg_options {
+  int32_t eval_mode;          /* mtcg_eval_mode */
+  int32_t precision;          /* mtcg_precision */
+  uint64_t memory_cap_bytes;  /* device arena cap; 0 = the handle's cap */
+  int32_t workers;            /* EvalOptions.workers (accepted; the device
+                                 runs slices itself — results never depend on
+                                 it, multieval.hpp:66-68) */
+  int32_t reserved;
+} mtcg_options;
+
+/* eval outputs. `values` is a caller buffer of values_capacity complex
+ * elements receiving, request-major, each request's tensor (order-0, or
+ * order-w over the batch legs ascending — tools/main.cpp:167-178). */
+typedef struct mtcg_result {
+  double* values;
+  uint64_t values_capacity;      /* complex elements available */
+  uint64_t* node_contractions;   /* [n_nodes] or NULL: contractions performed
+                                    per plan node, summed over slices */
+  uint64_t mults, adds, rw;      /* OpCounters (tensor.hpp:36-51), exact */
+  uint64_t hbm_peak_bytes;       /* device arena high-water mark (the GPU
+                                    schedule's; not the reference's
+                                    Session peak) */
+  int32_t cap_node;              /* node of a MEMORY_CAP failure, else -1 */
+  int32_t n_out_legs;            /* legs of each value tensor */
+  uint32_t out_legs[64];
+} mtcg_result;
+
+typedef struct mtcg_handle mtcg_handle;
+typedef struct mtcg_plan mtcg_plan;
+
+/* Static facts about a compiled problem. */
+typedef struct mtcg_plan_info {
+  uint64_t n_requests;
+  uint64_t n_rows;              /* distinct request tuples */
+  uint64_t row_elems;           /* 2^w: elements per request tensor */
+  uint64_t n_slices;            /* Π dims(sliced legs); 1 when unsliced */
+  uint64_t mults, adds, rw;     /* per full evaluation (all slices) */
+  uint64_t contractions;        /* Σ node contractions, all slices */
+  uint64_t hbm_arena_bytes;     /* device bytes of the per-slice schedule */
+  uint64_t hbm_resident_bytes;  /* leaves + index arrays kept on device */
+  int32_t precision;
+  int32_t n_kernels_per_slice;  /* device launches per slice */
+} mtcg_plan_info;
+
+int mtcg_version(void);
+
+/* Creates an engine bound to CUDA device `device`. hbm_cap_bytes caps the
+ * device arena of every compiled plan (0 = free device memory). */
+mtcg_status mtcg_create(int device, uint64_t hbm_cap_bytes,
+                        mtcg_handle** out, char* err, size_t errlen);
+void mtcg_destroy(mtcg_handle* h);
+
+/* One-shot evaluation: compile + run all slices + fetch. The drop-in for
+ * eval_all / eval_sliced. */
+mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p,
+                      const mtcg_options* opt, mtcg_result* res, char* err,
+                      size_t errlen);
+
+/* linear_xeb (xeb.cpp:43-50): (2^n / k) * Σ probs − 1, compensated sum;
+ * DataError on empty input, n outside [0, 1022] or a negative probability. */
+mtcg_status mtcg_linear_xeb(mtcg_handle* h, int n_qubits, const double* probs,
+                            uint64_t count, double* out, char* err,
+                            size_t errlen);
+/* The same over |amp|^2 of complex amplitudes (probs_from_amplitudes,
+ * xeb.cpp:67-73), fused on the device. */
+mtcg_status mtcg_linear_xeb_amplitudes(mtcg_handle* h, int n_qubits,
+                                       const double* amps, uint64_t count,
+                                       double* out, char* err, size_t errlen);
+
+/* ---- staged API -------------------------------------------------------- */
+
+/* Validates the problem exactly as eval_all/eval_sliced do, builds the
+ * tuple index (plan.cpp:292-333) and the device schedule, and uploads the
+ * leaves. The device arena is sized here (MEMORY_CAP → cap_node). */
+mtcg_status mtcg_compile(mtcg_handle* h, const mtcg_problem* p,
+                         const mtcg_options* opt, mtcg_plan** out,
+                         int32_t* cap_node, char* err, size_t errlen);
+void mtcg_plan_destroy(mtcg_plan* plan);
+mtcg_status mtcg_plan_get_info(const mtcg_plan* plan, mtcg_plan_info* info);
+
+/* Runs slices [slice_begin, slice_end) on `stream` (a cudaStream_t, NULL =
+ * the handle's stream) and accumulates the root values, by row, into the
+ * caller's device buffer `d_acc` (n_rows * row_elems complex of the plan's
+ * precision: float2 for C64, double2 for C128). accumulate = 0 overwrites
+ * with the first slice of the range. Slices are folded in increasing slice
+ * index (multieval.cpp:498-513). Asynchronous with respect to the host. */
+mtcg_status mtcg_run(mtcg_plan* plan, uint64_t slice_begin,
+                     uint64_t slice_end, void* d_acc, int accumulate,
+                     void* stream, char* err, size_t errlen);
+
+/* Copies a device accumulator back and fans rows out to requests
+ * (multieval.cpp:374-380), filling res->values / out_legs / counters for the
+ * slices [0, n_slices) (node_contractions, mults, adds, rw are the full
+ * evaluation's). Synchronises `stream`. */
+mtcg_status mtcg_fetch(mtcg_plan* plan, const void* d_acc, void* stream,
+                       mtcg_result* res, char* err, size_t errlen);
+
+/* Fused |amp|^2 -> linear XEB over every request (duplicates included, each
+ * batch element an amplitude, as the CLI's TSV feeds `mtc xeb`) straight from
+ * a device accumulator. Synchronises `stream`. */
+mtcg_status mtcg_xeb_device(mtcg_plan* plan, const void* d_acc,
+                            int n_qubits, void* stream, double* out,
+                            char* err, size_t errlen);
+
+/* Shape-only replay (the reference's `emulate`, multieval.hpp:72-75): runs
+ * every validation of mtcg_eval and the full schedule construction on the
+ * host — no device needed — and reports the exact counts (info->mults, adds,
+ * rw, contractions; node_contractions [n_nodes] or NULL) and the device
+ * arena the evaluation would use. cap_bytes = 0: no cap. */
+mtcg_status mtcg_emulate(const mtcg_problem* p, const mtcg_options* opt,
+                         uint64_t cap_bytes, mtcg_plan_info* info,
+                         uint64_t* node_contractions, int32_t* cap_node,
+                         char* err, size_t errlen);
+
+/* Count of device kernel launches issued by this process through the
+ * library since mtcg_create (evidence for the bench's gpu_launches). */
+uint64_t mtcg_launch_count(const mtcg_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MTCG_H */

@@ -1,0 +1,56 @@
+// Tile configurations of the batched contraction kernel, shared by the host
+// planner (selection) and the device code (instantiation).
+#pragma once
+
+namespace mtcg {
+
+struct TileConfig {
+  int tm, tn, rm, rn;  // block tile M x N, per-thread register tile rm x rn
+};
+
+// Index 0 is the per-output-element kernel (no tiling) used for contractions
+// with fewer than 256 outputs per item.
+constexpr int kGenericConfig = 0;
+constexpr int kNumTileConfigs = 11;
+constexpr TileConfig kTileConfigs[kNumTileConfigs] = {
+    {1, 1, 1, 1},      // 0: generic
+    {128, 64, 8, 4},   // 1
+    {128, 32, 8, 2},   // 2
+    {128, 16, 4, 2},   // 3
+    {256, 8, 8, 1},    // 4
+    {256, 4, 4, 1},    // 5
+    {256, 2, 2, 1},    // 6
+    {256, 1, 1, 1},    // 7
+    {64, 64, 4, 4},    // 8
+    {32, 32, 2, 2},    // 9
+    {16, 16, 1, 1},    // 10
+};
+
+// K elements staged per k-step (complex64 / complex128).
+constexpr int kTileK64 = 16;
+constexpr int kTileK128 = 8;
+
+inline int select_config(int fa, int fb) {
+  // fa >= fb by construction (A is the side with more free legs).
+  if (fa + fb < 8) return kGenericConfig;
+  const int M = fa, N = fb;  // log2
+  if (M >= 7) {
+    if (N >= 6) return 1;
+    if (N == 5) return 2;
+    if (N == 4) return 3;
+    if (M >= 8) {
+      if (N == 3) return 4;
+      if (N == 2) return 5;
+      if (N == 1) return 6;
+      return 7;
+    }
+    // M == 128 and N <= 8
+    return N == 3 ? 3 : kGenericConfig;
+  }
+  if (M == 6) return N >= 6 ? 8 : (N >= 4 ? 9 : kGenericConfig);
+  if (M == 5) return N >= 4 ? 9 : kGenericConfig;
+  if (M == 4) return N >= 4 ? 10 : kGenericConfig;
+  return kGenericConfig;
+}
+
+}  // namespace mtcg

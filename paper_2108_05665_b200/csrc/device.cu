@@ -1,0 +1,619 @@
+// Device side of the multi-tensor contraction engine (sm_100a).
+//
+// One batched launch per plan node per slice: every distinct (node, rank)
+// contraction of the node (plan.hpp:103-111 `distinct`) is an item of the
+// batch; operands are gathered from the children's HBM tables through
+// per-item entry indices and bit-permutation offset tables, so leg
+// permutations and slice projections (project_leg, tensor.cpp:255-282) are
+// folded into the loads instead of materialised.
+//
+// Kernels
+//   contract_tile     register/smem-tiled complex GEMM per item: A rows are
+//                     K-contiguous (the planner stores every intermediate as
+//                     [kept legs][legs the parent closes]); output written
+//                     through per-tile offset tables, lanes along the output's
+//                     contiguous dimension.
+//   contract_generic  one thread per output element, for items with < 256
+//                     outputs.
+//   leaf_root         single-slot networks.
+//   xeb_*             fused |amp|^2 -> compensated fp64 reductions.
+//
+// Precision: C64 uses fp32 FMA; C128 uses individually rounded fp64
+// multiplies/adds in the reference order (tensor.cpp:186-245) and is
+// bit-identical to the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "configs.hpp"
+#include "device.hpp"
+
+namespace mtcg {
+
+struct Engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+};
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t err__ = (x);                                                   \
+    if (err__ != cudaSuccess)                                                  \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(err__));     \
+  } while (0)
+
+namespace {
+
+// ---- complex arithmetic ----------------------------------------------------
+
+template <class R>
+struct V2;
+template <>
+struct V2<float> {
+  using T = float2;
+};
+template <>
+struct V2<double> {
+  using T = double2;
+};
+
+// acc (+)= a * b. C64: fp32 FMA. C128 exact: the reference's
+// pr = xr*yr - xi*yi, pi = xr*yi + xi*yr, each op rounded (no contraction),
+// and the first product seeds the accumulator (tensor.cpp:196-213).
+__device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b, bool) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+__device__ __forceinline__ void cmac(double2& acc, double2 a, double2 b, bool first) {
+  const double pr = __dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y));
+  const double pi = __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x));
+  if (first) {
+    acc.x = pr;
+    acc.y = pi;
+  } else {
+    acc.x = __dadd_rn(acc.x, pr);
+    acc.y = __dadd_rn(acc.y, pi);
+  }
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  return make_float2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+template <class T>
+__device__ __forceinline__ T czero();
+template <>
+__device__ __forceinline__ float2 czero<float2>() {
+  return make_float2(0.f, 0.f);
+}
+template <>
+__device__ __forceinline__ double2 czero<double2>() {
+  return make_double2(0.0, 0.0);
+}
+
+// ---- kernel parameters ---------------------------------------------------------
+
+struct DTable {
+  const uint32_t* lo;
+  const uint32_t* hi;
+  int lo_bits;
+  __device__ __forceinline__ uint32_t operator()(uint64_t x) const {
+    return __ldg(lo + (x & ((1u << lo_bits) - 1))) + __ldg(hi + (x >> lo_bits));
+  }
+};
+
+template <class T>
+struct DevOp {
+  const T* a;               // A table base
+  const T* b;
+  T* out;
+  const uint32_t* ia;       // per item entry
+  const uint32_t* ib;
+  const uint32_t* out_rows; // root: item -> accumulator row, else null
+  uint64_t a_item, b_item, out_item;
+  uint64_t a_slice, b_slice;  // slice projection offsets (elements)
+  DTable tam, tak, tbn, tbk, tom, ton;
+  uint32_t nb;
+  int fa, fb, kc;
+  int n_fast;               // epilogue lane order
+  int accumulate;           // root: add into the accumulator
+};
+
+// ---- tiled batched contraction -------------------------------------------------
+
+template <class R, int TM, int TN, int RM, int RN, int TK>
+__global__ void __launch_bounds__((TM / RM) * (TN / RN))
+    contract_tile(const DevOp<typename V2<R>::T> op) {
+  using T = typename V2<R>::T;
+  constexpr int NT = (TM / RM) * (TN / RN);
+  constexpr int TXN = TN / RN;  // threads along n
+  constexpr int TYM = TM / RM;  // threads along m
+  constexpr bool kExact = sizeof(R) == 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* As = reinterpret_cast<T*>(smem_raw);         // [TK][TM+1]
+  T* Bs = As + TK * (TM + 1);                     // [TK][TN+1]
+  uint32_t* aoff = reinterpret_cast<uint32_t*>(Bs + TK * (TN + 1));
+  uint32_t* boff = aoff + TM;
+  uint32_t* omo = boff + TN;
+  uint32_t* ono = omo + TM;
+  uint32_t* kao = ono + TN;
+  uint32_t* kbo = kao + TK;
+
+  const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb;
+  const uint64_t K = uint64_t{1} << op.kc;
+  const uint64_t tiles_m = (M + TM - 1) / TM, tiles_n = (N + TN - 1) / TN;
+  const uint64_t tile = blockIdx.x + uint64_t{gridDim.x} * blockIdx.y;
+  const uint64_t tn_i = tile % tiles_n;
+  const uint64_t tm_i = (tile / tiles_n) % tiles_m;
+  const uint64_t item = tile / (tiles_n * tiles_m);
+  if (item >= op.nb) return;
+  const uint64_t m0 = tm_i * TM, n0 = tn_i * TN;
+  const int tid = threadIdx.x;
+
+  const T* A = op.a + uint64_t{op.ia ? __ldg(op.ia + item) : (uint32_t)item} * op.a_item + op.a_slice;
+  const T* B = op.b + uint64_t{op.ib ? __ldg(op.ib + item) : (uint32_t)item} * op.b_item + op.b_slice;
+  T* O = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + item)} : item) * op.out_item;
+
+  for (int i = tid; i < TM; i += NT) {
+    aoff[i] = m0 + i < M ? op.tam(m0 + i) : 0u;
+    omo[i] = m0 + i < M ? op.tom(m0 + i) : 0u;
+  }
+  for (int i = tid; i < TN; i += NT) {
+    boff[i] = n0 + i < N ? op.tbn(n0 + i) : 0u;
+    ono[i] = n0 + i < N ? op.ton(n0 + i) : 0u;
+  }
+
+  int tx, ty;
+  if (op.n_fast) {
+    tx = tid % TXN;
+    ty = tid / TXN;
+  } else {
+    ty = tid % TYM;
+    tx = tid / TYM;
+  }
+
+  T acc[RM][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) acc[i][j] = czero<T>();
+
+  const int tk = static_cast<int>(K < TK ? K : TK);
+  const int m_valid = static_cast<int>(M - m0 < TM ? M - m0 : TM);
+  const int n_valid = static_cast<int>(N - n0 < TN ? N - n0 : TN);
+  for (uint64_t k0 = 0; k0 < K; k0 += tk) {
+    __syncthreads();  // previous chunk consumed; offsets visible
+    for (int i = tid; i < tk; i += NT) {
+      kao[i] = op.tak(k0 + i);
+      kbo[i] = op.tbk(k0 + i);
+    }
+    __syncthreads();
+    // A tile: k fastest across lanes (K-contiguous rows)
+    for (int e = tid; e < TM * tk; e += NT) {
+      const int row = e / tk, kk = e - row * tk;
+      As[kk * (TM + 1) + row] = row < m_valid ? A[aoff[row] + kao[kk]] : czero<T>();
+    }
+    for (int e = tid; e < TN * tk; e += NT) {
+      const int col = e / tk, kk = e - col * tk;
+      Bs[kk * (TN + 1) + col] = col < n_valid ? B[boff[col] + kbo[kk]] : czero<T>();
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < tk; ++kk) {
+      T av[RM], bv[RN];
+#pragma unroll
+      for (int i = 0; i < RM; ++i) av[i] = As[kk * (TM + 1) + ty + i * TYM];
+#pragma unroll
+      for (int j = 0; j < RN; ++j) bv[j] = Bs[kk * (TN + 1) + tx + j * TXN];
+      const bool first = kExact && k0 == 0 && kk == 0;
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) cmac(acc[i][j], av[i], bv[j], first);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RM; ++i) {
+    const int r = ty + i * TYM;
+    if (r >= m_valid) continue;
+#pragma unroll
+    for (int j = 0; j < RN; ++j) {
+      const int cidx = tx + j * TXN;
+      if (cidx >= n_valid) continue;
+      T* dst = O + omo[r] + ono[cidx];
+      *dst = op.accumulate ? cadd(*dst, acc[i][j]) : acc[i][j];
+    }
+  }
+}
+
+// ---- one thread per output element ---------------------------------------------
+
+template <class R>
+__global__ void __launch_bounds__(256)
+    contract_generic(const DevOp<typename V2<R>::T> op) {
+  using T = typename V2<R>::T;
+  const int r_out = op.fa + op.fb;
+  const uint64_t total = uint64_t{op.nb} << r_out;
+  const uint64_t K = uint64_t{1} << op.kc;
+  const uint64_t omask = (uint64_t{1} << r_out) - 1;
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t item = e >> r_out, o = e & omask;
+    const T* A = op.a + uint64_t{op.ia ? __ldg(op.ia + item) : (uint32_t)item} * op.a_item +
+                 op.a_slice + op.tam(o);
+    const T* B = op.b + uint64_t{op.ib ? __ldg(op.ib + item) : (uint32_t)item} * op.b_item +
+                 op.b_slice + op.tbn(o);
+    T acc = czero<T>();
+    for (uint64_t c = 0; c < K; ++c) cmac(acc, A[op.tak(c)], B[op.tbk(c)], c == 0);
+    T* dst = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + item)} : item) * op.out_item + o;
+    *dst = op.accumulate ? cadd(*dst, acc) : acc;
+  }
+}
+
+// ---- single-slot network: every row's value is the projected leaf ----------------
+
+template <class T>
+__global__ void leaf_root(const T* leaves, uint64_t item, const uint32_t* row_value,
+                          uint64_t rows, int r_out, DTable tout, uint64_t slice_off,
+                          T* acc, int accumulate) {
+  const uint64_t total = rows << r_out;
+  const uint64_t omask = (uint64_t{1} << r_out) - 1;
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t r = e >> r_out, o = e & omask;
+    const T v = leaves[uint64_t{row_value[r]} * item + slice_off + tout(o)];
+    acc[e] = accumulate ? cadd(acc[e], v) : v;
+  }
+}
+
+// ---- XEB reductions ------------------------------------------------------------------
+
+// Error-free pairwise combination of (sum, compensation) partials.
+__device__ __forceinline__ void two_sum_add(double& s, double& c, double x) {
+  const double t = s + x;
+  if (fabs(s) >= fabs(x))
+    c += (s - t) + x;
+  else
+    c += (x - t) + s;
+  s = t;
+}
+
+template <class T>
+__global__ void xeb_acc_kernel(const T* acc, const uint32_t* row_mult, uint64_t rows,
+                               int r_out, double* partial) {
+  const uint64_t total = rows << r_out;
+  double s = 0.0, c = 0.0;
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    const T v = acc[e];
+    const double re = v.x, im = v.y;
+    const double p = re * re + im * im;  // std::norm
+    const uint32_t mult = row_mult[e >> r_out];
+    for (uint32_t q = 0; q < mult; ++q) two_sum_add(s, c, p);
+  }
+  __shared__ double ss[256], sc[256];
+  ss[threadIdx.x] = s;
+  sc[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bs = 0.0, bc = 0.0;
+    for (int i = 0; i < blockDim.x; ++i) {
+      two_sum_add(bs, bc, ss[i]);
+      bc += sc[i];
+    }
+    partial[2 * blockIdx.x] = bs;
+    partial[2 * blockIdx.x + 1] = bc;
+  }
+}
+
+__global__ void xeb_probs_kernel(const double* probs, uint64_t count, int amplitudes,
+                                 double* partial, int* negative) {
+  double s = 0.0, c = 0.0;
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < count;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    double p;
+    if (amplitudes) {
+      const double re = probs[2 * e], im = probs[2 * e + 1];
+      p = re * re + im * im;
+    } else {
+      p = probs[e];
+    }
+    if (p < 0.0) *negative = 1;
+    two_sum_add(s, c, p);
+  }
+  __shared__ double ss[256], sc[256];
+  ss[threadIdx.x] = s;
+  sc[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bs = 0.0, bc = 0.0;
+    for (int i = 0; i < blockDim.x; ++i) {
+      two_sum_add(bs, bc, ss[i]);
+      bc += sc[i];
+    }
+    partial[2 * blockIdx.x] = bs;
+    partial[2 * blockIdx.x + 1] = bc;
+  }
+}
+
+double finish_partials(const std::vector<double>& part) {
+  double s = 0.0, c = 0.0;
+  for (size_t i = 0; i < part.size(); i += 2) {
+    const double x = part[i];
+    const double t = s + x;
+    if (std::fabs(s) >= std::fabs(x))
+      c += (s - t) + x;
+    else
+      c += (x - t) + s;
+    s = t;
+    c += part[i + 1];
+  }
+  return s + c;
+}
+
+// ---- launch helpers ---------------------------------------------------------------------
+
+constexpr int kSmSlots = 148 * 8;
+
+template <class R, int TM, int TN, int RM, int RN>
+void launch_tile(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
+  using T = typename V2<R>::T;
+  constexpr int TK = sizeof(R) == 4 ? kTileK64 : kTileK128;
+  constexpr int NT = (TM / RM) * (TN / RN);
+  const size_t smem = sizeof(T) * (TK * (TM + 1) + TK * (TN + 1)) +
+                      sizeof(uint32_t) * (2 * TM + 2 * TN + 2 * TK);
+  auto kern = contract_tile<R, TM, TN, RM, RN, TK>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    attr_set = true;
+  }
+  const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb;
+  const uint64_t tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN) * op.nb;
+  const uint64_t gx = std::min<uint64_t>(tiles, 65535);
+  const uint64_t gy = (tiles + gx - 1) / gx;
+  kern<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), NT, smem, st>>>(op);
+}
+
+template <class R>
+void launch_op(const DevOp<typename V2<R>::T>& op, int config, cudaStream_t st) {
+  switch (config) {
+    case 1: return launch_tile<R, 128, 64, 8, 4>(op, st);
+    case 2: return launch_tile<R, 128, 32, 8, 2>(op, st);
+    case 3: return launch_tile<R, 128, 16, 4, 2>(op, st);
+    case 4: return launch_tile<R, 256, 8, 8, 1>(op, st);
+    case 5: return launch_tile<R, 256, 4, 4, 1>(op, st);
+    case 6: return launch_tile<R, 256, 2, 2, 1>(op, st);
+    case 7: return launch_tile<R, 256, 1, 1, 1>(op, st);
+    case 8: return launch_tile<R, 64, 64, 4, 4>(op, st);
+    case 9: return launch_tile<R, 32, 32, 2, 2>(op, st);
+    case 10: return launch_tile<R, 16, 16, 1, 1>(op, st);
+    default: {
+      const uint64_t total = uint64_t{op.nb} << (op.fa + op.fb);
+      const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, kSmSlots * 4);
+      contract_generic<R><<<static_cast<unsigned>(blocks), 256, 0, st>>>(op);
+    }
+  }
+}
+
+DTable dtable(const uint32_t* blob, const SplitTable& t) {
+  DTable d;
+  d.lo = blob + t.dev_off;
+  d.hi = blob + t.dev_off + t.lo.size();
+  d.lo_bits = t.lo_bits;
+  return d;
+}
+
+uint64_t slice_offset(const std::vector<uint64_t>& strides, uint64_t s) {
+  uint64_t off = 0;
+  for (size_t b = 0; b < strides.size(); ++b)
+    if (s >> b & 1) off += strides[b];
+  return off;
+}
+
+template <class R>
+void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
+                  cudaStream_t st) {
+  using T = typename V2<R>::T;
+  Compiled& c = dp.c;
+  T* arena = static_cast<T*>(dp.d_arena);
+  const T* leaves = static_cast<const T*>(dp.d_leaves);
+  T* acc = static_cast<T*>(d_acc);
+  for (uint64_t s = s0; s < s1; ++s) {
+    const int acc_flag = (accumulate || s > s0) ? 1 : 0;
+    for (const Op& op : c.ops) {
+      if (op.nb == 0) continue;
+      DevOp<T> d;
+      d.a = op.a_leaf ? leaves + op.a_base : arena + op.a_base;
+      d.b = op.b_leaf ? leaves + op.b_base : arena + op.b_base;
+      d.out = op.root ? acc : arena + op.out_base;
+      d.ia = dp.d_index + op.ia_off;
+      d.ib = dp.d_index + op.ib_off;
+      d.out_rows = op.root ? dp.d_index + op.out_rows_off : nullptr;
+      d.a_item = op.a_item;
+      d.b_item = op.b_item;
+      d.out_item = op.out_item;
+      d.a_slice = op.a_leaf ? slice_offset(op.a_slice_stride, s) : 0;
+      d.b_slice = op.b_leaf ? slice_offset(op.b_slice_stride, s) : 0;
+      d.tam = dtable(dp.d_tables, op.tam);
+      d.tak = dtable(dp.d_tables, op.tak);
+      d.tbn = dtable(dp.d_tables, op.tbn);
+      d.tbk = dtable(dp.d_tables, op.tbk);
+      d.tom = dtable(dp.d_tables, op.tom);
+      d.ton = dtable(dp.d_tables, op.ton);
+      d.nb = op.nb;
+      d.fa = op.fa;
+      d.fb = op.fb;
+      d.kc = op.kc;
+      d.n_fast = op.store_n_fast ? 1 : 0;
+      d.accumulate = op.root ? acc_flag : 0;
+      launch_op<R>(d, op.config, st);
+      dp.engine->launches++;
+    }
+    if (c.has_leaf_root && c.n_rows > 0) {
+      const LeafRoot& lr = c.leaf_root;
+      const int r_out = static_cast<int>(c.out_legs.size());
+      const uint64_t total = c.n_rows << r_out;
+      const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, kSmSlots * 4);
+      leaf_root<T><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+          leaves + c.slot_base[lr.slot], lr.item, dp.d_index + lr.rows_off, c.n_rows, r_out,
+          dtable(dp.d_tables, lr.tout), slice_offset(lr.slice_stride, s), acc, acc_flag);
+      dp.engine->launches++;
+    }
+  }
+  CK(cudaGetLastError());
+}
+
+}  // namespace
+
+// ---- engine / plan lifetime -----------------------------------------------------------
+
+Engine* engine_create(int device) {
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) throw CudaError("CUDA device " + std::to_string(device) + " not present");
+  CK(cudaSetDevice(device));
+  auto* e = new Engine;
+  e->device = device;
+  CK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+  return e;
+}
+
+void engine_destroy(Engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+uint64_t engine_launches(const Engine* e) { return e->launches; }
+void* engine_stream(Engine* e) { return e->stream; }
+
+DevicePlan::~DevicePlan() {
+  if (engine) cudaSetDevice(engine->device);
+  for (void* p : {d_leaves, d_arena, static_cast<void*>(d_tables), static_cast<void*>(d_index),
+                  static_cast<void*>(d_slice_strides), static_cast<void*>(d_row_mult)})
+    if (p) cudaFree(p);
+}
+
+std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
+  CK(cudaSetDevice(e->device));
+  auto dp = std::make_unique<DevicePlan>();
+  dp->engine = e;
+  dp->c = std::move(c);
+  Compiled& cc = dp->c;
+  const size_t eb = cc.elem_bytes;
+  // leaves in the plan precision
+  CK(cudaMalloc(&dp->d_leaves, std::max<size_t>(cc.leaf_elems * eb, 16)));
+  if (cc.precision == MTCG_C64) {
+    std::vector<float> tmp(2 * cc.leaf_elems);
+    for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = static_cast<float>(cc.leaf_values[i]);
+    CK(cudaMemcpy(dp->d_leaves, tmp.data(), tmp.size() * sizeof(float), cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemcpy(dp->d_leaves, cc.leaf_values.data(), cc.leaf_values.size() * sizeof(double),
+                  cudaMemcpyHostToDevice));
+  }
+  if (cc.arena_elems) CK(cudaMalloc(&dp->d_arena, cc.arena_elems * eb));
+  CK(cudaMalloc(&dp->d_tables, std::max<size_t>(cc.table_blob.size(), 1) * 4));
+  if (!cc.table_blob.empty())
+    CK(cudaMemcpy(dp->d_tables, cc.table_blob.data(), cc.table_blob.size() * 4,
+                  cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&dp->d_index, std::max<size_t>(cc.index_blob.size(), 1) * 4));
+  if (!cc.index_blob.empty())
+    CK(cudaMemcpy(dp->d_index, cc.index_blob.data(), cc.index_blob.size() * 4,
+                  cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&dp->d_row_mult, std::max<size_t>(cc.row_mult.size(), 1) * 4));
+  if (!cc.row_mult.empty())
+    CK(cudaMemcpy(dp->d_row_mult, cc.row_mult.data(), cc.row_mult.size() * 4,
+                  cudaMemcpyHostToDevice));
+  return dp;
+}
+
+void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
+                void* stream) {
+  CK(cudaSetDevice(dp.engine->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
+  if (dp.c.precision == MTCG_C64)
+    run_slices_t<float>(dp, s0, s1, d_acc, accumulate, st);
+  else
+    run_slices_t<double>(dp, s0, s1, d_acc, accumulate, st);
+}
+
+double xeb_device(DevicePlan& dp, const void* d_acc, int n_qubits, void* stream) {
+  CK(cudaSetDevice(dp.engine->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
+  const Compiled& c = dp.c;
+  const int r_out = static_cast<int>(c.out_legs.size());
+  const uint64_t total = c.n_rows << r_out;
+  const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 592)));
+  double* d_part = nullptr;
+  CK(cudaMallocAsync(&d_part, sizeof(double) * 2 * blocks, st));
+  if (c.precision == MTCG_C64)
+    xeb_acc_kernel<float2><<<blocks, 256, 0, st>>>(static_cast<const float2*>(d_acc),
+                                                   dp.d_row_mult, c.n_rows, r_out, d_part);
+  else
+    xeb_acc_kernel<double2><<<blocks, 256, 0, st>>>(static_cast<const double2*>(d_acc),
+                                                    dp.d_row_mult, c.n_rows, r_out, d_part);
+  dp.engine->launches++;
+  std::vector<double> part(2 * blocks);
+  CK(cudaMemcpyAsync(part.data(), d_part, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_part, st));
+  CK(cudaStreamSynchronize(st));
+  const double count = static_cast<double>(c.n_requests) * static_cast<double>(c.row_elems);
+  return std::ldexp(finish_partials(part) / count, n_qubits) - 1.0;
+}
+
+double xeb_probs(Engine* e, const double* probs, uint64_t count, int n_qubits, bool amplitudes) {
+  CK(cudaSetDevice(e->device));
+  cudaStream_t st = e->stream;
+  const uint64_t words = amplitudes ? 2 * count : count;
+  double* d_in = nullptr;
+  double* d_part = nullptr;
+  int* d_neg = nullptr;
+  const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, 592)));
+  CK(cudaMallocAsync(&d_in, sizeof(double) * words, st));
+  CK(cudaMallocAsync(&d_part, sizeof(double) * 2 * blocks, st));
+  CK(cudaMallocAsync(&d_neg, sizeof(int), st));
+  CK(cudaMemsetAsync(d_neg, 0, sizeof(int), st));
+  CK(cudaMemcpyAsync(d_in, probs, sizeof(double) * words, cudaMemcpyHostToDevice, st));
+  xeb_probs_kernel<<<blocks, 256, 0, st>>>(d_in, count, amplitudes ? 1 : 0, d_part, d_neg);
+  e->launches++;
+  std::vector<double> part(2 * blocks);
+  int neg = 0;
+  CK(cudaMemcpyAsync(part.data(), d_part, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&neg, d_neg, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_in, st));
+  CK(cudaFreeAsync(d_part, st));
+  CK(cudaFreeAsync(d_neg, st));
+  CK(cudaStreamSynchronize(st));
+  if (neg) throw DataError("negative probability");
+  return std::ldexp(finish_partials(part) / static_cast<double>(count), n_qubits) - 1.0;
+}
+
+void* device_alloc(Engine* e, uint64_t bytes) {
+  CK(cudaSetDevice(e->device));
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<uint64_t>(bytes, 16)));
+  return p;
+}
+
+void device_free(Engine* e, void* p) {
+  cudaSetDevice(e->device);
+  if (p) cudaFree(p);
+}
+
+void copy_to_host(Engine* e, void* dst, const void* src, uint64_t bytes, void* stream) {
+  CK(cudaSetDevice(e->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+}  // namespace mtcg

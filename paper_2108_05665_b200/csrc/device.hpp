@@ -1,0 +1,57 @@
+// Device executor for a Compiled schedule (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "planner.hpp"
+
+namespace mtcg {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct Engine;  // one per handle (device + stream + counters)
+
+struct DevicePlan {
+  Compiled c;
+  Engine* engine = nullptr;
+  void* d_leaves = nullptr;
+  void* d_arena = nullptr;
+  uint32_t* d_tables = nullptr;
+  uint32_t* d_index = nullptr;
+  uint64_t* d_slice_strides = nullptr;  // per op: S strides for A then B
+  uint32_t* d_row_mult = nullptr;
+  std::vector<uint64_t> op_slice_off;   // word offset of each op's strides
+  uint64_t leaf_root_slice_off = 0;
+  ~DevicePlan();
+};
+
+Engine* engine_create(int device);
+void engine_destroy(Engine* e);
+uint64_t engine_launches(const Engine* e);
+void* engine_stream(Engine* e);
+
+std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c);
+
+// Runs slices [s0, s1) accumulating into d_acc (rows x row_elems elements of
+// the plan precision). accumulate=false: the first slice overwrites.
+void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc,
+                bool accumulate, void* stream);
+
+// Fused |amp|^2 -> linear XEB over all requests (row multiplicities).
+double xeb_device(DevicePlan& dp, const void* d_acc, int n_qubits, void* stream);
+
+// linear_xeb over host probabilities / amplitudes (device reduction).
+double xeb_probs(Engine* e, const double* probs, uint64_t count, int n_qubits,
+                 bool amplitudes);
+
+// Device buffer helpers for the one-shot path.
+void* device_alloc(Engine* e, uint64_t bytes);
+void device_free(Engine* e, void* p);
+void copy_to_host(Engine* e, void* dst, const void* src, uint64_t bytes, void* stream);
+
+}  // namespace mtcg

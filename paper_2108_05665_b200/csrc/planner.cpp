@@ -1,0 +1,624 @@
+// Host compilation of a multi-tensor evaluation (see planner.hpp).
+//
+// Reference behaviour reproduced here (paths under /root/reference/proj):
+//   validation            index_plan plan.cpp:201-259, check_inputs
+//                         multieval.cpp:284-297, slice_spec :332-348,
+//                         check_legs tensor.cpp:31-40
+//   tuple index           build_tuple_index plan.cpp:292-333
+//   contraction shapes    shared_legs multieval.cpp:57-64 (every shared leg
+//                         is closed, :97), contraction_result_legs
+//                         tensor.cpp:100-130
+//   counts                predicted_cost tensor.cpp:132-148, Session
+//                         node_contractions multieval.cpp:258
+//
+// B200-specific choices (not in the reference): every distinct (node, rank)
+// is evaluated once in one batched launch per node (level batching instead of
+// the recursive left/right caches, multieval.cpp:213-274 — the values are
+// pure functions of (node, rank), so results and counts are unchanged);
+// intermediate layouts are chosen per node so the parent contraction reads
+// K-contiguous rows; the HBM arena is planned statically.
+#include "planner.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <numeric>
+
+#include "configs.hpp"
+
+namespace mtcg {
+
+namespace {
+
+std::string fmt(const char* f, long long a = 0, long long b = 0) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, f, a, b);
+  return buf;
+}
+
+struct PlanIdx {
+  std::vector<int> parent, postorder;
+};
+
+// index_plan (plan.cpp:201-259): the plan must be a tree whose leaves are a
+// permutation of the slots.
+PlanIdx index_plan(const mtcg_problem& p) {
+  const int n = p.n_nodes;
+  if (p.root < 0 || p.root >= n) throw DataError("plan has no root");
+  PlanIdx ix;
+  ix.parent.assign(n, -2);
+  std::vector<int> inorder;
+  std::vector<std::pair<int, int>> stack{{p.root, 0}};
+  ix.parent[p.root] = -1;
+  while (!stack.empty()) {
+    auto& [node, phase] = stack.back();
+    if (p.node_slot[node] >= 0) {
+      if (p.node_slot[node] >= p.n_slots)
+        throw DataError(fmt("leaf slot %lld out of range", p.node_slot[node]));
+      inorder.push_back(p.node_slot[node]);
+      ix.postorder.push_back(node);
+      stack.pop_back();
+      continue;
+    }
+    const int l = p.node_left[node], r = p.node_right[node];
+    if (l < 0 || r < 0 || l >= n || r >= n) throw DataError("malformed plan node");
+    if (phase < 2) {
+      const int child = phase == 0 ? l : r;
+      phase += 1;
+      if (ix.parent[child] != -2) throw DataError("plan is not a tree");
+      ix.parent[child] = node;
+      stack.push_back({child, 0});
+    } else {
+      ix.postorder.push_back(node);
+      stack.pop_back();
+    }
+  }
+  std::vector<char> seen(p.n_slots, 0);
+  for (int s : inorder) {
+    if (seen[s]) throw DataError(fmt("slot %lld appears twice in plan", s));
+    seen[s] = 1;
+  }
+  if (static_cast<int>(inorder.size()) != p.n_slots)
+    throw DataError(fmt("plan covers %lld slots, diagram has %lld",
+                        static_cast<long long>(inorder.size()), p.n_slots));
+  return ix;
+}
+
+struct TupleIndex {
+  uint64_t rows = 0;
+  std::vector<uint32_t> row_tuple_first;  // request index representing row
+  std::vector<uint64_t> row_of_request;
+  std::vector<std::vector<uint32_t>> rank;  // [node][row]
+  std::vector<uint32_t> distinct;
+};
+
+// build_tuple_index (plan.cpp:292-333). Rows are the distinct request tuples
+// in lexicographic order; rank[node][row] is the dense rank of the row's
+// restriction to the node's leaves, ordered by (rank_left, rank_right).
+TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
+  TupleIndex ti;
+  const uint64_t k = p.n_requests;
+  const int m = p.n_slots;
+  const uint32_t* T = p.tuples;
+  std::vector<uint64_t> order(k);
+  std::iota(order.begin(), order.end(), 0);
+  auto lex_less = [&](uint64_t a, uint64_t b) {
+    return std::lexicographical_compare(T + a * m, T + a * m + m, T + b * m,
+                                        T + b * m + m);
+  };
+  auto lex_eq = [&](uint64_t a, uint64_t b) {
+    return std::equal(T + a * m, T + a * m + m, T + b * m);
+  };
+  std::stable_sort(order.begin(), order.end(), lex_less);
+  ti.row_of_request.assign(k, 0);
+  for (uint64_t i = 0; i < k; ++i) {
+    if (i == 0 || !lex_eq(order[i - 1], order[i]))
+      ti.row_tuple_first.push_back(static_cast<uint32_t>(order[i]));
+    ti.row_of_request[order[i]] = ti.row_tuple_first.size() - 1;
+  }
+  ti.rows = ti.row_tuple_first.size();
+  const uint64_t rows = ti.rows;
+  ti.rank.assign(p.n_nodes, {});
+  ti.distinct.assign(p.n_nodes, 0);
+  std::vector<uint64_t> keys(rows);
+  std::vector<uint32_t> mark;
+  std::vector<uint64_t> sorted;
+  for (int node : ix.postorder) {
+    std::vector<uint32_t>& rk = ti.rank[node];
+    rk.resize(rows);
+    uint64_t span;  // keys lie in [0, span)
+    if (p.node_slot[node] >= 0) {
+      const int slot = p.node_slot[node];
+      for (uint64_t r = 0; r < rows; ++r)
+        keys[r] = T[static_cast<uint64_t>(ti.row_tuple_first[r]) * m + slot];
+      span = static_cast<uint64_t>(p.slot_n_values[slot]);
+    } else {
+      const auto& rl = ti.rank[p.node_left[node]];
+      const auto& rr = ti.rank[p.node_right[node]];
+      const uint64_t dr = ti.distinct[p.node_right[node]];
+      for (uint64_t r = 0; r < rows; ++r) keys[r] = rl[r] * dr + rr[r];
+      span = ti.distinct[p.node_left[node]] * dr;
+    }
+    // Dense ranks in key order. Keys order like the reference's
+    // (rank_l << 32 | rank_r) since rank_r < distinct[right].
+    uint32_t next = 0;
+    if (span <= 8 * rows + 4096) {
+      mark.assign(span, 0);
+      for (uint64_t r = 0; r < rows; ++r) mark[keys[r]] = 1;
+      for (uint64_t v = 0; v < span; ++v)
+        if (mark[v]) mark[v] = ++next;
+      for (uint64_t r = 0; r < rows; ++r) rk[r] = mark[keys[r]] - 1;
+    } else {
+      sorted = keys;
+      std::sort(sorted.begin(), sorted.end());
+      sorted.erase(std::unique(sorted.begin(), sorted.end()), sorted.end());
+      next = static_cast<uint32_t>(sorted.size());
+      for (uint64_t r = 0; r < rows; ++r)
+        rk[r] = static_cast<uint32_t>(
+            std::lower_bound(sorted.begin(), sorted.end(), keys[r]) - sorted.begin());
+    }
+    ti.distinct[node] = rows == 0 ? 0 : next;
+  }
+  return ti;
+}
+
+bool contains(const std::vector<uint32_t>& v, uint32_t x) {
+  return std::find(v.begin(), v.end(), x) != v.end();
+}
+
+// Stride (elements) of each leg in a row-major layout.
+uint64_t stride_in(const std::vector<uint32_t>& layout, uint32_t leg) {
+  uint64_t s = 1;
+  for (size_t i = layout.size(); i-- > 0;) {
+    if (layout[i] == leg) return s;
+    s <<= 1;
+  }
+  throw InternalError("leg not in layout");
+}
+
+}  // namespace
+
+void SplitTable::build(const std::vector<uint64_t>& strides) {
+  bits = static_cast<int>(strides.size());
+  lo_bits = std::min(bits, 10);
+  const int hi_bits = bits - lo_bits;
+  lo.assign(size_t{1} << lo_bits, 0);
+  hi.assign(size_t{1} << hi_bits, 0);
+  for (uint64_t x = 0; x < lo.size(); ++x) {
+    uint64_t o = 0;
+    for (int b = 0; b < lo_bits; ++b)
+      if (x >> b & 1) o += strides[b];
+    lo[x] = static_cast<uint32_t>(o);
+  }
+  for (uint64_t x = 0; x < hi.size(); ++x) {
+    uint64_t o = 0;
+    for (int b = 0; b < hi_bits; ++b)
+      if (x >> b & 1) o += strides[lo_bits + b];
+    hi[x] = static_cast<uint32_t>(o);
+  }
+}
+
+Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
+                         uint64_t cap_bytes) {
+  Compiled c;
+  c.precision = opt.precision;
+  if (opt.precision != MTCG_C64 && opt.precision != MTCG_C128)
+    throw DataError("unknown precision mode");
+  c.elem_bytes = opt.precision == MTCG_C64 ? 8 : 16;
+  if (p.n_nodes < 0 || p.n_slots < 0 || p.n_sliced < 0 || p.n_batch_legs < 0)
+    throw DataError("negative array length");
+  c.n_nodes = p.n_nodes;
+  c.n_slots = p.n_slots;
+  c.root = p.root;
+
+  // --- check_inputs (multieval.cpp:284-297) --------------------------------
+  const PlanIdx ix = index_plan(p);
+  for (uint64_t i = 0; i < p.n_requests; ++i)
+    for (int j = 0; j < p.n_slots; ++j)
+      if (p.tuples[i * p.n_slots + j] >= static_cast<uint32_t>(p.slot_n_values[j]))
+        throw DataError(fmt("request tuple indexes past slot %lld's value set", j));
+  for (int j = 0; j < p.n_slots; ++j)
+    if (p.slot_n_values[j] < 1)
+      throw DataError(fmt("slot %lld has an empty value set", j));
+
+  if (opt.eval_mode == MTCG_EVAL_ALL && p.n_sliced > 0)
+    throw DataError("plan has sliced legs; use eval_sliced");
+  if (opt.eval_mode == MTCG_EVAL_SLICED && p.n_sliced == 0)
+    throw DataError("plan has no sliced legs; use eval_all");
+
+  // --- slice_spec (multieval.cpp:332-348) ----------------------------------
+  for (int x = 0; x < p.n_sliced; ++x) {
+    const uint32_t l = p.sliced[x];
+    if (l >= p.n_legs) throw DataError(fmt("sliced leg %lld does not exist", l));
+    if (l >= p.n_closed) throw DataError("output legs cannot be sliced");
+    if (contains(c.sliced, l)) throw DataError(fmt("leg %lld sliced twice", l));
+    c.sliced.push_back(l);
+    c.n_slices *= p.leg_dims[l];
+    if (c.n_slices > (1ull << 24))
+      throw DataError("slice list expands to more than 2^24 slices");
+  }
+  const int S = p.n_sliced;
+
+  // --- leaf shapes (check_legs, tensor.cpp:31-40) ---------------------------
+  std::vector<std::vector<uint32_t>> slot_layout(p.n_slots);  // stored legs
+  for (int j = 0; j < p.n_slots; ++j) {
+    for (int i = p.slot_leg_begin[j]; i < p.slot_leg_begin[j + 1]; ++i) {
+      const uint32_t l = p.slot_legs[i];
+      if (l >= p.n_legs) throw DataError("leg id out of range");
+      if (contains(slot_layout[j], l))
+        throw DataError(fmt("malformed tensor: duplicate leg %lld", l));
+      if (p.leg_dims[l] != 2)
+        throw DataError(fmt("leg %lld has bond dimension %lld; this engine "
+                            "evaluates qubit networks (dimension 2)",
+                            l, p.leg_dims[l]));
+      slot_layout[j].push_back(l);
+    }
+    if (slot_layout[j].size() > 32)
+      throw DataError("leaf tensor order above 32 is not supported");
+  }
+  for (uint32_t l : c.sliced)
+    if (p.leg_dims[l] != 2)
+      throw DataError(fmt("leg %lld has bond dimension %lld; this engine "
+                          "evaluates qubit networks (dimension 2)",
+                          l, p.leg_dims[l]));
+
+  // leaf blob: every value tensor as given
+  c.slot_base.resize(p.n_slots);
+  c.slot_item.resize(p.n_slots);
+  uint64_t leaf_elems = 0;
+  for (int j = 0; j < p.n_slots; ++j) {
+    c.slot_base[j] = leaf_elems;
+    c.slot_item[j] = uint64_t{1} << slot_layout[j].size();
+    leaf_elems += c.slot_item[j] * static_cast<uint64_t>(p.slot_n_values[j]);
+  }
+  c.leaf_elems = leaf_elems;
+  c.leaf_values.assign(p.values, p.values + 2 * leaf_elems);
+
+  // --- tuple index ----------------------------------------------------------
+  TupleIndex ti = build_tuple_index(p, ix);
+  c.n_requests = p.n_requests;
+  c.n_rows = ti.rows;
+  c.row_of_request = ti.row_of_request;
+  c.row_mult.assign(ti.rows, 0);
+  for (uint64_t r : ti.row_of_request) c.row_mult[r] += 1;
+
+  // --- logical shapes ----------------------------------------------------------
+  const int n = p.n_nodes;
+  std::vector<std::vector<uint32_t>> legs(n);  // logical legs (sorted for internal)
+  for (int node : ix.postorder) {
+    if (p.node_slot[node] >= 0) {
+      for (uint32_t l : slot_layout[p.node_slot[node]])
+        if (!contains(c.sliced, l)) legs[node].push_back(l);
+      continue;
+    }
+    const auto& L = legs[p.node_left[node]];
+    const auto& R = legs[p.node_right[node]];
+    std::vector<uint32_t> out;
+    for (uint32_t l : L)
+      if (!contains(R, l)) out.push_back(l);
+    for (uint32_t l : R)
+      if (!contains(L, l)) out.push_back(l);
+    std::sort(out.begin(), out.end());
+    if (out.size() > 40) throw DataError("intermediate tensor of order above 40");
+    legs[node] = std::move(out);
+  }
+  c.out_legs = legs[p.root];
+  c.row_elems = uint64_t{1} << c.out_legs.size();
+  if (c.out_legs.size() > 30)
+    throw DataError("request tensors of order above 30 are not supported");
+
+  // --- stored layouts -------------------------------------------------------------
+  // root: ascending (the observable layout); other internal nodes:
+  // [legs kept by the parent][legs the parent closes], each ascending, so the
+  // parent contraction reads K-contiguous rows.
+  std::vector<std::vector<uint32_t>> layout(n);
+  for (int node : ix.postorder) {
+    if (p.node_slot[node] >= 0) {
+      layout[node] = slot_layout[p.node_slot[node]];
+      continue;
+    }
+    const int par = ix.parent[node];
+    if (par < 0) {
+      layout[node] = legs[node];
+      continue;
+    }
+    const int sib = p.node_left[par] == node ? p.node_right[par] : p.node_left[par];
+    std::vector<uint32_t> keep, close;
+    for (uint32_t l : legs[node]) (contains(legs[sib], l) ? close : keep).push_back(l);
+    layout[node] = keep;
+    layout[node].insert(layout[node].end(), close.begin(), close.end());
+  }
+
+  // --- schedule order: post-order, larger-footprint child first -------------------
+  std::vector<uint64_t> table_elems(n, 0), peak(n, 0);
+  for (int node : ix.postorder) {
+    if (p.node_slot[node] >= 0) continue;
+    table_elems[node] = static_cast<uint64_t>(ti.distinct[node]) << legs[node].size();
+  }
+  std::vector<char> left_first(n, 1);
+  for (int node : ix.postorder) {
+    if (p.node_slot[node] >= 0) continue;
+    const int l = p.node_left[node], r = p.node_right[node];
+    const uint64_t sl = table_elems[l], sr = table_elems[r];
+    const uint64_t pl = std::max(peak[l], sl), pr = std::max(peak[r], sr);
+    const uint64_t lf = std::max(pl, sl + pr), rf = std::max(pr, sr + pl);
+    left_first[node] = lf <= rf;
+    peak[node] = std::max(std::min(lf, rf), sl + sr + table_elems[node]);
+  }
+  std::vector<int> sched;  // internal nodes in execution order
+  {
+    std::vector<std::pair<int, int>> st{{p.root, 0}};
+    while (!st.empty()) {
+      auto& [node, ph] = st.back();
+      if (p.node_slot[node] >= 0) {
+        st.pop_back();
+        continue;
+      }
+      const int first = left_first[node] ? p.node_left[node] : p.node_right[node];
+      const int second = left_first[node] ? p.node_right[node] : p.node_left[node];
+      if (ph == 0) {
+        ph = 1;
+        st.push_back({first, 0});
+      } else if (ph == 1) {
+        ph = 2;
+        st.push_back({second, 0});
+      } else {
+        sched.push_back(node);
+        st.pop_back();
+      }
+    }
+  }
+
+  // --- static arena: first-fit over the schedule ---------------------------
+  const uint64_t align = 256 / c.elem_bytes;
+  std::map<uint64_t, uint64_t> free_blocks;  // offset -> length
+  uint64_t arena_top = 0;
+  std::vector<uint64_t> arena_off(n, 0);
+  const uint64_t fixed_bytes =
+      leaf_elems * c.elem_bytes + 2 * c.n_rows * c.row_elems * c.elem_bytes;
+  auto alloc = [&](uint64_t elems, int node) -> uint64_t {
+    elems = (elems + align - 1) / align * align;
+    for (auto it = free_blocks.begin(); it != free_blocks.end(); ++it)
+      if (it->second >= elems) {
+        const uint64_t off = it->first, len = it->second;
+        free_blocks.erase(it);
+        if (len > elems) free_blocks[off + elems] = len - elems;
+        return off;
+      }
+    uint64_t off = arena_top;
+    // extend: merge with a trailing free block
+    if (!free_blocks.empty()) {
+      auto last = std::prev(free_blocks.end());
+      if (last->first + last->second == arena_top) {
+        off = last->first;
+        free_blocks.erase(last);
+      }
+    }
+    arena_top = off + elems;
+    if (cap_bytes && arena_top * c.elem_bytes + fixed_bytes > cap_bytes)
+      throw MemoryCapError(
+          "memory cap exceeded at node " + std::to_string(node) + " (" +
+              std::to_string(arena_top * c.elem_bytes + fixed_bytes) + " > " +
+              std::to_string(cap_bytes) + " bytes)",
+          node);
+    return off;
+  };
+  auto release = [&](uint64_t off, uint64_t elems) {
+    elems = (elems + align - 1) / align * align;
+    auto [it, ok] = free_blocks.emplace(off, elems);
+    (void)ok;
+    auto nx = std::next(it);
+    if (nx != free_blocks.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_blocks.erase(nx);
+    }
+    if (it != free_blocks.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_blocks.erase(it);
+      }
+    }
+  };
+  if (cap_bytes && fixed_bytes > cap_bytes)
+    throw MemoryCapError("memory cap exceeded at node " + std::to_string(p.root) +
+                             " (" + std::to_string(fixed_bytes) + " > " +
+                             std::to_string(cap_bytes) + " bytes)",
+                         p.root);
+
+  // --- ops ------------------------------------------------------------------------
+  c.node_contractions.assign(n, 0);
+  for (int node : sched) {
+    const int l = p.node_left[node], r = p.node_right[node];
+    const auto& L = legs[l];
+    const auto& R = legs[r];
+    std::vector<uint32_t> closed, fl, fr;
+    for (uint32_t x : L) (contains(R, x) ? closed : fl).push_back(x);
+    for (uint32_t x : R)
+      if (!contains(L, x)) fr.push_back(x);
+    std::sort(closed.begin(), closed.end());
+
+    Op op;
+    op.node = node;
+    op.a_is_left = fl.size() >= fr.size();
+    op.child_a = op.a_is_left ? l : r;
+    op.child_b = op.a_is_left ? r : l;
+    const auto& fa_legs = op.a_is_left ? fl : fr;
+    const auto& fb_legs = op.a_is_left ? fr : fl;
+    op.fa = static_cast<int>(fa_legs.size());
+    op.fb = static_cast<int>(fb_legs.size());
+    op.kc = static_cast<int>(closed.size());
+    op.nb = ti.distinct[node];
+    op.root = node == p.root;
+    const auto& out_layout = layout[node];
+
+    // operand sources and per-item entries
+    auto setup_operand = [&](int child, bool& is_leaf, uint64_t& base, uint64_t& item,
+                             std::vector<uint32_t>& idx) {
+      is_leaf = p.node_slot[child] >= 0;
+      idx.resize(op.nb);
+      if (is_leaf) {
+        const int slot = p.node_slot[child];
+        base = c.slot_base[slot];
+        item = c.slot_item[slot];
+      } else {
+        base = arena_off[child];
+        item = uint64_t{1} << legs[child].size();
+      }
+    };
+    setup_operand(op.child_a, op.a_leaf, op.a_base, op.a_item, op.ia);
+    setup_operand(op.child_b, op.b_leaf, op.b_base, op.b_item, op.ib);
+    // entry of each child per distinct rank of this node; a leaf's rank is
+    // the rank of its value index among the rows (ranks == value indices when
+    // every value occurs, which build_assignments guarantees; map explicitly).
+    {
+      const auto& rk = ti.rank[node];
+      const auto& ra = ti.rank[op.child_a];
+      const auto& rb = ti.rank[op.child_b];
+      for (uint64_t row = 0; row < ti.rows; ++row) {
+        const uint32_t b = rk[row];
+        op.ia[b] = ra[row];
+        op.ib[b] = rb[row];
+        if (op.a_leaf)
+          op.ia[b] = p.tuples[static_cast<uint64_t>(ti.row_tuple_first[row]) * p.n_slots +
+                              p.node_slot[op.child_a]];
+        if (op.b_leaf)
+          op.ib[b] = p.tuples[static_cast<uint64_t>(ti.row_tuple_first[row]) * p.n_slots +
+                              p.node_slot[op.child_b]];
+      }
+    }
+    const auto& a_layout = layout[op.child_a];
+    const auto& b_layout = layout[op.child_b];
+    // m / n bit orders: free legs by increasing address in the output layout
+    auto by_out_addr = [&](std::vector<uint32_t> v) {
+      std::sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) {
+        return stride_in(out_layout, x) < stride_in(out_layout, y);
+      });
+      return v;
+    };
+    const std::vector<uint32_t> m_legs = by_out_addr(fa_legs);
+    const std::vector<uint32_t> n_legs = by_out_addr(fb_legs);
+    // k bit order: reference reduction order (ascending ids, row-major):
+    // bit 0 of k is the highest-id closed leg
+    std::vector<uint32_t> k_legs(closed.rbegin(), closed.rend());
+
+    op.config = select_config(op.fa, op.fb);
+    auto strides_of = [&](const std::vector<uint32_t>& space,
+                          const std::vector<uint32_t>& lay) {
+      std::vector<uint64_t> s;
+      for (uint32_t x : space) s.push_back(contains(lay, x) ? stride_in(lay, x) : 0);
+      return s;
+    };
+    if (op.config == kGenericConfig) {
+      // per-output-element kernel: index the stored output directly
+      std::vector<uint32_t> o_legs(out_layout.rbegin(), out_layout.rend());
+      op.tam.build(strides_of(o_legs, a_layout));   // A offset per out index
+      op.tbn.build(strides_of(o_legs, b_layout));   // B offset per out index
+      op.tom.build({});
+      op.ton.build({});
+    } else {
+      op.tam.build(strides_of(m_legs, a_layout));
+      op.tbn.build(strides_of(n_legs, b_layout));
+      op.tom.build(strides_of(m_legs, out_layout));
+      op.ton.build(strides_of(n_legs, out_layout));
+    }
+    op.tak.build(strides_of(k_legs, a_layout));
+    op.tbk.build(strides_of(k_legs, b_layout));
+    op.store_n_fast = out_layout.empty() || contains(fb_legs, out_layout.back());
+
+    // sliced legs carried by leaf operands: offsets per set bit of the slice
+    auto slice_strides = [&](int child, std::vector<uint64_t>& v) {
+      if (p.node_slot[child] < 0 || S == 0) return false;
+      bool any = false;
+      v.assign(S, 0);
+      for (int x = 0; x < S; ++x) {
+        const uint32_t leg = c.sliced[x];
+        if (contains(layout[child], leg)) {
+          v[S - 1 - x] = stride_in(layout[child], leg);  // bit S-1-x of idx
+          any = true;
+        }
+      }
+      return any;
+    };
+    const bool sa = slice_strides(op.child_a, op.a_slice_stride);
+    const bool sb = slice_strides(op.child_b, op.b_slice_stride);
+    if (sa || sb) op.slice_slot = c.n_slice_slots++;
+
+    // exact counts (predicted_cost, tensor.cpp:132-148)
+    const uint64_t d_closed = uint64_t{1} << op.kc;
+    const uint64_t d_open = uint64_t{1} << (op.fa + op.fb);
+    op.mults = d_closed * d_open;
+    op.adds = (d_closed - 1) * d_open;
+    op.rw = (uint64_t{1} << L.size()) + (uint64_t{1} << R.size()) + d_open;
+    c.node_contractions[node] = static_cast<uint64_t>(op.nb) * c.n_slices;
+    c.mults += op.mults * op.nb * c.n_slices;
+    c.adds += op.adds * op.nb * c.n_slices;
+    c.rw += op.rw * op.nb * c.n_slices;
+    c.contractions += static_cast<uint64_t>(op.nb) * c.n_slices;
+
+    // output storage
+    op.out_item = d_open;
+    if (op.root) {
+      op.out_rows.resize(op.nb);
+      const auto& rk = ti.rank[node];
+      for (uint64_t row = 0; row < ti.rows; ++row) op.out_rows[rk[row]] = row;
+    } else if (op.nb > 0) {
+      arena_off[node] = alloc(table_elems[node], node);
+      op.out_base = arena_off[node];
+    }
+    // children are dead once consumed
+    for (int ch : {l, r})
+      if (p.node_slot[ch] < 0 && ti.distinct[ch] > 0)
+        release(arena_off[ch], table_elems[ch]);
+    c.ops.push_back(std::move(op));
+  }
+  c.arena_elems = arena_top;
+
+  if (p.node_slot[p.root] >= 0) {
+    // single-slot network: the root leaf itself is every request's value
+    c.has_leaf_root = true;
+    LeafRoot& lr = c.leaf_root;
+    lr.slot = p.node_slot[p.root];
+    lr.item = c.slot_item[lr.slot];
+    lr.row_value.resize(ti.rows);
+    for (uint64_t row = 0; row < ti.rows; ++row)
+      lr.row_value[row] =
+          p.tuples[static_cast<uint64_t>(ti.row_tuple_first[row]) * p.n_slots + lr.slot];
+    std::vector<uint32_t> o_legs(c.out_legs.rbegin(), c.out_legs.rend());
+    std::vector<uint64_t> st;
+    for (uint32_t x : o_legs) st.push_back(stride_in(slot_layout[lr.slot], x));
+    lr.tout.build(st);
+    if (S > 0) {
+      lr.slice_stride.assign(S, 0);
+      for (int x = 0; x < S; ++x)
+        if (contains(slot_layout[lr.slot], c.sliced[x]))
+          lr.slice_stride[S - 1 - x] = stride_in(slot_layout[lr.slot], c.sliced[x]);
+    }
+  }
+
+  // --- blobs -----------------------------------------------------------------
+  auto put_table = [&](SplitTable& t) {
+    t.dev_off = c.table_blob.size();
+    c.table_blob.insert(c.table_blob.end(), t.lo.begin(), t.lo.end());
+    c.table_blob.insert(c.table_blob.end(), t.hi.begin(), t.hi.end());
+  };
+  auto put_index = [&](const std::vector<uint32_t>& v) {
+    const uint64_t off = c.index_blob.size();
+    c.index_blob.insert(c.index_blob.end(), v.begin(), v.end());
+    return off;
+  };
+  for (Op& op : c.ops) {
+    for (SplitTable* t : {&op.tam, &op.tak, &op.tbn, &op.tbk, &op.tom, &op.ton})
+      put_table(*t);
+    op.ia_off = put_index(op.ia);
+    op.ib_off = put_index(op.ib);
+    op.out_rows_off = put_index(op.out_rows);
+  }
+  if (c.has_leaf_root) {
+    put_table(c.leaf_root.tout);
+    c.leaf_root.rows_off = put_index(c.leaf_root.row_value);
+  }
+  return c;
+}
+
+}  // namespace mtcg

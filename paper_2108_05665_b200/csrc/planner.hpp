@@ -1,0 +1,123 @@
+// Host-side compilation of one multi-tensor evaluation into a static device
+// schedule. Pure C++ (no CUDA): validation, tuple index, per-node shapes and
+// layouts, the batched contraction op list, the static HBM arena plan and the
+// exact operation counts. Citations are to /root/reference/proj.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mtcg.h"
+
+namespace mtcg {
+
+// Exceptions mirror the reference's classes (errors.hpp:26-55); the C ABI
+// maps them to mtcg_status codes.
+struct DataError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct MemoryCapError : std::runtime_error {
+  MemoryCapError(const std::string& w, int node) : std::runtime_error(w), node(node) {}
+  int node;
+};
+struct InternalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Offset table for one bit-permuted index space: offset(x) = lo[x & lo_mask]
+// + hi[x >> lo_bits], element units. Bits of x map to legs; each leg
+// contributes bit * stride (bond dimension 2 everywhere).
+struct SplitTable {
+  int bits = 0;
+  int lo_bits = 0;
+  std::vector<uint32_t> lo, hi;
+  uint64_t dev_off = 0;  // word offset of lo in the plan's table blob
+  void build(const std::vector<uint64_t>& strides);  // strides[bit], LSB first
+};
+
+// One batched pairwise contraction: node `node` for every distinct rank of it
+// (plan.hpp:103-111 `distinct`), out[b] = Σ_c A[ia[b]] B[ib[b]].
+struct Op {
+  int node = -1;
+  int child_a = -1, child_b = -1;  // plan nodes feeding the A (m) / B (n) side
+  bool a_is_left = true;
+  uint32_t nb = 0;                 // batch = distinct[node]
+  int fa = 0, fb = 0, kc = 0;      // log2 M, N, K
+  // operand sources: table base (arena offset or leaf blob offset, elements)
+  bool a_leaf = false, b_leaf = false;
+  uint64_t a_base = 0, b_base = 0;          // element offsets
+  uint64_t a_item = 0, b_item = 0;          // elements per stored entry
+  std::vector<uint32_t> ia, ib;             // per item entry index
+  uint64_t ia_off = 0, ib_off = 0;          // word offsets in the index blob
+  SplitTable tam, tak, tbn, tbk, tom, ton;  // A(m), A(k), B(n), B(k), out(m), out(n)
+  // slice projection of leaf operands: element offset added per set bit of
+  // the slice index (bit j = sliced leg n_sliced-1-j, multieval.cpp:322-329)
+  std::vector<uint64_t> a_slice_stride, b_slice_stride;
+  int slice_slot = -1;             // index into the per-slice offset array
+  // output
+  bool root = false;
+  uint64_t out_base = 0;           // arena element offset (non-root)
+  uint64_t out_item = 0;           // elements per output entry
+  bool store_n_fast = true;        // epilogue lane order
+  std::vector<uint32_t> out_rows;  // root: item -> accumulator row
+  uint64_t out_rows_off = 0;
+  int config = 0;                  // kernel tile configuration
+  // exact algorithmic counts per slice (tensor.cpp:132-148)
+  uint64_t mults = 0, adds = 0, rw = 0;
+};
+
+// A plan whose root is a leaf (single-slot network): copy/accumulate the
+// projected leaf tensors into the accumulator.
+struct LeafRoot {
+  int slot = -1;
+  std::vector<uint32_t> row_value;   // row -> value index
+  uint64_t item = 0;                 // stored elements per value
+  SplitTable tout;                   // out index -> offset in the value
+  std::vector<uint64_t> slice_stride;
+  uint64_t rows_off = 0;
+};
+
+struct Compiled {
+  // inputs (copied)
+  int precision = MTCG_C64;
+  int n_nodes = 0, n_slots = 0, root = -1;
+  std::vector<uint32_t> sliced;
+  uint64_t n_slices = 1;
+  uint64_t n_requests = 0, n_rows = 0;
+  uint64_t row_elems = 1;
+  std::vector<uint32_t> out_legs;      // legs of every request tensor
+  std::vector<uint64_t> row_of_request;
+  std::vector<uint32_t> row_mult;      // requests per row (XEB weights)
+  // leaves: all value sets, stored as given (incl. sliced legs)
+  std::vector<uint64_t> slot_base;     // element offset of slot j's values
+  std::vector<uint64_t> slot_item;     // elements per value tensor
+  uint64_t leaf_elems = 0;
+  std::vector<double> leaf_values;     // complex128 interleaved (host copy)
+  // schedule
+  std::vector<Op> ops;
+  bool has_leaf_root = false;
+  LeafRoot leaf_root;
+  std::vector<uint32_t> table_blob;    // all SplitTables
+  std::vector<uint32_t> index_blob;    // ia/ib/out_rows arrays
+  uint64_t arena_elems = 0;            // per-slice intermediate arena
+  int elem_bytes = 8;
+  // counts (whole evaluation)
+  std::vector<uint64_t> node_contractions;
+  uint64_t mults = 0, adds = 0, rw = 0, contractions = 0;
+  int n_slice_slots = 0;               // ops/leaf root needing slice offsets
+
+  uint64_t arena_bytes() const { return arena_elems * elem_bytes; }
+  uint64_t resident_bytes() const {
+    return leaf_elems * elem_bytes + 4 * (table_blob.size() + index_blob.size());
+  }
+};
+
+// Validates `p` with the reference's checks and messages, builds the tuple
+// index and the schedule. cap_bytes = 0: no cap. Throws DataError /
+// MemoryCapError.
+Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
+                         uint64_t cap_bytes);
+
+}  // namespace mtcg

@@ -1,0 +1,295 @@
+"""Python face of the B200 engine, mirroring the reference's hot-path API.
+
+    eval_all(plan, d, as, opts)      multieval.hpp:62-63
+    eval_sliced(plan, d, as, opts)   multieval.hpp:69-70
+    emulate(plan, d, as, opts)       multieval.hpp:74-75 (host-side, exact counts)
+    linear_xeb(n, probs)             xeb.hpp:38
+    probs_from_amplitudes(amps)      xeb.hpp:42-43
+
+Every call crosses the C ABI of ``libmtcg.so`` (include/mtcg.h); there is no
+CPU fallback. `Engine` additionally exposes the staged API (compile once, run
+slice ranges into a device accumulator, fetch / fused XEB) used by the bench
+and the multi-GPU slice scheduler.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi as A
+from ._lib import lib
+from .errors import DataError, EngineError, MemoryCapError
+from .network import AssignmentSet, NetworkDiagram, Plan, Tensor
+
+PRECISIONS = {"c64": A.MTCG_C64, "c128": A.MTCG_C128}
+
+
+@dataclass
+class EvalOptions:
+    """EvalOptions (multieval.hpp:26-29) plus the device precision."""
+
+    memory_cap_bytes: int = 0
+    workers: int = 1
+    precision: str = "c64"
+
+
+@dataclass
+class OpCounters:
+    mults: int = 0
+    adds: int = 0
+    rw: int = 0
+
+
+@dataclass
+class EvalResult:
+    """EvalResult (multieval.hpp:36-41). `values[i]` is request i's tensor;
+    `amplitudes` is the same data as an (n_requests, 2^w) array."""
+
+    values: List[Tensor]
+    counters: OpCounters
+    peak_bytes: int
+    node_contractions: np.ndarray
+    amplitudes: np.ndarray = field(repr=False, default=None)
+
+
+@dataclass
+class EmulateResult:
+    counters: OpCounters
+    peak_bytes: int
+    node_contractions: np.ndarray
+    contractions: int = 0
+
+
+def _raise(status: int, err: C.Array, cap_node: int = -1):
+    msg = err.value.decode(errors="replace")
+    if status == A.MTCG_ERR_DATA:
+        raise DataError(msg)
+    if status == A.MTCG_ERR_MEMORY_CAP:
+        raise MemoryCapError(msg, cap_node)
+    raise EngineError(f"mtcg status {status}: {msg}")
+
+
+def problem_arrays(plan: Plan, d: NetworkDiagram, assignments: AssignmentSet) -> A.ProblemArrays:
+    """Pack the reference-shaped inputs into the C ABI's POD arrays."""
+    vs = [(s[0].legs, np.stack([t.data for t in s])) for s in assignments.value_sets]
+    nodes = list(zip(plan.left, plan.right, plan.slot))
+    return A.ProblemArrays.build(nodes, plan.root, plan.sliced, d.n_closed, d.leg_dims, vs,
+                                 assignments.tuples, assignments.batch_legs)
+
+
+def _options(mode: int, opts: Optional[EvalOptions]) -> A.mtcg_options:
+    opts = opts or EvalOptions()
+    o = A.mtcg_options()
+    o.eval_mode = mode
+    if opts.precision not in PRECISIONS:
+        raise DataError(f"unknown precision '{opts.precision}'")
+    o.precision = PRECISIONS[opts.precision]
+    o.memory_cap_bytes = int(opts.memory_cap_bytes)
+    o.workers = int(opts.workers)
+    return o
+
+
+class CompiledProblem:
+    """A problem compiled and resident on one device (mtcg_compile)."""
+
+    def __init__(self, engine: "Engine", handle: C.c_void_p, problem: A.ProblemArrays):
+        self.engine = engine
+        self.h = handle
+        self.problem = problem
+        info = A.mtcg_plan_info()
+        lib().mtcg_plan_get_info(self.h, C.byref(info))
+        self.info = info
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().mtcg_plan_destroy(self.h)
+            self.h = None
+
+    @property
+    def n_slices(self) -> int:
+        return int(self.info.n_slices)
+
+    @property
+    def complex_dtype_bytes(self) -> int:
+        return 8 if self.info.precision == A.MTCG_C64 else 16
+
+    def new_accumulator(self, device=None):
+        """A zeroed torch device buffer for mtcg_run: (rows, 2^w, 2) reals."""
+        import torch
+
+        dt = torch.float32 if self.info.precision == A.MTCG_C64 else torch.float64
+        dev = device if device is not None else torch.device("cuda", self.engine.device)
+        return torch.zeros((max(int(self.info.n_rows), 1), int(self.info.row_elems), 2),
+                           dtype=dt, device=dev)
+
+    def run(self, slice_begin: int, slice_end: int, acc_ptr: int, accumulate: bool = False,
+            stream: int = 0) -> None:
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_run(self.h, slice_begin, slice_end, C.c_void_p(acc_ptr),
+                            int(accumulate), C.c_void_p(stream or None), err, 1024)
+        if st:
+            _raise(st, err)
+
+    def fetch(self, acc_ptr: int, stream: int = 0, node_contractions: bool = True):
+        p = self.problem
+        w = int(self.info.row_elems)
+        vals = np.zeros(2 * p.n_requests * w, dtype=np.float64)
+        nc = np.zeros(max(p.n_nodes, 1), dtype=np.uint64)
+        res = A.mtcg_result()
+        res.values = vals.ctypes.data_as(C.POINTER(C.c_double))
+        res.values_capacity = p.n_requests * w
+        res.node_contractions = nc.ctypes.data_as(C.POINTER(C.c_uint64)) if node_contractions else None
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_fetch(self.h, C.c_void_p(acc_ptr), C.c_void_p(stream or None),
+                              C.byref(res), err, 1024)
+        if st:
+            _raise(st, err)
+        return _result_from(res, vals, nc[:p.n_nodes], p.n_requests, w)
+
+    def xeb(self, acc_ptr: int, n_qubits: int, stream: int = 0) -> float:
+        out = C.c_double()
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_xeb_device(self.h, C.c_void_p(acc_ptr), n_qubits,
+                                   C.c_void_p(stream or None), C.byref(out), err, 1024)
+        if st:
+            _raise(st, err)
+        return out.value
+
+
+def _result_from(res: A.mtcg_result, vals: np.ndarray, nc: np.ndarray, n_req: int,
+                 w: int) -> EvalResult:
+    amps = vals.view(np.complex128).reshape(n_req, w)
+    legs = [int(res.out_legs[i]) for i in range(res.n_out_legs)]
+    values = [Tensor(list(legs), amps[i]) for i in range(n_req)]
+    return EvalResult(values, OpCounters(int(res.mults), int(res.adds), int(res.rw)),
+                      int(res.hbm_peak_bytes), nc.copy(), amps)
+
+
+class Engine:
+    """An mtcg handle bound to one CUDA device."""
+
+    def __init__(self, device: int = 0, hbm_cap_bytes: int = 0):
+        self.device = device
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_create(device, hbm_cap_bytes, C.byref(h), err, 1024)
+        if st:
+            _raise(st, err)
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().mtcg_destroy(self.h)
+            self.h = None
+
+    @property
+    def launches(self) -> int:
+        return int(lib().mtcg_launch_count(self.h))
+
+    def eval(self, problem: A.ProblemArrays, mode: int = A.MTCG_EVAL_AUTO,
+             opts: Optional[EvalOptions] = None) -> EvalResult:
+        o = _options(mode, opts)
+        w = problem.row_elems
+        vals = np.zeros(2 * problem.n_requests * w, dtype=np.float64)
+        nc = np.zeros(max(problem.n_nodes, 1), dtype=np.uint64)
+        res = A.mtcg_result()
+        res.values = vals.ctypes.data_as(C.POINTER(C.c_double))
+        res.values_capacity = problem.n_requests * w
+        res.node_contractions = nc.ctypes.data_as(C.POINTER(C.c_uint64))
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_eval(self.h, C.byref(problem.struct()), C.byref(o), C.byref(res),
+                             err, 1024)
+        if st:
+            _raise(st, err, res.cap_node)
+        return _result_from(res, vals, nc[:problem.n_nodes], problem.n_requests, w)
+
+    def compile(self, problem: A.ProblemArrays, mode: int = A.MTCG_EVAL_AUTO,
+                opts: Optional[EvalOptions] = None) -> CompiledProblem:
+        o = _options(mode, opts)
+        h = C.c_void_p()
+        cap_node = C.c_int32(-1)
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_compile(self.h, C.byref(problem.struct()), C.byref(o), C.byref(h),
+                                C.byref(cap_node), err, 1024)
+        if st:
+            _raise(st, err, cap_node.value)
+        return CompiledProblem(self, h, problem)
+
+    def linear_xeb(self, n: int, probs) -> float:
+        p = np.ascontiguousarray(probs, dtype=np.float64)
+        out = C.c_double()
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_linear_xeb(self.h, n, p.ctypes.data_as(C.POINTER(C.c_double)),
+                                   p.size, C.byref(out), err, 1024)
+        if st:
+            _raise(st, err)
+        return out.value
+
+    def linear_xeb_amplitudes(self, n: int, amps) -> float:
+        a = np.ascontiguousarray(np.asarray(amps, dtype=np.complex128).ravel())
+        out = C.c_double()
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_linear_xeb_amplitudes(
+            self.h, n, a.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), a.size,
+            C.byref(out), err, 1024)
+        if st:
+            _raise(st, err)
+        return out.value
+
+
+_default: Optional[Engine] = None
+
+
+def default_engine() -> Engine:
+    global _default
+    if _default is None:
+        _default = Engine(0)
+    return _default
+
+
+def eval_all(plan: Plan, d: NetworkDiagram, assignments: AssignmentSet,
+             opts: Optional[EvalOptions] = None) -> EvalResult:
+    return default_engine().eval(problem_arrays(plan, d, assignments), A.MTCG_EVAL_ALL, opts)
+
+
+def eval_sliced(plan: Plan, d: NetworkDiagram, assignments: AssignmentSet,
+                opts: Optional[EvalOptions] = None) -> EvalResult:
+    return default_engine().eval(problem_arrays(plan, d, assignments), A.MTCG_EVAL_SLICED, opts)
+
+
+def emulate_arrays(problem: A.ProblemArrays, opts: Optional[EvalOptions] = None,
+                   mode: int = A.MTCG_EVAL_AUTO) -> EmulateResult:
+    """Host-only schedule construction with exact counts (mtcg_emulate)."""
+    o = _options(mode, opts)
+    info = A.mtcg_plan_info()
+    nc = np.zeros(max(problem.n_nodes, 1), dtype=np.uint64)
+    cap_node = C.c_int32(-1)
+    err = C.create_string_buffer(1024)
+    st = lib().mtcg_emulate(C.byref(problem.struct()), C.byref(o),
+                            int((opts or EvalOptions()).memory_cap_bytes), C.byref(info),
+                            nc.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(cap_node),
+                            err, 1024)
+    if st:
+        _raise(st, err, cap_node.value)
+    return EmulateResult(OpCounters(int(info.mults), int(info.adds), int(info.rw)),
+                         int(info.hbm_arena_bytes + info.hbm_resident_bytes),
+                         nc[:problem.n_nodes].copy(), int(info.contractions))
+
+
+def emulate(plan: Plan, d: NetworkDiagram, assignments: AssignmentSet,
+            opts: Optional[EvalOptions] = None) -> EmulateResult:
+    return emulate_arrays(problem_arrays(plan, d, assignments), opts)
+
+
+def probs_from_amplitudes(amps) -> np.ndarray:
+    """|a|^2 per amplitude (xeb.cpp:67-73) — host helper."""
+    a = np.asarray(amps, dtype=np.complex128)
+    return a.real * a.real + a.imag * a.imag
+
+
+def linear_xeb(n: int, probs: Sequence[float]) -> float:
+    """linear_xeb (xeb.cpp:43-50) reduced on the device."""
+    return default_engine().linear_xeb(n, probs)
