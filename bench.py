@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""Throughput of the multi-amplitude XEB hot path on B200 (BASELINE.json).
+
+Workload (BASELINE.json configs[1], "cfg2"): synthetic 30-qubit 5x6 grid,
+m=12 (grid_circuit seed 12345, fused), 10^4 uniformly random bitstrings
+(seed 99), the reference-annealed plan plans/cfg2.plan with 4 sliced legs
+(16 slices). One step = every slice of the whole evaluation + the slice sum
+(+ one NCCL reduce when N>1) + the fused |amp|^2 -> linear-XEB reduction.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W]           # this engine
+    python bench.py --impl reference [...]                        # reference CPU
+
+N>1 runs under torchrun: one process per GPU, slices split into contiguous
+blocks, partial amplitudes summed by one NCCL reduce to rank 0.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("amplitudes/sec and effective TFLOP/s (complex64) for batched XEB at "
+          "1/2/4/8 B200")
+WORKLOADS = {
+    "cfg1": dict(rows=3, cols=4, layers=8, k=1000,
+                 text="cfg1: synthetic 12-qubit 3x4 grid, m=8 (grid_circuit seed 12345, "
+                      "fused), 1000 random bitstrings (seed 99), plans/cfg1.plan (no slicing)"),
+    "cfg2": dict(rows=5, cols=6, layers=12, k=10000,
+                 text="cfg2: synthetic 30-qubit 5x6 grid, m=12 (grid_circuit seed 12345, "
+                      "fused), 10^4 random bitstrings (seed 99), plans/cfg2.plan "
+                      "(4 sliced legs, 16 slices)"),
+}
+
+
+def load_workload(name: str):
+    from paper_2108_05665_b200 import network as N
+    from paper_2108_05665_b200.engine import problem_arrays
+
+    w = WORKLOADS[name]
+    c = N.grid_circuit(w["rows"], w["cols"], w["layers"], 12345)
+    bits = N.random_bitstrings(N.Rng(99), w["rows"] * w["cols"], w["k"])
+    d = N.to_diagram(c, True)
+    asg = N.build_assignments(d, bits, [])
+    plan_text = open(os.path.join(ROOT, "plans", f"{name}.plan")).read()
+    plan = N.parse_plan(plan_text)
+    return problem_arrays(plan, d, asg), c, bits, plan_text
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(problem, circ, bits, plan_text, threads: int):
+    """Reference CPU path on this host: bounded sample of the same workload.
+
+    oracle/_ref (the unmodified reference library): its contract_pair is
+    timed on every node shape of the plan (sub-blocks above 2^24 MACs, scaled
+    linearly) and weighted by the exact per-node evaluation counts ->
+    single-thread time of eval_sliced; eval_sliced runs slices on `threads`
+    workers, so T = T1 / min(threads, S). Returns the dict for the JSON line.
+    """
+    from oracle import refimpl
+
+    from paper_2108_05665_b200 import network as N
+
+    S = 1 << len(problem.sliced)
+    if refimpl.available():
+        p = refimpl.RefProblem(N.format_circuit(circ), bits, plan_text, fuse=True)
+        est1, wall, frac = p.sample_eval_time(1 << 24, threads)
+        kind = "reference"
+    else:
+        est1, wall, frac = port_sample_eval_time(problem, threads)
+        kind = "port"
+    t = est1 / min(threads, S)
+    k = problem.n_requests
+    return {
+        "value": k / t, "unit": "amplitudes/s", "cores": min(threads, S), "kind": kind,
+        "sample": (f"contract_pair (tensor.cpp:150-253, ~94% of eval time) timed on all "
+                   f"{sum(1 for s in problem.node_slot if s < 0)} node shapes of the plan "
+                   f"({frac * 100:.2f}% of per-slice MACs executed, larger nodes on projected "
+                   f"sub-blocks scaled linearly), weighted by exact per-node counts x {S} "
+                   f"slices; eval_sliced with {min(threads, S)} workers; sampling took "
+                   f"{wall:.1f}s on {threads} threads"),
+        "est_seconds_full_eval": t,
+        "est_seconds_1thread": est1,
+    }
+
+
+def port_sample_eval_time(problem, threads):
+    """Same sampling with the C restatement (oracle/liboracle.so) when the
+    reference build is absent."""
+    import ctypes as C
+
+    from oracle import oracle as O
+    from paper_2108_05665_b200.engine import emulate_arrays
+
+    em = emulate_arrays(problem)
+    L = O.lib()
+    sl = set(int(x) for x in problem.sliced)
+    legs = {}
+    n = problem.n_nodes
+    order = []
+
+    def visit(x):
+        if problem.node_slot[x] >= 0:
+            j = int(problem.node_slot[x])
+            legs[x] = [int(l) for l in problem.slot_legs[problem.slot_leg_begin[j]:
+                                                         problem.slot_leg_begin[j + 1]]
+                       if int(l) not in sl]
+            return
+        visit(int(problem.node_left[x]))
+        visit(int(problem.node_right[x]))
+        a, b = legs[int(problem.node_left[x])], legs[int(problem.node_right[x])]
+        legs[x] = sorted(set(a) ^ set(b))
+        order.append(x)
+
+    visit(int(problem.root))
+    rng = np.random.default_rng(0)
+    total, t0 = 0.0, time.time()
+    for x in order:
+        if em.node_contractions[x] == 0:
+            continue
+        a = list(legs[int(problem.node_left[x])])
+        b = list(legs[int(problem.node_right[x])])
+        closed = sorted(set(a) & set(b))
+        scale = 1.0
+        while (1 << (len(set(a) ^ set(b)) + len(closed))) > (1 << 24):
+            big = a if len(a) >= len(b) else b
+            free = [l for l in big if l not in closed]
+            if not free:
+                break
+            big.remove(free[0])
+            scale *= 2
+        da = (rng.random(2 << len(a)) - 0.5)
+        db = (rng.random(2 << len(b)) - 0.5)
+        nr = len(set(a) ^ set(b))
+        out = np.zeros(2 << nr)
+        ol, od = np.zeros(64, np.uint32), np.zeros(64, np.uint32)
+        u32 = lambda v: np.array(v, dtype=np.uint32)
+        aa, bb, cc = u32(a), u32(b), u32(closed)
+        dims_a, dims_b = u32([2] * len(a)), u32([2] * len(b))
+        P = lambda arr, ct: arr.ctypes.data_as(C.POINTER(ct))
+        s = time.perf_counter()
+        L.orc_contract_pair(len(a), P(aa, C.c_uint32), P(dims_a, C.c_uint32), P(da, C.c_double),
+                            len(b), P(bb, C.c_uint32), P(dims_b, C.c_uint32), P(db, C.c_double),
+                            len(closed), P(cc, C.c_uint32), P(ol, C.c_uint32), P(od, C.c_uint32),
+                            P(out, C.c_double), None)
+        total += (time.perf_counter() - s) * scale * float(em.node_contractions[x])
+    return total, time.time() - t0, float("nan")
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    problem, circ, bits, plan_text = load_workload(args.config)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_baseline(problem, circ, bits, plan_text, threads)
+    times, base = [], None
+    for _ in range(args.steps):
+        base = cpu_baseline(problem, circ, bits, plan_text, threads)
+        times.append(base["est_seconds_full_eval"])
+    t = statistics.mean(times)
+    k = problem.n_requests
+    from paper_2108_05665_b200.engine import emulate_arrays
+
+    mults = emulate_arrays(problem).counters.mults
+    value = k / t
+    line = {
+        "metric": METRIC, "value": value, "unit": "amplitudes/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config]["text"], "n_qubits": circ.n_qubits,
+                   "bitstrings": k, "slices": 1 << len(problem.sliced)},
+        "effective_tflops": 8 * mults / t / 1e12,
+        "cpu_baseline": {key: base[key] for key in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": value, "unit": "amplitudes/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
+    """Time every op of one slice with CUDA events on the launching stream;
+    report the op with the largest device time as the dominant kernel."""
+    import ctypes as C
+
+    from paper_2108_05665_b200 import _abi as A
+    from paper_2108_05665_b200._lib import lib
+
+    L = lib()
+    L.mtcg_plan_op_count.argtypes = [C.c_void_p]
+    L.mtcg_plan_op_count.restype = C.c_int32
+    n = L.mtcg_plan_op_count(cp.h)
+    ms = (C.c_float * n)()
+    err = C.create_string_buffer(512)
+    L.mtcg_time_ops.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p,
+                                C.POINTER(C.c_float), C.c_char_p, C.c_size_t]
+    rc = L.mtcg_time_ops(cp.h, 0, C.c_void_p(acc.data_ptr()), 0, C.c_void_p(stream), ms, err, 512)
+    if rc:
+        raise RuntimeError(err.value.decode())
+
+    class OpInfo(C.Structure):
+        _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
+                    ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
+                    ("mults", C.c_uint64), ("bytes", C.c_uint64)]
+
+    L.mtcg_plan_op_info.argtypes = [C.c_void_p, C.c_int32, C.POINTER(OpInfo)]
+    ops = []
+    for i in range(n):
+        oi = OpInfo()
+        L.mtcg_plan_op_info(cp.h, i, C.byref(oi))
+        ops.append((float(ms[i]), oi))
+    slice_ms = sum(m for m, _ in ops)
+    top_ms, top = max(ops, key=lambda t: t[0])
+    flops = 8.0 * top.mults
+    intensity = flops / max(top.bytes, 1)
+    ridge = tensor_tflops * 1e12 / (hbm_gbs * 1e9)
+    if intensity >= ridge:
+        achieved = flops / (top_ms * 1e-3) / 1e12
+        bound, peak, unit = "tensor", tensor_tflops, "TFLOP/s"
+    else:
+        achieved = top.bytes / (top_ms * 1e-3) / 1e9
+        bound, peak, unit = "hbm", hbm_gbs, "GB/s"
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(f"node{top.node}")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    return {
+        "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+        "frac": achieved / peak, "traffic": traffic,
+        "kernel": (f"node {top.node}: M=2^{top.fa} N=2^{top.fb} K=2^{top.kc} x{top.batch} "
+                   f"(tile config {top.kernel})"),
+        "launch_ms": top_ms, "share_of_slice": top_ms / slice_ms if slice_ms else None,
+        "per_launch_flops": flops, "per_launch_bytes": int(top.bytes),
+        "peak_source": f"{peak_src} ({'bf16 dense' if bound == 'tensor' else 'copy'})",
+        "slice_ms_serialised": slice_ms,
+    }
+
+
+def run_engine(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2108_05665_b200.engine import Engine, EvalOptions
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    problem, circ, bits, plan_text = load_workload(args.config)
+    n_qubits = circ.n_qubits
+    eng = Engine(local)
+    opts = EvalOptions(precision=args.precision)
+    cp = eng.compile(problem, 0, opts)
+    S = cp.n_slices
+    s0, s1 = S * rank // world, S * (rank + 1) // world
+    stream = torch.cuda.current_stream().cuda_stream
+    acc = cp.new_accumulator()
+
+    def step():
+        cp.run(s0, s1, acc.data_ptr(), accumulate=False, stream=stream)
+        if world > 1:
+            dist.reduce(acc, dst=0)
+        if rank == 0:
+            return cp.xeb(acc.data_ptr(), n_qubits, stream=stream)
+        return None
+
+    for _ in range(max(args.warmup, 0)):
+        xeb = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = eng.launches
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for _ in range(args.steps):
+            xeb = step()
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = eng.launches - launches0
+    t_ms = start.elapsed_time(end)
+    t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    ms_per_step = t_ms / args.steps
+    k = problem.n_requests
+    value = k * args.steps / (t_ms * 1e-3)
+    mults = int(cp.info.mults)
+
+    # ---- end to end through the public API: host inputs -> device -> host ----
+    def e2e_step():
+        cpe = eng.compile(problem, 0, opts)
+        acc_e = cpe.new_accumulator()
+        cpe.run(s0, s1, acc_e.data_ptr(), accumulate=False, stream=stream)
+        if world > 1:
+            dist.reduce(acc_e, dst=0)
+        if rank == 0:
+            r = cpe.fetch(acc_e.data_ptr(), stream=stream, node_contractions=False)
+            eng.linear_xeb_amplitudes(n_qubits, r.amplitudes)
+        torch.cuda.synchronize()
+
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = k * e2e_steps / float(te.item())
+    # H2D: leaves (plan precision) + offset tables + index arrays, then the
+    # host amplitudes for linear_xeb; D2H: the accumulator + XEB partials.
+    h2d = int(cp.info.hbm_resident_bytes + k * cp.info.row_elems * 16)
+    d2h = int(cp.info.n_rows * cp.info.row_elems * cp.complex_dtype_bytes + 2 * 8 * 592)
+
+    if rank == 0:
+        hbm, tflops, src = measured_peaks()
+        roof = roofline_for(cp, acc, stream, ms_per_step, hbm, tflops, src)
+        base = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                base = cpu_baseline(problem, circ, bits, plan_text, os.cpu_count() or 1)
+                base = {key: base[key] for key in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as e:  # noqa: BLE001
+                base = {"value": None, "unit": "amplitudes/s", "cores": 0, "kind": "reference",
+                        "sample": f"unavailable: {e}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "amplitudes/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config]["text"], "n_qubits": n_qubits,
+                       "bitstrings": k, "slices": S, "slices_per_gpu": f"{s1 - s0}",
+                       "parallelism": f"slices/{world}" + (" + 1 NCCL reduce" if world > 1 else ""),
+                       "l2": (f"per-slice working set {cp.info.hbm_arena_bytes / 1e9:.2f} GB "
+                              "> 126 MB L2 (no flush needed)")},
+            "effective_tflops": 8 * mults * args.steps / (t_ms * 1e-3) / 1e12,
+            "xeb": xeb,
+            "roofline": roof,
+            "cpu_baseline": base,
+            "e2e": {"value": e2e_value, "unit": "amplitudes/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "includes": "host planning + tuple index, H2D leaves/tables, all slices, "
+                                "D2H amplitudes + fan-out, XEB"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mtcg", choices=["mtcg", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_engine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

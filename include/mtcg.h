@@ -225,6 +225,27 @@ mtcg_status mtcg_emulate(const mtcg_problem* p, const mtcg_options* opt,
                          uint64_t* node_contractions, int32_t* cap_node,
                          char* err, size_t errlen);
 
+/* Per-op introspection of a compiled schedule (one op = one batched launch
+ * per slice). */
+typedef struct mtcg_op_info {
+  int32_t node;          /* plan node */
+  int32_t kernel;        /* tile configuration (0 = per-element kernel) */
+  int32_t fa, fb, kc;    /* log2 of M, N, K */
+  uint32_t batch;        /* distinct evaluations of the node per slice */
+  uint64_t mults;        /* algorithmic complex MACs per slice */
+  uint64_t bytes;        /* algorithmic HBM bytes per slice: |A|+|B|+|out|
+                            per item x element size (predicted_cost rw) */
+} mtcg_op_info;
+int32_t mtcg_plan_op_count(const mtcg_plan* plan);
+mtcg_status mtcg_plan_op_info(const mtcg_plan* plan, int32_t i, mtcg_op_info* info);
+
+/* Runs slice `slice` once with a CUDA event pair around every op launch
+ * (on `stream`) and writes each op's device time in milliseconds to
+ * op_ms[mtcg_plan_op_count]. Accumulates into d_acc like mtcg_run. */
+mtcg_status mtcg_time_ops(mtcg_plan* plan, uint64_t slice, void* d_acc,
+                          int accumulate, void* stream, float* op_ms,
+                          char* err, size_t errlen);
+
 /* Count of device kernel launches issued by this process through the
  * library since mtcg_create (evidence for the bench's gpu_launches). */
 uint64_t mtcg_launch_count(const mtcg_handle* h);

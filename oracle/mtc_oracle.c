@@ -434,6 +434,18 @@ int orc_eval(const mtcg_problem* p, int mode, double* out_values,
              uint64_t values_capacity, uint64_t* node_contractions,
              uint64_t* counters, int32_t* out_legs, int32_t* n_out_legs,
              char* err, size_t errlen) {
+  return orc_eval_slices(p, mode, 0, UINT64_MAX, out_values, values_capacity,
+                         node_contractions, counters, out_legs, n_out_legs, err,
+                         errlen);
+}
+
+/* The slice fold restricted to slices [s_begin, min(s_end, S)): the partial
+ * sum one rank of a slice-sharded run owns. */
+int orc_eval_slices(const mtcg_problem* p, int mode, uint64_t s_begin,
+                    uint64_t s_end, double* out_values,
+                    uint64_t values_capacity, uint64_t* node_contractions,
+                    uint64_t* counters, int32_t* out_legs, int32_t* n_out_legs,
+                    char* err, size_t errlen) {
   plan_index ix;
   int rc = index_plan(p, &ix, err, errlen); /* check_inputs :284-297 */
   if (rc) {
@@ -503,7 +515,11 @@ int orc_eval(const mtcg_problem* p, int mode, double* out_values,
 
   otensor* by_row = (otensor*)calloc(ti.rows + 1, sizeof(otensor));
   uint32_t vals[MAXR];
-  for (uint64_t s = 0; s < n_slices && !rc; ++s) {
+  if (s_end > n_slices) s_end = n_slices;
+  if (s_begin >= s_end && ti.rows > 0) {
+    rc = fail(err, errlen, MTCG_ERR_ARGUMENT, "empty slice range");
+  }
+  for (uint64_t s = s_begin; s < s_end && !rc; ++s) {
     /* values_of (multieval.cpp:322-329): mixed radix, last leg fastest */
     uint64_t idx = s;
     for (int x = p->n_sliced; x-- > 0;) {
@@ -544,7 +560,7 @@ int orc_eval(const mtcg_problem* p, int mode, double* out_values,
         break;
       }
       /* fold in slice-index order (multieval.cpp:498-513) */
-      if (s == 0) {
+      if (s == s_begin) {
         by_row[r] = *v;
         by_row[r].data = (double*)malloc(sizeof(double) * 2 * v->size);
         by_row[r].owned = 1;

@@ -34,6 +34,13 @@ int orc_eval(const mtcg_problem* p, int mode, double* out_values,
              uint64_t* counters, int32_t* out_legs, int32_t* n_out_legs,
              char* err, size_t errlen);
 
+/* Same, folding only slices [s_begin, min(s_end, S)) (a rank's partial). */
+int orc_eval_slices(const mtcg_problem* p, int mode, uint64_t s_begin,
+                    uint64_t s_end, double* out_values,
+                    uint64_t values_capacity, uint64_t* node_contractions,
+                    uint64_t* counters, int32_t* out_legs, int32_t* n_out_legs,
+                    char* err, size_t errlen);
+
 /* One pairwise contraction with the reference kernel's exact reduction
  * order (contract_pair, tensor.cpp:150-253). Legs are ids; dims all given.
  * out_legs receives the result legs (ascending); returns their count or -1

@@ -39,14 +39,17 @@ def lib():
         u64p, dp, i32p = C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.POINTER(C.c_int32)
         L.orc_eval.argtypes = [C.POINTER(mtcg_problem), C.c_int, dp, C.c_uint64, u64p,
                                u64p, i32p, i32p, C.c_char_p, C.c_size_t]
+        L.orc_eval_slices.argtypes = [C.POINTER(mtcg_problem), C.c_int, C.c_uint64,
+                                      C.c_uint64, dp, C.c_uint64, u64p, u64p, i32p, i32p,
+                                      C.c_char_p, C.c_size_t]
         L.orc_linear_xeb.argtypes = [C.c_int, dp, C.c_uint64, dp, C.c_char_p, C.c_size_t]
         _lib = L
     return _lib
 
 
-def eval_problem(p: ProblemArrays, mode: int = 0):
+def eval_problem(p: ProblemArrays, mode: int = 0, slices=None):
     """-> (values[n_requests, 2^w] complex128, node_contractions, (mults, adds, rw),
-    out_legs)."""
+    out_legs). slices=(s0, s1) folds only that slice range."""
     w = p.row_elems
     vals = np.zeros(2 * p.n_requests * w, dtype=np.float64)
     nc = np.zeros(max(p.n_nodes, 1), dtype=np.uint64)
@@ -54,7 +57,8 @@ def eval_problem(p: ProblemArrays, mode: int = 0):
     legs = np.zeros(64, dtype=np.int32)
     nlegs = C.c_int32(0)
     err = C.create_string_buffer(512)
-    rc = lib().orc_eval(C.byref(p.struct()), mode,
+    s0, s1 = slices if slices is not None else (0, 2 ** 64 - 1)
+    rc = lib().orc_eval_slices(C.byref(p.struct()), mode, s0, s1,
                         vals.ctypes.data_as(C.POINTER(C.c_double)), p.n_requests * w,
                         nc.ctypes.data_as(C.POINTER(C.c_uint64)),
                         cnt.ctypes.data_as(C.POINTER(C.c_uint64)),

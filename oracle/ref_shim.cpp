@@ -19,6 +19,8 @@
 // Nothing here is on the product path and nothing here is shipped.
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -445,6 +447,124 @@ int ref_add_slices_greedy(void* h, int n, std::uint64_t k, std::uint64_t m_max,
       cp.add_slice(best_leg);
     }
     p->plan = cp.plan();
+    return 0;
+  } catch (...) {
+    return classify(std::current_exception(), nullptr);
+  }
+}
+
+// Bounded-sample timing of the reference engine's hot loop on this problem.
+//
+// For every internal plan node the reference's own contract_pair
+// (tensor.cpp:150-253, ~94% of eval time) is run on random operands with
+// the node's real leg lists (slice-projected leaves, contraction_result_legs
+// intermediates, every shared leg closed as multieval.cpp:97 does). Nodes
+// costing more than `budget` complex MACs are sampled on a sub-block: free
+// legs of the larger operand are projected away (project_leg) until the
+// contraction fits — contract_pair's cost per output element is d_closed
+// multiply-adds whatever d_open is, so time scales linearly by the
+// projected-away factor. Returns the single-thread-equivalent time of the
+// whole evaluation, Σ_n distinct[n] · S · t_n, plus the sampling wall time.
+// Nodes are sampled concurrently on `threads` std::threads (the per-core
+// rate under a loaded socket, as eval_sliced's workers see it).
+int ref_sample_eval_time(void* h, std::uint64_t budget, int threads,
+                         double* est_seconds_1thread, double* sample_wall,
+                         double* sampled_fraction) {
+  auto* p = static_cast<Problem*>(h);
+  try {
+    TupleIndex ti = build_tuple_index(p->plan, p->as);
+    PlanIndex ix = index_plan(p->plan, p->d.slot_count());
+    std::uint64_t slices = 1;
+    for (LegId l : p->plan.sliced) slices *= p->d.leg_dims[l];
+    const std::size_t n = p->plan.nodes.size();
+    std::vector<std::vector<Leg>> legs(n);
+    std::vector<int> work;
+    for (int node : ix.postorder) {
+      const Plan::Node& nd = p->plan.nodes[node];
+      if (nd.leaf()) {
+        for (const Leg& l : p->as.value_sets[nd.slot].front().legs())
+          if (std::find(p->plan.sliced.begin(), p->plan.sliced.end(), l.id) ==
+              p->plan.sliced.end())
+            legs[node].push_back(l);
+        continue;
+      }
+      std::vector<LegId> closed;
+      for (const Leg& a : legs[nd.left])
+        for (const Leg& b : legs[nd.right])
+          if (a.id == b.id) closed.push_back(a.id);
+      legs[node] = contraction_result_legs(legs[nd.left], legs[nd.right], closed);
+      if (ti.distinct[node] > 0) work.push_back(node);
+    }
+    std::vector<double> node_time(n, 0.0);
+    std::vector<double> node_frac(n, 1.0);
+    std::atomic<std::size_t> next{0};
+    auto worker = [&](int w) {
+      Rng rng(0x5eed + w);
+      for (std::size_t i = next++; i < work.size(); i = next++) {
+        const int node = work[i];
+        const Plan::Node& nd = p->plan.nodes[node];
+        std::vector<Leg> la = legs[nd.left], lb = legs[nd.right];
+        std::vector<LegId> closed;
+        for (const Leg& a : la)
+          for (const Leg& b : lb)
+            if (a.id == b.id) closed.push_back(a.id);
+        auto is_closed = [&](LegId id) {
+          return std::find(closed.begin(), closed.end(), id) != closed.end();
+        };
+        auto size_of = [](const std::vector<Leg>& v) {
+          std::uint64_t s = 1;
+          for (const Leg& l : v) s *= l.dim;
+          return s;
+        };
+        PairCost full = predicted_cost(la, lb, closed);
+        PairCost pc = full;
+        double scale = 1.0;
+        while (pc.mults > budget) {
+          std::vector<Leg>& big = size_of(la) >= size_of(lb) ? la : lb;
+          auto it = std::find_if(big.begin(), big.end(),
+                                 [&](const Leg& l) { return !is_closed(l.id); });
+          if (it == big.end()) break;
+          scale *= it->dim;
+          big.erase(it);
+          pc = predicted_cost(la, lb, closed);
+        }
+        auto random_tensor = [&](const std::vector<Leg>& v) {
+          std::vector<Complex> data(size_of(v));
+          for (Complex& c : data) c = {rng.uniform_real01() - 0.5, rng.uniform_real01() - 0.5};
+          return Tensor(v, std::move(data));
+        };
+        Tensor a = random_tensor(la), b = random_tensor(lb);
+        double best = 1e300;
+        for (int rep = 0; rep < 2; ++rep) {
+          auto t0 = std::chrono::steady_clock::now();
+          Tensor r = contract_pair(a, b, closed);
+          double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          best = std::min(best, dt);
+          if (dt > 0.05) break;  // large samples: one timing is enough
+        }
+        node_time[node] = best * scale;
+        node_frac[node] = 1.0 / scale;
+      }
+    };
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int w = 0; w < std::max(1, threads); ++w) pool.emplace_back(worker, w);
+    for (auto& t : pool) t.join();
+    *sample_wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double total = 0.0, full_mults = 0.0, sampled_mults = 0.0;
+    for (int node : work) {
+      total += static_cast<double>(ti.distinct[node]) * slices * node_time[node];
+      const Plan::Node& nd = p->plan.nodes[node];
+      std::vector<LegId> closed;
+      for (const Leg& a : legs[nd.left])
+        for (const Leg& b : legs[nd.right])
+          if (a.id == b.id) closed.push_back(a.id);
+      const double m = static_cast<double>(predicted_cost(legs[nd.left], legs[nd.right], closed).mults);
+      full_mults += m;
+      sampled_mults += m * node_frac[node];
+    }
+    *est_seconds_1thread = total;
+    if (sampled_fraction) *sampled_fraction = full_mults > 0 ? sampled_mults / full_mults : 1.0;
     return 0;
   } catch (...) {
     return classify(std::current_exception(), nullptr);

@@ -78,6 +78,7 @@ def lib():
                                  C.c_uint32, dp]
         L.ref_add_slices_greedy.argtypes = [vp, C.c_int, C.c_uint64, C.c_uint64,
                                             C.c_int]
+        L.ref_sample_eval_time.argtypes = [vp, C.c_uint64, C.c_int, dp, dp, dp]
         L.ref_statevector.argtypes = [C.c_char_p, C.c_char_p, dp]
         L.ref_linear_xeb.argtypes = [C.c_int, dp, C.c_uint64, dp]
         L.ref_xeb_from_amplitudes.argtypes = [C.c_int, dp, C.c_uint64, dp]
@@ -281,6 +282,16 @@ class RefProblem:
         j = lambda x: (int(x[0]) << 64) | int(x[1])
         return {"mults": j(m), "adds": j(a), "rw": j(r),
                 "k_t": kt[:n_nodes], "size": sz[:n_nodes]}
+
+    def sample_eval_time(self, budget: int = 1 << 24, threads: int = 1):
+        """-> (single-thread-equivalent seconds of the full evaluation,
+        sampling wall seconds, fraction of per-slice MACs actually executed)."""
+        est, wall, frac = C.c_double(), C.c_double(), C.c_double()
+        rc = lib().ref_sample_eval_time(self.h, budget, threads, C.byref(est),
+                                        C.byref(wall), C.byref(frac))
+        if rc:
+            raise RefError(rc, lib().ref_last_error().decode())
+        return est.value, wall.value, frac.value
 
     def add_slices_greedy(self, n: int, k: int, m_max: int = 8 << 30,
                           criterion: str = "cost") -> None:

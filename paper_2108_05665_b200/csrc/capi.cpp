@@ -269,6 +269,35 @@ mtcg_status mtcg_linear_xeb_amplitudes(mtcg_handle* h, int n_qubits, const doubl
   });
 }
 
+int32_t mtcg_plan_op_count(const mtcg_plan* plan) {
+  return plan ? static_cast<int32_t>(plan->dp->c.ops.size()) : 0;
+}
+
+mtcg_status mtcg_plan_op_info(const mtcg_plan* plan, int32_t i, mtcg_op_info* info) {
+  if (!plan || !info || i < 0 || i >= static_cast<int32_t>(plan->dp->c.ops.size()))
+    return MTCG_ERR_ARGUMENT;
+  const Compiled& c = plan->dp->c;
+  const Op& op = c.ops[i];
+  info->node = op.node;
+  info->kernel = op.config;
+  info->fa = op.fa;
+  info->fb = op.fb;
+  info->kc = op.kc;
+  info->batch = op.nb;
+  info->mults = op.mults * op.nb;
+  info->bytes = op.rw * op.nb * static_cast<uint64_t>(c.elem_bytes);
+  return MTCG_OK;
+}
+
+mtcg_status mtcg_time_ops(mtcg_plan* plan, uint64_t slice, void* d_acc, int accumulate,
+                          void* stream, float* op_ms, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!plan || !op_ms) throw DataError("null argument");
+    if (slice >= plan->dp->c.n_slices) throw DataError("slice out of range");
+    time_ops(*plan->dp, slice, d_acc, accumulate != 0, stream, op_ms);
+  });
+}
+
 uint64_t mtcg_launch_count(const mtcg_handle* h) { return h ? engine_launches(h->engine) : 0; }
 
 }  // extern "C"

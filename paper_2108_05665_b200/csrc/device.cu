@@ -420,7 +420,7 @@ uint64_t slice_offset(const std::vector<uint64_t>& strides, uint64_t s) {
 
 template <class R>
 void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
-                  cudaStream_t st) {
+                  cudaStream_t st, cudaEvent_t* op_events = nullptr) {
   using T = typename V2<R>::T;
   Compiled& c = dp.c;
   T* arena = static_cast<T*>(dp.d_arena);
@@ -428,8 +428,10 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
   T* acc = static_cast<T*>(d_acc);
   for (uint64_t s = s0; s < s1; ++s) {
     const int acc_flag = (accumulate || s > s0) ? 1 : 0;
-    for (const Op& op : c.ops) {
+    for (size_t oi = 0; oi < c.ops.size(); ++oi) {
+      const Op& op = c.ops[oi];
       if (op.nb == 0) continue;
+      if (op_events) CK(cudaEventRecord(op_events[2 * oi], st));
       DevOp<T> d;
       d.a = op.a_leaf ? leaves + op.a_base : arena + op.a_base;
       d.b = op.b_leaf ? leaves + op.b_base : arena + op.b_base;
@@ -456,6 +458,7 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
       d.accumulate = op.root ? acc_flag : 0;
       launch_op<R>(d, op.config, st);
       dp.engine->launches++;
+      if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
     }
     if (c.has_leaf_root && c.n_rows > 0) {
       const LeafRoot& lr = c.leaf_root;
@@ -544,6 +547,25 @@ void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accu
     run_slices_t<float>(dp, s0, s1, d_acc, accumulate, st);
   else
     run_slices_t<double>(dp, s0, s1, d_acc, accumulate, st);
+}
+
+void time_ops(DevicePlan& dp, uint64_t slice, void* d_acc, bool accumulate, void* stream,
+              float* op_ms) {
+  CK(cudaSetDevice(dp.engine->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
+  const size_t n = dp.c.ops.size();
+  std::vector<cudaEvent_t> ev(2 * n);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  if (dp.c.precision == MTCG_C64)
+    run_slices_t<float>(dp, slice, slice + 1, d_acc, accumulate, st, ev.data());
+  else
+    run_slices_t<double>(dp, slice, slice + 1, d_acc, accumulate, st, ev.data());
+  CK(cudaStreamSynchronize(st));
+  for (size_t i = 0; i < n; ++i) {
+    op_ms[i] = 0.f;
+    if (dp.c.ops[i].nb) CK(cudaEventElapsedTime(&op_ms[i], ev[2 * i], ev[2 * i + 1]));
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
 }
 
 double xeb_device(DevicePlan& dp, const void* d_acc, int n_qubits, void* stream) {

@@ -42,6 +42,11 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c);
 void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc,
                 bool accumulate, void* stream);
 
+// Same as run_slices for one slice, with an event pair around each op;
+// op_ms[i] receives op i's device time (ops with batch 0 get 0).
+void time_ops(DevicePlan& dp, uint64_t slice, void* d_acc, bool accumulate, void* stream,
+              float* op_ms);
+
 // Fused |amp|^2 -> linear XEB over all requests (row multiplicities).
 double xeb_device(DevicePlan& dp, const void* d_acc, int n_qubits, void* stream);
 

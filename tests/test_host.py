@@ -1,0 +1,111 @@
+"""Host side of the C ABI, no GPU: the library loads and exports every symbol
+include/mtcg.h declares; mtcg_emulate (validation + tuple index + schedule)
+reproduces the reference's counts, node_contractions and error behaviour."""
+import ctypes as C
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2108_05665_b200 import _abi as A
+from paper_2108_05665_b200._lib import EXPORTS, LIB_PATH, lib
+from paper_2108_05665_b200.engine import EvalOptions, emulate_arrays
+from paper_2108_05665_b200.errors import DataError, MemoryCapError
+
+from .helpers import ROOT, random_instance, workload
+from .test_oracle import CASES, MODES, problem_of
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    L = lib()
+    header = open(os.path.join(ROOT, "include", "mtcg.h")).read()
+    declared = set(re.findall(r"\b(mtcg_[a-z_]+)\s*\(", header))
+    assert declared, "no declarations parsed"
+    for sym in sorted(declared):
+        assert hasattr(L, sym), sym
+    assert set(EXPORTS) <= declared | {"mtcg_version"}
+    assert L.mtcg_version() == 1
+
+
+def test_library_is_an_in_tree_sm100a_build():
+    import subprocess
+
+    assert LIB_PATH.startswith(ROOT)
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("case", [c for c in CASES["cases"]], ids=lambda c: c["name"])
+def test_emulate_matches_reference_counts_and_errors(case):
+    try:
+        p, _ = problem_of(case)
+    except Exception:  # noqa: BLE001
+        assert case["status"] != 0
+        return
+    if case["status"]:
+        with pytest.raises(DataError) as ei:
+            emulate_arrays(p, mode=MODES[case["mode"]])
+        assert str(ei.value) == case["message"]
+        return
+    em = emulate_arrays(p, mode=MODES[case["mode"]])
+    assert [int(x) for x in em.node_contractions] == case["node_contractions"]
+    assert [em.counters.mults, em.counters.adds, em.counters.rw] == case["counters"]
+
+
+def test_emulate_cfg2_counts_match_reference_totals():
+    # exact-mode CostedPlan totals of the bench workload (769,600
+    # contractions, 1.585e12 complex MACs with the survey's annealed plan)
+    p, _, _ = workload("cfg2")
+    em = emulate_arrays(p)
+    assert em.contractions == 769600
+    assert em.counters.mults == 1584552545792  # CostedPlan exact total_mults
+    golden = os.path.join(ROOT, "tests", "golden", "cfg2_reference.npz")
+    if os.path.exists(golden):
+        g = np.load(golden)
+        assert np.array_equal(em.node_contractions, g["node_contractions"])
+        assert (em.counters.mults, em.counters.adds, em.counters.rw) == tuple(int(x) for x in g["counters"])
+
+
+def test_memory_cap_names_a_node():
+    p, _, _ = random_instance(0)
+    with pytest.raises(MemoryCapError) as ei:
+        emulate_arrays(p, EvalOptions(memory_cap_bytes=64))
+    assert "memory cap exceeded at node" in str(ei.value)
+    assert 0 <= ei.value.node < p.n_nodes
+
+
+def test_unsupported_bond_dimension_is_a_data_error():
+    p, _, _ = random_instance(2)
+    dims = np.array(p.leg_dims)
+    dims[0] = 3
+    q = A.ProblemArrays(p.node_left, p.node_right, p.node_slot, p.root, p.sliced, p.n_closed,
+                        dims, p.slot_n_values, p.slot_leg_begin, p.slot_legs, p.values,
+                        p.tuples, p.batch_legs)
+    with pytest.raises(DataError, match="bond dimension"):
+        emulate_arrays(q)
+
+
+def test_request_tuple_out_of_range():
+    p, _, _ = random_instance(4)
+    t = p.tuples.copy()
+    t[0, 0] = 99
+    q = A.ProblemArrays(p.node_left, p.node_right, p.node_slot, p.root, p.sliced, p.n_closed,
+                        p.leg_dims, p.slot_n_values, p.slot_leg_begin, p.slot_legs, p.values,
+                        t, p.batch_legs)
+    with pytest.raises(DataError, match="indexes past slot 0's value set"):
+        emulate_arrays(q)
+
+
+def test_device_entry_points_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2108_05665_b200.engine import Engine
+    from paper_2108_05665_b200.errors import EngineError
+
+    with pytest.raises(EngineError):
+        Engine(0)

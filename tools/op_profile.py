@@ -1,0 +1,79 @@
+"""Per-op device-time table of one slice (CUDA events around every launch).
+
+    python tools/op_profile.py [--config cfg2] [--precision c64] [--top 40]
+
+Prints one row per op sorted by time: node, shape (log2 M/N/K), batch, kernel
+config, ms, achieved GB/s over the algorithmic bytes and TFLOP/s over the
+algorithmic flops. Writes gpurun_out/op_profile.json when that dir exists.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import load_workload  # noqa: E402
+
+
+class OpInfo(C.Structure):
+    _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
+                ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
+                ("mults", C.c_uint64), ("bytes", C.c_uint64)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--precision", default="c64")
+    ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--slice", type=int, default=0)
+    a = ap.parse_args()
+    import torch
+
+    from paper_2108_05665_b200._lib import lib
+    from paper_2108_05665_b200.engine import Engine, EvalOptions
+
+    problem, circ, bits, _ = load_workload(a.config)
+    eng = Engine(0)
+    cp = eng.compile(problem, 0, EvalOptions(precision=a.precision))
+    acc = cp.new_accumulator()
+    L = lib()
+    L.mtcg_plan_op_count.argtypes = [C.c_void_p]
+    L.mtcg_plan_op_count.restype = C.c_int32
+    L.mtcg_time_ops.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_int, C.c_void_p,
+                                C.POINTER(C.c_float), C.c_char_p, C.c_size_t]
+    L.mtcg_plan_op_info.argtypes = [C.c_void_p, C.c_int32, C.POINTER(OpInfo)]
+    n = L.mtcg_plan_op_count(cp.h)
+    ms = (C.c_float * n)()
+    err = C.create_string_buffer(512)
+    stream = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):  # warm
+        L.mtcg_time_ops(cp.h, a.slice, C.c_void_p(acc.data_ptr()), 0, C.c_void_p(stream), ms, err, 512)
+    rows = []
+    for i in range(n):
+        oi = OpInfo()
+        L.mtcg_plan_op_info(cp.h, i, C.byref(oi))
+        t = float(ms[i])
+        rows.append(dict(op=i, node=oi.node, fa=oi.fa, fb=oi.fb, kc=oi.kc, batch=oi.batch,
+                         kernel=oi.kernel, ms=t, bytes=int(oi.bytes), flops=8 * int(oi.mults),
+                         gbs=oi.bytes / (t * 1e-3) / 1e9 if t else 0.0,
+                         tflops=8 * oi.mults / (t * 1e-3) / 1e12 if t else 0.0))
+    total = sum(r["ms"] for r in rows)
+    rows.sort(key=lambda r: -r["ms"])
+    print(f"slice {a.slice}: {n} ops, {total:.3f} ms serialised")
+    print(f"{'node':>5} {'M':>3} {'N':>3} {'K':>3} {'batch':>6} {'cfg':>3} {'ms':>8} "
+          f"{'share':>6} {'GB/s':>8} {'TF/s':>7}")
+    for r in rows[:a.top]:
+        print(f"{r['node']:>5} {r['fa']:>3} {r['fb']:>3} {r['kc']:>3} {r['batch']:>6} "
+              f"{r['kernel']:>3} {r['ms']:>8.3f} {r['ms'] / total:>6.1%} {r['gbs']:>8.0f} "
+              f"{r['tflops']:>7.2f}")
+    if os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        with open(os.path.join(ROOT, "gpurun_out", "op_profile.json"), "w") as f:
+            json.dump({"total_ms": total, "ops": rows}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
