@@ -118,8 +118,11 @@ typedef struct mtcg_options {
   int32_t workers;            /* EvalOptions.workers (accepted; the device
                                  runs slices itself — results never depend on
                                  it, multieval.hpp:66-68) */
-  int32_t reserved;
+  int32_t flags;              /* MTCG_FLAG_* */
 } mtcg_options;
+
+/* mtcg_options.flags */
+#define MTCG_FLAG_NO_TENSOR_CORES 1 /* dense ops on the CUDA-core kernels */
 
 /* eval outputs. `values` is a caller buffer of values_capacity complex
  * elements receiving, request-major, each request's tensor (order-0, or

@@ -61,7 +61,7 @@ class mtcg_options(C.Structure):
         ("precision", C.c_int32),
         ("memory_cap_bytes", C.c_uint64),
         ("workers", C.c_int32),
-        ("reserved", C.c_int32),
+        ("flags", C.c_int32),
     ]
 
 

@@ -30,8 +30,14 @@ constexpr TileConfig kTileConfigs[kNumTileConfigs] = {
 constexpr int kTileK64 = 16;
 constexpr int kTileK128 = 8;
 
-inline int select_config(int fa, int fb) {
+// Row-streaming kernel for skinny ops (N <= 8, K <= 32, M >= 256).
+constexpr int kRowsConfig = 11;
+// tcgen05 3xTF32 complex GEMM (dense ops, complex64 only; tc_gemm.cu).
+constexpr int kTcConfig = 12;
+
+inline int select_config(int fa, int fb, int kc = 0) {
   // fa >= fb by construction (A is the side with more free legs).
+  if (fb <= 4 && fa >= 8 && kc <= 5) return kRowsConfig;
   if (fa + fb < 8) return kGenericConfig;
   const int M = fa, N = fb;  // log2
   if (M >= 7) {

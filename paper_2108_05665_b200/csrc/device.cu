@@ -29,6 +29,7 @@
 
 #include "configs.hpp"
 #include "device.hpp"
+#include "tc_gemm.hpp"
 
 namespace mtcg {
 
@@ -123,6 +124,8 @@ struct DevOp {
   int fa, fb, kc;
   int n_fast;               // epilogue lane order
   int accumulate;           // root: add into the accumulator
+  int a_kcontig;            // rows kernel: A rows K-contiguous
+  int o_ncontig;            // rows kernel: output n contiguous
 };
 
 // ---- tiled batched contraction -------------------------------------------------
@@ -228,6 +231,86 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
       if (cidx >= n_valid) continue;
       T* dst = O + omo[r] + ono[cidx];
       *dst = op.accumulate ? cadd(*dst, acc[i][j]) : acc[i][j];
+    }
+  }
+}
+
+// ---- skinny contractions: stream A rows, B resident in shared memory -----------
+//
+// For N <= 8 the op is a stream over A (M rows of K contiguous elements) and
+// the output (M x N): HBM-bound. One thread per row (RPT rows per thread,
+// strided by the block so every load/store instruction is warp-coalesced),
+// the whole K x N block of B broadcast from shared memory, rows read with
+// 16-byte vector loads when K-contiguous, outputs written as one vector run
+// when the N legs are the output's lowest bits.
+
+template <class T>
+struct Vec4 {
+  using type = float4;
+};
+template <>
+struct Vec4<double2> {
+  using type = double4;
+};
+
+template <class R, int K, int N, int RPT>
+__global__ void __launch_bounds__(256)
+    contract_rows(const DevOp<typename V2<R>::T> op) {
+  using T = typename V2<R>::T;
+  __shared__ T Bs[K * N];
+  __shared__ uint32_t kao[K];
+  __shared__ uint32_t ono[N];
+  const uint64_t item = blockIdx.y + uint64_t{gridDim.y} * blockIdx.z;
+  if (item >= op.nb) return;
+  const T* A = op.a + uint64_t{op.ia ? __ldg(op.ia + item) : (uint32_t)item} * op.a_item + op.a_slice;
+  const T* B = op.b + uint64_t{op.ib ? __ldg(op.ib + item) : (uint32_t)item} * op.b_item + op.b_slice;
+  T* O = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + item)} : item) * op.out_item;
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int k = e / N, n = e - k * N;
+    Bs[e] = B[op.tbn(n) + op.tbk(k)];
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) kao[k] = op.tak(k);
+  for (int n = threadIdx.x; n < N; n += blockDim.x) ono[n] = op.ton(n);
+  __syncthreads();
+  const uint64_t M = uint64_t{1} << op.fa;
+  const uint64_t base = uint64_t{blockIdx.x} * (256 * RPT) + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const uint64_t m = base + j * 256;
+    if (m >= M) break;
+    T av[K];
+    const T* row = A + op.tam(m);
+    if (K >= 2 && op.a_kcontig) {
+      using V4 = typename Vec4<T>::type;
+#pragma unroll
+      for (int k = 0; k < K; k += 2) {
+        const V4 v = *reinterpret_cast<const V4*>(row + k);
+        av[k] = T{v.x, v.y};
+        av[k + 1] = T{v.z, v.w};
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) av[k] = row[kao[k]];
+    }
+    T acc[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) acc[n] = czero<T>();
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int n = 0; n < N; ++n) cmac(acc[n], av[k], Bs[k * N + n], k == 0);
+    T* dst = O + op.tom(m);
+    if (N >= 2 && op.o_ncontig && !op.accumulate) {
+      using V4 = typename Vec4<T>::type;
+#pragma unroll
+      for (int n = 0; n < N; n += 2)
+        *reinterpret_cast<V4*>(dst + n) = V4{acc[n].x, acc[n].y, acc[n + 1].x, acc[n + 1].y};
+    } else {
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        T* d = dst + ono[n];
+        *d = op.accumulate ? cadd(*d, acc[n]) : acc[n];
+      }
     }
   }
 }
@@ -382,9 +465,43 @@ void launch_tile(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
   kern<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy)), NT, smem, st>>>(op);
 }
 
+template <class R, int K, int N>
+void launch_rows_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
+  constexpr int RPT = 2;
+  const uint64_t M = uint64_t{1} << op.fa;
+  const unsigned gx = static_cast<unsigned>((M + 256 * RPT - 1) / (256 * RPT));
+  const unsigned gy = std::min<uint32_t>(op.nb, 65535u);
+  const unsigned gz = (op.nb + gy - 1) / gy;
+  contract_rows<R, K, N, RPT><<<dim3(gx, gy, gz), 256, 0, st>>>(op);
+}
+
+template <class R, int K>
+void launch_rows_k(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
+  switch (op.fb) {
+    case 0: return launch_rows_kn<R, K, 1>(op, st);
+    case 1: return launch_rows_kn<R, K, 2>(op, st);
+    case 2: return launch_rows_kn<R, K, 4>(op, st);
+    case 3: return launch_rows_kn<R, K, 8>(op, st);
+    default: return launch_rows_kn<R, K, 16>(op, st);
+  }
+}
+
+template <class R>
+void launch_rows(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
+  switch (op.kc) {
+    case 0: return launch_rows_k<R, 1>(op, st);
+    case 1: return launch_rows_k<R, 2>(op, st);
+    case 2: return launch_rows_k<R, 4>(op, st);
+    case 3: return launch_rows_k<R, 8>(op, st);
+    case 4: return launch_rows_k<R, 16>(op, st);
+    default: return launch_rows_k<R, 32>(op, st);
+  }
+}
+
 template <class R>
 void launch_op(const DevOp<typename V2<R>::T>& op, int config, cudaStream_t st) {
   switch (config) {
+    case kRowsConfig: return launch_rows<R>(op, st);
     case 1: return launch_tile<R, 128, 64, 8, 4>(op, st);
     case 2: return launch_tile<R, 128, 32, 8, 2>(op, st);
     case 3: return launch_tile<R, 128, 16, 4, 2>(op, st);
@@ -455,7 +572,50 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
       d.fb = op.fb;
       d.kc = op.kc;
       d.n_fast = op.store_n_fast ? 1 : 0;
+      d.a_kcontig = op.a_kcontig ? 1 : 0;
+      d.o_ncontig = op.o_ncontig ? 1 : 0;
       d.accumulate = op.root ? acc_flag : 0;
+      if constexpr (sizeof(R) == 4) {
+        if (op.config == kTcConfig) {
+          TcOp t;
+          t.fa = op.fa;
+          t.fb = op.fb;
+          t.kc = op.kc;
+          t.nb = op.nb;
+          t.a_entries = op.a_entries;
+          t.a = reinterpret_cast<float*>(arena + op.a_base);
+          t.a_lo = reinterpret_cast<float*>(arena + op.scratch_off);
+          t.ia = d.ia;
+          t.b = reinterpret_cast<const float2*>(d.b);
+          t.b_item = op.b_item;
+          t.b_slice = d.b_slice;
+          t.ib = d.ib;
+          t.tbn_lo = d.tbn.lo;
+          t.tbn_hi = d.tbn.hi;
+          t.tbn_bits = d.tbn.lo_bits;
+          t.tbk_lo = d.tbk.lo;
+          t.tbk_hi = d.tbk.hi;
+          t.tbk_bits = d.tbk.lo_bits;
+          const uint64_t a_lo_elems = op.a_entries << (op.fa + op.kc);
+          const uint64_t bhat_elems = uint64_t{op.nb} << (op.fb + op.kc + 1);
+          t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off + a_lo_elems);
+          t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + a_lo_elems + bhat_elems);
+          t.out = reinterpret_cast<float2*>(d.out);
+          t.out_rows = d.out_rows;
+          t.out_item = op.out_item;
+          t.tom_lo = d.tom.lo;
+          t.tom_hi = d.tom.hi;
+          t.tom_bits = d.tom.lo_bits;
+          t.ton_lo = d.ton.lo;
+          t.ton_hi = d.ton.hi;
+          t.ton_bits = d.ton.lo_bits;
+          t.accumulate = d.accumulate;
+          tc_contract(t, st);
+          dp.engine->launches += 3;
+          if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
+          continue;
+        }
+      }
       launch_op<R>(d, op.config, st);
       dp.engine->launches++;
       if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));

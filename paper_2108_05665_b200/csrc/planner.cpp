@@ -20,6 +20,7 @@
 #include "planner.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -496,13 +497,32 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       });
       return v;
     };
-    const std::vector<uint32_t> m_legs = by_out_addr(fa_legs);
+    op.config = select_config(op.fa, op.fb, op.kc);
+    // Tensor-core path (complex64 only): dense, K-contiguous intermediate A,
+    // shapes the 128 x (2N) x (2K) real tiles cover exactly.
+    // Only compute-bound ops: intensity MNK / (MK + NK + MN) >= 32 complex MACs
+    // per element moved (HBM-bound skinny ops stay on the streaming kernels,
+    // which move 5x fewer bytes than the split + GEMM path).
+    const double Md = std::ldexp(1.0, op.fa), Nd = std::ldexp(1.0, op.fb),
+                 Kd = std::ldexp(1.0, op.kc);
+    const double intensity = Md * Nd * Kd / (Md * Kd + Nd * Kd + Md * Nd);
+    const bool tc_ok = c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) &&
+                       !op.a_leaf && op.fa >= 7 && op.fb >= 3 && op.kc >= 4 &&
+                       intensity >= 32.0 &&
+                       (uint64_t{op.nb} << (op.fa + op.fb + op.kc)) >= (uint64_t{1} << 26);
+    if (tc_ok) op.config = kTcConfig;
+    // m / n bit orders: free legs by increasing address in the output layout;
+    // the tensor-core path walks A rows in A's memory order instead (TMA rows)
+    std::vector<uint32_t> m_legs = by_out_addr(fa_legs);
+    if (op.config == kTcConfig)
+      std::sort(m_legs.begin(), m_legs.end(), [&](uint32_t x, uint32_t y) {
+        return stride_in(layout[op.child_a], x) < stride_in(layout[op.child_a], y);
+      });
     const std::vector<uint32_t> n_legs = by_out_addr(fb_legs);
     // k bit order: reference reduction order (ascending ids, row-major):
     // bit 0 of k is the highest-id closed leg
     std::vector<uint32_t> k_legs(closed.rbegin(), closed.rend());
 
-    op.config = select_config(op.fa, op.fb);
     auto strides_of = [&](const std::vector<uint32_t>& space,
                           const std::vector<uint32_t>& lay) {
       std::vector<uint64_t> s;
@@ -525,6 +545,14 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     op.tak.build(strides_of(k_legs, a_layout));
     op.tbk.build(strides_of(k_legs, b_layout));
     op.store_n_fast = out_layout.empty() || contains(fb_legs, out_layout.back());
+    {
+      const auto ks = strides_of(k_legs, a_layout);
+      op.a_kcontig = !op.a_leaf;
+      for (size_t b = 0; b < ks.size(); ++b) op.a_kcontig &= ks[b] == (uint64_t{1} << b);
+      const auto ns = strides_of(n_legs, out_layout);
+      op.o_ncontig = op.config != kGenericConfig;
+      for (size_t b = 0; b < ns.size(); ++b) op.o_ncontig &= ns[b] == (uint64_t{1} << b);
+    }
 
     // sliced legs carried by leaf operands: offsets per set bit of the slice
     auto slice_strides = [&](int child, std::vector<uint64_t>& v) {
@@ -565,6 +593,15 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     } else if (op.nb > 0) {
       arena_off[node] = alloc(table_elems[node], node);
       op.out_base = arena_off[node];
+    }
+    if (op.config == kTcConfig && op.nb > 0) {
+      // scratch: TF32 residuals of A's table + B̂ hi/lo (2N x 2K floats each)
+      op.a_entries = ti.distinct[op.child_a];
+      const uint64_t a_lo = op.a_entries << (op.fa + op.kc);
+      const uint64_t bhat = uint64_t{op.nb} << (op.fb + op.kc + 1);
+      op.scratch_elems = a_lo + 2 * bhat;
+      op.scratch_off = alloc(op.scratch_elems, node);
+      release(op.scratch_off, op.scratch_elems);  // free again once the op is done
     }
     // children are dead once consumed
     for (int ch : {l, r})

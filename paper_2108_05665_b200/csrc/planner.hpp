@@ -64,6 +64,11 @@ struct Op {
   std::vector<uint32_t> out_rows;  // root: item -> accumulator row
   uint64_t out_rows_off = 0;
   int config = 0;                  // kernel tile configuration
+  uint64_t a_entries = 0;          // tensor-core path: entries in A's table
+  uint64_t scratch_off = 0;        // tensor-core path: arena scratch (elements)
+  uint64_t scratch_elems = 0;
+  bool a_kcontig = false;          // A rows are K-contiguous (tak(k) == k)
+  bool o_ncontig = false;          // output n index is contiguous (ton(n) == n)
   // exact algorithmic counts per slice (tensor.cpp:132-148)
   uint64_t mults = 0, adds = 0, rw = 0;
 };

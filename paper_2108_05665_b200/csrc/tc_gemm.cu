@@ -1,0 +1,372 @@
+// tcgen05 complex64 GEMM for the dense contractions (sm_100a).
+//
+// A complex GEMM C[m][n] = Σ_k A[m][k] B[k][n] is one REAL GEMM on the
+// interleaved layouts: with Â = A viewed as M x 2K floats ([ar, ai] per k —
+// exactly how an intermediate is stored, K-contiguous rows) and
+// B̂ (2N x 2K, K-major) rows 2n = [br, -bi]_k, 2n+1 = [bi, br]_k, the real
+// product Ĉ = Â B̂ᵀ is C in interleaved (re, im) layout: 8 real flops per
+// complex MAC, no 4M/3M overhead.
+//
+// fp32 accuracy on TF32 tensor cores: each operand x = hi + lo with
+// hi = rna_tf32(x) and lo = x - hi (exact), and Ĉ = Âhi B̂hi + Âhi B̂lo +
+// Âlo B̂hi (3xTF32; the dropped lo·lo term is < 2^-22 |ab|).
+//
+// Kernel: one CTA per 128 x BN output tile (BN <= 256 real columns), K in
+// 32-float (128-byte) stages: TMA (SWIZZLE_128B) loads the four operand tiles
+// into a 2-stage smem ring guarded by mbarriers; one elected thread issues
+// 3 x 4 tcgen05.mma.kind::tf32 per stage into a TMEM accumulator and
+// tcgen05.commit frees the stage; four epilogue warps tcgen05.ld the
+// accumulator and scatter complex results through the output offset tables
+// (the parent's layout / the root accumulator), optionally accumulating.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "tc_gemm.hpp"
+
+namespace mtcg {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;        // floats per stage row (128 B: one swizzle row)
+constexpr int kStages = 2;
+constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA, warps 2-5 epilogue
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// K-major, SWIZZLE_128B smem matrix descriptor (8-row atoms of 128 B rows;
+// stride between atoms 1024 B; sm100 descriptor version 1).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t{(saddr >> 4) & 0x3FFFu}) | (uint64_t{1} << 16) | (uint64_t{64} << 32) |
+         (uint64_t{1} << 46) | (uint64_t{2} << 61);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcTable {
+  const uint32_t* lo;
+  const uint32_t* hi;
+  int lo_bits;
+  __device__ __forceinline__ uint32_t operator()(uint64_t x) const {
+    return __ldg(lo + (x & ((1u << lo_bits) - 1))) + __ldg(hi + (x >> lo_bits));
+  }
+};
+
+struct TcParams {
+  int M, Nr, Kr;             // rows, real columns (2N), real K (2K)
+  int bn;                    // real columns per tile
+  uint32_t nb;               // items
+  const uint32_t* ia;        // item -> A entry
+  float2* out;               // output base
+  const uint32_t* out_rows;  // root: item -> accumulator row
+  uint64_t out_item;         // complex elements per output entry
+  TcTable tom, ton;          // m / n -> output offset (complex elements)
+  int accumulate;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_3xtf32(const __grid_constant__ CUtensorMap map_ahi,
+                   const __grid_constant__ CUtensorMap map_alo,
+                   const __grid_constant__ CUtensorMap map_bhi,
+                   const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned carve-up: per stage Ahi | Alo (BM x 128 B), Bhi | Blo (bn x 128 B)
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+  const int a_bytes = kBM * kBK * 4;
+  const int b_bytes = p.bn * kBK * 4;
+  const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * stage_bytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* accum = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint64_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
+  const uint64_t tiles_m = (p.M + kBM - 1) / kBM;
+  const uint64_t tile = blockIdx.x;
+  const int tn = static_cast<int>(tile % tiles_n);
+  const int tm = static_cast<int>((tile / tiles_n) % tiles_m);
+  const uint32_t item = static_cast<uint32_t>(tile / (tiles_n * tiles_m));
+  const int m0 = tm * kBM, n0 = tn * p.bn;
+  const int a_row0 = static_cast<int>((p.ia ? p.ia[item] : item) * static_cast<uint64_t>(p.M)) + m0;
+  const int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
+  const int k_stages = p.Kr / kBK;
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < static_cast<uint32_t>(p.bn)) tmem_cols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int s = 0; s < k_stages; ++s) {
+      const int st = s % kStages;
+      if (s >= kStages) mbar_wait(&empty[st], ((s / kStages) - 1) & 1);
+      uint8_t* sp = base + st * stage_bytes;
+      mbar_expect_tx(&full[st], stage_bytes);
+      const int kc = s * kBK;
+      tma_load_2d(sp, &map_ahi, &full[st], kc, a_row0);
+      tma_load_2d(sp + a_bytes, &map_alo, &full[st], kc, a_row0);
+      tma_load_2d(sp + 2 * a_bytes, &map_bhi, &full[st], kc, b_row0);
+      tma_load_2d(sp + 2 * a_bytes + b_bytes, &map_blo, &full[st], kc, b_row0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    // instruction descriptor: D f32, A/B tf32, K-major, N = bn, M = 128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                           (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
+    for (int s = 0; s < k_stages; ++s) {
+      const int st = s % kStages;
+      mbar_wait(&full[st], (s / kStages) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t sp = smem_u32(base + st * stage_bytes);
+      const uint32_t ahi = sp, alo = sp + a_bytes, bhi = sp + 2 * a_bytes,
+                     blo = sp + 2 * a_bytes + b_bytes;
+#pragma unroll
+      for (int kk = 0; kk < kBK / 8; ++kk) {  // tf32 MMA K = 8 (32 bytes)
+        const uint32_t off = kk * 32;
+        const uint32_t acc0 = (s > 0 || kk > 0) ? 1u : 0u;
+        mma_tf32(tmem, sw128_desc(alo + off), sw128_desc(bhi + off), idesc, acc0);
+        mma_tf32(tmem, sw128_desc(ahi + off), sw128_desc(blo + off), idesc, 1u);
+        mma_tf32(tmem, sw128_desc(ahi + off), sw128_desc(bhi + off), idesc, 1u);
+      }
+      mma_commit(&empty[st]);  // stage consumed once these MMAs retire
+    }
+    mma_commit(accum);
+  } else if (warp >= 2) {
+    // ---- epilogue: TMEM -> registers -> complex scatter ----
+    mbar_wait(accum, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quarter = warp % 4;  // TMEM lane quarter this warp may access
+    const int r = quarter * 32 + lane;
+    const int m = m0 + r;
+    float2* O = p.out + (p.out_rows ? uint64_t{p.out_rows[item]} : uint64_t{item}) * p.out_item;
+    const uint32_t om = m < p.M ? p.tom(m) : 0u;
+    for (int c0 = 0; c0 < p.bn; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
+      if (m >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int nr = n0 + c0 + 2 * j;
+        if (nr >= p.Nr) break;
+        float2 val = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        float2* dst = O + om + p.ton(nr >> 1);
+        if (p.accumulate) {
+          const float2 old = *dst;
+          val.x += old.x;
+          val.y += old.y;
+        }
+        *dst = val;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_cols));
+  }
+}
+
+// hi = rna_tf32(x) in place, lo = x - hi
+__global__ void split_tf32_kernel(float* x, float* lo, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const float v = x[i];
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
+    const float hf = __uint_as_float(h);
+    x[i] = hf;
+    lo[i] = v - hf;
+  }
+}
+
+// B̂ (2N x 2K floats per item, K-major) from the B operand, split hi/lo.
+__global__ void build_bhat_kernel(const float2* b, uint64_t b_item, const uint32_t* ib,
+                                  uint64_t b_slice, TcTable tbn, TcTable tbk, int fb, int kc,
+                                  uint32_t nb, float* bhi, float* blo) {
+  const uint64_t N = uint64_t{1} << fb, K = uint64_t{1} << kc;
+  const uint64_t total = uint64_t{nb} * N * K;
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    const uint64_t k = e % K, n = (e / K) % N, item = e / (K * N);
+    const float2 v = b[uint64_t{ib ? ib[item] : (uint32_t)item} * b_item + b_slice + tbn(n) + tbk(k)];
+    const float q[4] = {v.x, -v.y, v.y, v.x};  // row 2n: [br, -bi]; row 2n+1: [bi, br]
+    const uint64_t r0 = (item * 2 * N + 2 * n) * (2 * K) + 2 * k;
+    const uint64_t r1 = r0 + 2 * K;
+    const uint64_t idx[4] = {r0, r0 + 1, r1, r1 + 1};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      uint32_t h;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(q[t]));
+      bhi[idx[t]] = __uint_as_float(h);
+      blo[idx[t]] = q[t] - __uint_as_float(h);
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !ptr)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+CUtensorMap make_map(const float* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * sizeof(float)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+
+}  // namespace
+
+size_t tc_smem_bytes(int bn) {
+  return 1024 + kStages * (2 * kBM * kBK * 4 + 2 * bn * kBK * 4) + 64;
+}
+
+int tc_tile_n(int Nr) { return Nr >= 256 ? 256 : Nr; }
+
+void tc_contract(const TcOp& op, cudaStream_t st) {
+  const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb, K = uint64_t{1} << op.kc;
+  const uint64_t Nr = 2 * N, Kr = 2 * K;
+  // 1) split A (the child's table, dead after this op) in place: hi | lo
+  const uint64_t a_floats = 2 * op.a_entries * M * K;
+  const int blocks = 148 * 8;
+  split_tf32_kernel<<<blocks, 256, 0, st>>>(op.a, op.a_lo, a_floats);
+  // 2) B̂ hi / lo
+  TcTable tbn{op.tbn_lo, op.tbn_hi, op.tbn_bits}, tbk{op.tbk_lo, op.tbk_hi, op.tbk_bits};
+  build_bhat_kernel<<<blocks, 256, 0, st>>>(op.b, op.b_item, op.ib, op.b_slice, tbn, tbk, op.fb,
+                                            op.kc, op.nb, op.bhat_hi, op.bhat_lo);
+  // 3) GEMM
+  const int bn = tc_tile_n(static_cast<int>(Nr));
+  const CUtensorMap mahi = make_map(op.a, Kr, op.a_entries * M, kBM);
+  const CUtensorMap malo = make_map(op.a_lo, Kr, op.a_entries * M, kBM);
+  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{op.nb} * Nr, bn);
+  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{op.nb} * Nr, bn);
+  TcParams p;
+  p.M = static_cast<int>(M);
+  p.Nr = static_cast<int>(Nr);
+  p.Kr = static_cast<int>(Kr);
+  p.bn = bn;
+  p.nb = op.nb;
+  p.ia = op.ia;
+  p.out = op.out;
+  p.out_rows = op.out_rows;
+  p.out_item = op.out_item;
+  p.tom = TcTable{op.tom_lo, op.tom_hi, op.tom_bits};
+  p.ton = TcTable{op.ton_lo, op.ton_hi, op.ton_bits};
+  p.accumulate = op.accumulate;
+  const size_t smem = tc_smem_bytes(bn);
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    cudaFuncSetAttribute(tc_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    smem_set = smem;
+  }
+  const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * op.nb;
+  tc_gemm_3xtf32<<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(mahi, malo, mbhi, mblo, p);
+}
+
+}  // namespace mtcg

@@ -34,6 +34,7 @@ class EvalOptions:
     memory_cap_bytes: int = 0
     workers: int = 1
     precision: str = "c64"
+    tensor_cores: bool = True  # dense complex64 ops on tcgen05 (3xTF32)
 
 
 @dataclass
@@ -89,6 +90,7 @@ def _options(mode: int, opts: Optional[EvalOptions]) -> A.mtcg_options:
     o.precision = PRECISIONS[opts.precision]
     o.memory_cap_bytes = int(opts.memory_cap_bytes)
     o.workers = int(opts.workers)
+    o.flags = 0 if opts.tensor_cores else 1  # MTCG_FLAG_NO_TENSOR_CORES
     return o
 
 
