@@ -78,6 +78,7 @@ uint64_t device_cap(const mtcg_handle* h, const mtcg_options& o) {
   if (h->cap) return h->cap;
   size_t free_b = 0, total_b = 0;
   if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return 0;
+  free_b += engine_arena_bytes(h->engine);  // the cached arena is reusable
   return free_b > (256ull << 20) ? free_b - (256ull << 20) : free_b;
 }
 

@@ -33,10 +33,16 @@
 
 namespace mtcg {
 
+// One per handle. The intermediate arena is owned here and shared by every
+// plan compiled on the handle (plans only keep per-slice intermediates in it
+// and the handle is not reentrant), so repeated compiles of a workload do not
+// pay cudaMalloc/cudaFree of a multi-GB region each time.
 struct Engine {
   int device = 0;
   cudaStream_t stream = nullptr;
   uint64_t launches = 0;
+  void* arena = nullptr;
+  uint64_t arena_bytes = 0;
 };
 
 #define CK(x)                                                                  \
@@ -256,7 +262,11 @@ struct Vec4<double2> {
 template <class R, int K, int N, int RPT>
 __global__ void __launch_bounds__(256)
     contract_rows(const DevOp<typename V2<R>::T> op) {
+  // RPT rows per thread computed together: each B row (N complex, one
+  // broadcast smem read per element) feeds RPT x N multiply-adds; K streams
+  // in chunks of KC so A never occupies more than RPT x KC registers.
   using T = typename V2<R>::T;
+  constexpr int KC = K < 8 ? K : 8;
   __shared__ T Bs[K * N];
   __shared__ uint32_t kao[K];
   __shared__ uint32_t ono[N];
@@ -274,42 +284,64 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   const uint64_t M = uint64_t{1} << op.fa;
   const uint64_t base = uint64_t{blockIdx.x} * (256 * RPT) + threadIdx.x;
+  const T* rows[RPT];
+  bool live[RPT];
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const uint64_t m = base + j * 256;
-    if (m >= M) break;
-    T av[K];
-    const T* row = A + op.tam(m);
-    if (K >= 2 && op.a_kcontig) {
-      using V4 = typename Vec4<T>::type;
+    live[j] = m < M;
+    rows[j] = A + (live[j] ? op.tam(m) : 0u);
+  }
+  T acc[RPT][N];
 #pragma unroll
-      for (int k = 0; k < K; k += 2) {
-        const V4 v = *reinterpret_cast<const V4*>(row + k);
-        av[k] = T{v.x, v.y};
-        av[k + 1] = T{v.z, v.w};
+  for (int j = 0; j < RPT; ++j)
+#pragma unroll
+    for (int n = 0; n < N; ++n) acc[j][n] = czero<T>();
+#pragma unroll 1
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    T av[RPT][KC];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      if (KC >= 2 && op.a_kcontig) {
+        using V4 = typename Vec4<T>::type;
+#pragma unroll
+        for (int kk = 0; kk < KC; kk += 2) {
+          const V4 v = live[j] ? *reinterpret_cast<const V4*>(rows[j] + k0 + kk) : V4{};
+          av[j][kk] = T{v.x, v.y};
+          av[j][kk + 1] = T{v.z, v.w};
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) av[j][kk] = live[j] ? rows[j][kao[k0 + kk]] : czero<T>();
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) av[k] = row[kao[k]];
     }
-    T acc[N];
 #pragma unroll
-    for (int n = 0; n < N; ++n) acc[n] = czero<T>();
+    for (int kk = 0; kk < KC; ++kk) {
+      T bv[N];
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+      for (int n = 0; n < N; ++n) bv[n] = Bs[(k0 + kk) * N + n];
+      const bool first = k0 == 0 && kk == 0;
 #pragma unroll
-      for (int n = 0; n < N; ++n) cmac(acc[n], av[k], Bs[k * N + n], k == 0);
-    T* dst = O + op.tom(m);
+      for (int j = 0; j < RPT; ++j)
+#pragma unroll
+        for (int n = 0; n < N; ++n) cmac(acc[j][n], av[j][kk], bv[n], first);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    if (!live[j]) continue;
+    T* dst = O + op.tom(base + j * 256);
     if (N >= 2 && op.o_ncontig && !op.accumulate) {
       using V4 = typename Vec4<T>::type;
 #pragma unroll
       for (int n = 0; n < N; n += 2)
-        *reinterpret_cast<V4*>(dst + n) = V4{acc[n].x, acc[n].y, acc[n + 1].x, acc[n + 1].y};
+        *reinterpret_cast<V4*>(dst + n) =
+            V4{acc[j][n].x, acc[j][n].y, acc[j][n + 1].x, acc[j][n + 1].y};
     } else {
 #pragma unroll
       for (int n = 0; n < N; ++n) {
         T* d = dst + ono[n];
-        *d = op.accumulate ? cadd(*d, acc[n]) : acc[n];
+        *d = op.accumulate ? cadd(*d, acc[j][n]) : acc[j][n];
       }
     }
   }
@@ -467,7 +499,8 @@ void launch_tile(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
 
 template <class R, int K, int N>
 void launch_rows_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
-  constexpr int RPT = 2;
+  // rows per thread: amortise B reads over more rows when N is small
+  constexpr int RPT = sizeof(R) == 8 ? 1 : (N <= 4 ? 4 : 2);
   const uint64_t M = uint64_t{1} << op.fa;
   const unsigned gx = static_cast<unsigned>((M + 256 * RPT - 1) / (256 * RPT));
   const unsigned gy = std::min<uint32_t>(op.nb, 65535u);
@@ -652,16 +685,18 @@ Engine* engine_create(int device) {
 void engine_destroy(Engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
+  if (e->arena) cudaFree(e->arena);
   cudaStreamDestroy(e->stream);
   delete e;
 }
 
 uint64_t engine_launches(const Engine* e) { return e->launches; }
+uint64_t engine_arena_bytes(const Engine* e) { return e->arena_bytes; }
 void* engine_stream(Engine* e) { return e->stream; }
 
 DevicePlan::~DevicePlan() {
   if (engine) cudaSetDevice(engine->device);
-  for (void* p : {d_leaves, d_arena, static_cast<void*>(d_tables), static_cast<void*>(d_index),
+  for (void* p : {d_leaves, static_cast<void*>(d_tables), static_cast<void*>(d_index),
                   static_cast<void*>(d_slice_strides), static_cast<void*>(d_row_mult)})
     if (p) cudaFree(p);
 }
@@ -683,7 +718,20 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
     CK(cudaMemcpy(dp->d_leaves, cc.leaf_values.data(), cc.leaf_values.size() * sizeof(double),
                   cudaMemcpyHostToDevice));
   }
-  if (cc.arena_elems) CK(cudaMalloc(&dp->d_arena, cc.arena_elems * eb));
+  if (cc.arena_elems) {
+    const uint64_t need = cc.arena_elems * eb;
+    if (e->arena_bytes < need) {
+      if (e->arena) {
+        CK(cudaStreamSynchronize(e->stream));
+        CK(cudaFree(e->arena));
+        e->arena = nullptr;
+        e->arena_bytes = 0;
+      }
+      CK(cudaMalloc(&e->arena, need));
+      e->arena_bytes = need;
+    }
+    dp->d_arena = e->arena;
+  }
   CK(cudaMalloc(&dp->d_tables, std::max<size_t>(cc.table_blob.size(), 1) * 4));
   if (!cc.table_blob.empty())
     CK(cudaMemcpy(dp->d_tables, cc.table_blob.data(), cc.table_blob.size() * 4,

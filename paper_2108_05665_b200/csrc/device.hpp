@@ -33,6 +33,7 @@ struct DevicePlan {
 Engine* engine_create(int device);
 void engine_destroy(Engine* e);
 uint64_t engine_launches(const Engine* e);
+uint64_t engine_arena_bytes(const Engine* e);  // cached intermediate arena
 void* engine_stream(Engine* e);
 
 std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c);

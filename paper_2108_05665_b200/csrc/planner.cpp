@@ -20,7 +20,10 @@
 #include "planner.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -89,26 +92,39 @@ struct TupleIndex {
   uint64_t rows = 0;
   std::vector<uint32_t> row_tuple_first;  // request index representing row
   std::vector<uint64_t> row_of_request;
-  std::vector<std::vector<uint32_t>> rank;  // [node][row]
+  std::vector<std::vector<uint32_t>> rank;        // [node][row]
+  std::vector<std::vector<uint32_t>> rank_value;  // leaves: rank -> value index
+  std::vector<std::vector<uint32_t>> pair_l, pair_r;  // internal: rank -> child ranks
   std::vector<uint32_t> distinct;
 };
 
 // build_tuple_index (plan.cpp:292-333). Rows are the distinct request tuples
 // in lexicographic order; rank[node][row] is the dense rank of the row's
 // restriction to the node's leaves, ordered by (rank_left, rank_right).
+// Same ranks as the reference; faster: tuples are compared on the slots that
+// have more than one value only (every other column is 0 in every tuple),
+// and ranks come from marking the keys each row produces (keys of a node lie
+// in [0, distinct[left] * distinct[right])) and sorting only the distinct ones.
 TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
   TupleIndex ti;
   const uint64_t k = p.n_requests;
   const int m = p.n_slots;
   const uint32_t* T = p.tuples;
+  std::vector<int> informative;
+  for (int j = 0; j < m; ++j)
+    if (p.slot_n_values[j] > 1) informative.push_back(j);
+  const size_t w = informative.size();
+  std::vector<uint32_t> compact(k * w);
+  for (uint64_t i = 0; i < k; ++i)
+    for (size_t c = 0; c < w; ++c) compact[i * w + c] = T[i * m + informative[c]];
+  const uint32_t* Cp = compact.data();
   std::vector<uint64_t> order(k);
   std::iota(order.begin(), order.end(), 0);
   auto lex_less = [&](uint64_t a, uint64_t b) {
-    return std::lexicographical_compare(T + a * m, T + a * m + m, T + b * m,
-                                        T + b * m + m);
+    return std::lexicographical_compare(Cp + a * w, Cp + a * w + w, Cp + b * w, Cp + b * w + w);
   };
   auto lex_eq = [&](uint64_t a, uint64_t b) {
-    return std::equal(T + a * m, T + a * m + m, T + b * m);
+    return std::equal(Cp + a * w, Cp + a * w + w, Cp + b * w);
   };
   std::stable_sort(order.begin(), order.end(), lex_less);
   ti.row_of_request.assign(k, 0);
@@ -120,19 +136,35 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
   ti.rows = ti.row_tuple_first.size();
   const uint64_t rows = ti.rows;
   ti.rank.assign(p.n_nodes, {});
+  ti.rank_value.assign(p.n_nodes, {});
   ti.distinct.assign(p.n_nodes, 0);
+  ti.pair_l.assign(p.n_nodes, {});
+  ti.pair_r.assign(p.n_nodes, {});
+  // informative columns of the distinct rows, slot-major (sequential reads)
+  std::vector<int> column_of(m, -1);
+  for (size_t c = 0; c < w; ++c) column_of[informative[c]] = static_cast<int>(c);
+  std::vector<uint32_t> cols(w * rows);
+  for (uint64_t r = 0; r < rows; ++r)
+    for (size_t c = 0; c < w; ++c)
+      cols[c * rows + r] = Cp[static_cast<uint64_t>(ti.row_tuple_first[r]) * w + c];
   std::vector<uint64_t> keys(rows);
   std::vector<uint32_t> mark;
-  std::vector<uint64_t> sorted;
+  std::vector<uint64_t> touched;
+  const uint64_t mark_limit = 16 * rows + 4096;
   for (int node : ix.postorder) {
     std::vector<uint32_t>& rk = ti.rank[node];
     rk.resize(rows);
     uint64_t span;  // keys lie in [0, span)
     if (p.node_slot[node] >= 0) {
-      const int slot = p.node_slot[node];
-      for (uint64_t r = 0; r < rows; ++r)
-        keys[r] = T[static_cast<uint64_t>(ti.row_tuple_first[r]) * m + slot];
-      span = static_cast<uint64_t>(p.slot_n_values[slot]);
+      const int c = column_of[p.node_slot[node]];
+      if (c < 0) {  // single-valued slot: every row has value 0
+        std::fill(rk.begin(), rk.end(), 0u);
+        ti.distinct[node] = rows ? 1 : 0;
+        if (rows) ti.rank_value[node].assign(1, 0u);
+        continue;
+      }
+      for (uint64_t r = 0; r < rows; ++r) keys[r] = cols[c * rows + r];
+      span = static_cast<uint64_t>(p.slot_n_values[p.node_slot[node]]);
     } else {
       const auto& rl = ti.rank[p.node_left[node]];
       const auto& rr = ti.rank[p.node_right[node]];
@@ -142,23 +174,41 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
     }
     // Dense ranks in key order. Keys order like the reference's
     // (rank_l << 32 | rank_r) since rank_r < distinct[right].
-    uint32_t next = 0;
-    if (span <= 8 * rows + 4096) {
-      mark.assign(span, 0);
-      for (uint64_t r = 0; r < rows; ++r) mark[keys[r]] = 1;
-      for (uint64_t v = 0; v < span; ++v)
-        if (mark[v]) mark[v] = ++next;
+    touched.clear();
+    if (span <= mark_limit) {
+      if (mark.size() < span) mark.resize(span, 0);
+      for (uint64_t r = 0; r < rows; ++r)
+        if (!mark[keys[r]]) {
+          mark[keys[r]] = 1;
+          touched.push_back(keys[r]);
+        }
+      std::sort(touched.begin(), touched.end());
+      for (size_t i = 0; i < touched.size(); ++i) mark[touched[i]] = static_cast<uint32_t>(i + 1);
       for (uint64_t r = 0; r < rows; ++r) rk[r] = mark[keys[r]] - 1;
+      for (uint64_t key : touched) mark[key] = 0;
     } else {
-      sorted = keys;
-      std::sort(sorted.begin(), sorted.end());
-      sorted.erase(std::unique(sorted.begin(), sorted.end()), sorted.end());
-      next = static_cast<uint32_t>(sorted.size());
+      touched = keys;
+      std::sort(touched.begin(), touched.end());
+      touched.erase(std::unique(touched.begin(), touched.end()), touched.end());
       for (uint64_t r = 0; r < rows; ++r)
         rk[r] = static_cast<uint32_t>(
-            std::lower_bound(sorted.begin(), sorted.end(), keys[r]) - sorted.begin());
+            std::lower_bound(touched.begin(), touched.end(), keys[r]) - touched.begin());
     }
-    ti.distinct[node] = rows == 0 ? 0 : next;
+    ti.distinct[node] = static_cast<uint32_t>(touched.size());
+    if (p.node_slot[node] >= 0) {
+      ti.rank_value[node].assign(touched.begin(), touched.end());
+    } else {
+      // (rank_left, rank_right) of every distinct rank: the batch entries
+      const uint64_t dr = ti.distinct[p.node_right[node]];
+      auto& pl = ti.pair_l[node];
+      auto& pr = ti.pair_r[node];
+      pl.resize(touched.size());
+      pr.resize(touched.size());
+      for (size_t i = 0; i < touched.size(); ++i) {
+        pl[i] = static_cast<uint32_t>(touched[i] / dr);
+        pr[i] = static_cast<uint32_t>(touched[i] % dr);
+      }
+    }
   }
   return ti;
 }
@@ -199,8 +249,24 @@ void SplitTable::build(const std::vector<uint64_t>& strides) {
   }
 }
 
+namespace {
+// MTCG_TIMING=1 prints the host compile phases to stderr.
+struct PhaseTimer {
+  bool on = std::getenv("MTCG_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[mtcg] %-14s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
                          uint64_t cap_bytes) {
+  PhaseTimer timer;
   Compiled c;
   c.precision = opt.precision;
   if (opt.precision != MTCG_C64 && opt.precision != MTCG_C128)
@@ -275,6 +341,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
   c.leaf_elems = leaf_elems;
   c.leaf_values.assign(p.values, p.values + 2 * leaf_elems);
 
+  timer.mark("validate+leaves");
   // --- tuple index ----------------------------------------------------------
   TupleIndex ti = build_tuple_index(p, ix);
   c.n_requests = p.n_requests;
@@ -283,6 +350,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
   c.row_mult.assign(ti.rows, 0);
   for (uint64_t r : ti.row_of_request) c.row_mult[r] += 1;
 
+  timer.mark("tuple index");
   // --- logical shapes ----------------------------------------------------------
   const int n = p.n_nodes;
   std::vector<std::vector<uint32_t>> legs(n);  // logical legs (sorted for internal)
@@ -427,6 +495,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
                              std::to_string(cap_bytes) + " bytes)",
                          p.root);
 
+  timer.mark("shapes+sched");
   // --- ops ------------------------------------------------------------------------
   c.node_contractions.assign(n, 0);
   for (int node : sched) {
@@ -473,19 +542,14 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     // the rank of its value index among the rows (ranks == value indices when
     // every value occurs, which build_assignments guarantees; map explicitly).
     {
-      const auto& rk = ti.rank[node];
-      const auto& ra = ti.rank[op.child_a];
-      const auto& rb = ti.rank[op.child_b];
-      for (uint64_t row = 0; row < ti.rows; ++row) {
-        const uint32_t b = rk[row];
-        op.ia[b] = ra[row];
-        op.ib[b] = rb[row];
-        if (op.a_leaf)
-          op.ia[b] = p.tuples[static_cast<uint64_t>(ti.row_tuple_first[row]) * p.n_slots +
-                              p.node_slot[op.child_a]];
-        if (op.b_leaf)
-          op.ib[b] = p.tuples[static_cast<uint64_t>(ti.row_tuple_first[row]) * p.n_slots +
-                              p.node_slot[op.child_b]];
+      const auto& ra = op.a_is_left ? ti.pair_l[node] : ti.pair_r[node];
+      const auto& rb = op.a_is_left ? ti.pair_r[node] : ti.pair_l[node];
+      // a leaf child's rank maps to its value index through rank_value
+      const auto& va = ti.rank_value[op.child_a];
+      const auto& vb = ti.rank_value[op.child_b];
+      for (uint32_t b = 0; b < op.nb; ++b) {
+        op.ia[b] = op.a_leaf ? va[ra[b]] : ra[b];
+        op.ib[b] = op.b_leaf ? vb[rb[b]] : rb[b];
       }
     }
     const auto& a_layout = layout[op.child_a];
@@ -633,6 +697,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     }
   }
 
+  timer.mark("ops");
   // --- blobs -----------------------------------------------------------------
   auto put_table = [&](SplitTable& t) {
     t.dev_off = c.table_blob.size();
@@ -655,6 +720,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     put_table(c.leaf_root.tout);
     c.leaf_root.rows_off = put_index(c.leaf_root.row_value);
   }
+  timer.mark("blobs");
   return c;
 }
 
