@@ -260,7 +260,7 @@ struct Vec4<double2> {
 };
 
 template <class R, int K, int N, int RPT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     contract_rows(const DevOp<typename V2<R>::T> op) {
   // RPT rows per thread computed together: each B row (N complex, one
   // broadcast smem read per element) feeds RPT x N multiply-adds; K streams
@@ -297,7 +297,9 @@ __global__ void __launch_bounds__(256)
   for (int j = 0; j < RPT; ++j)
 #pragma unroll
     for (int n = 0; n < N; ++n) acc[j][n] = czero<T>();
-#pragma unroll 1
+  // fully unrolled over the (<= 4) chunks so the next chunk's loads issue
+  // under the current chunk's FMAs; the launch bound keeps 2 blocks per SM
+#pragma unroll
   for (int k0 = 0; k0 < K; k0 += KC) {
     T av[RPT][KC];
 #pragma unroll
@@ -616,8 +618,7 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
           t.kc = op.kc;
           t.nb = op.nb;
           t.a_entries = op.a_entries;
-          t.a = reinterpret_cast<float*>(arena + op.a_base);
-          t.a_lo = reinterpret_cast<float*>(arena + op.scratch_off);
+          t.a = reinterpret_cast<const float*>(arena + op.a_base);
           t.ia = d.ia;
           t.b = reinterpret_cast<const float2*>(d.b);
           t.b_item = op.b_item;
@@ -629,10 +630,9 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
           t.tbk_lo = d.tbk.lo;
           t.tbk_hi = d.tbk.hi;
           t.tbk_bits = d.tbk.lo_bits;
-          const uint64_t a_lo_elems = op.a_entries << (op.fa + op.kc);
           const uint64_t bhat_elems = uint64_t{op.nb} << (op.fb + op.kc + 1);
-          t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off + a_lo_elems);
-          t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + a_lo_elems + bhat_elems);
+          t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off);
+          t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + bhat_elems);
           t.out = reinterpret_cast<float2*>(d.out);
           t.out_rows = d.out_rows;
           t.out_item = op.out_item;
@@ -643,8 +643,10 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
           t.ton_hi = d.ton.hi;
           t.ton_bits = d.ton.lo_bits;
           t.accumulate = d.accumulate;
+          t.n_contig = op.o_ncontig ? 1 : 0;
+          t.m_contig = op.o_mcontig ? 1 : 0;
           tc_contract(t, st);
-          dp.engine->launches += 3;
+          dp.engine->launches += 2;  // B̂ build + GEMM
           if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
           continue;
         }

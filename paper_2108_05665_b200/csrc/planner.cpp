@@ -377,11 +377,15 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     throw DataError("request tensors of order above 30 are not supported");
 
   // --- stored layouts -------------------------------------------------------------
-  // root: ascending (the observable layout); other internal nodes:
-  // [legs kept by the parent][legs the parent closes], each ascending, so the
-  // parent contraction reads K-contiguous rows.
+  // Top-down. Root: ascending (the observable layout). Other internal nodes:
+  // [legs kept by the parent, in the parent's layout order][legs the parent
+  // closes, ascending] — the parent contraction reads K-contiguous rows (K in
+  // the reference's reduction order), and walking those rows in memory order
+  // walks the parent's output in address order, so row-parallel epilogues
+  // (tensor-core tiles, streaming kernels) write coalesced.
   std::vector<std::vector<uint32_t>> layout(n);
-  for (int node : ix.postorder) {
+  for (size_t q = ix.postorder.size(); q-- > 0;) {  // parents before children
+    const int node = ix.postorder[q];
     if (p.node_slot[node] >= 0) {
       layout[node] = slot_layout[p.node_slot[node]];
       continue;
@@ -393,7 +397,10 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     }
     const int sib = p.node_left[par] == node ? p.node_right[par] : p.node_left[par];
     std::vector<uint32_t> keep, close;
-    for (uint32_t l : legs[node]) (contains(legs[sib], l) ? close : keep).push_back(l);
+    for (uint32_t l : layout[par])  // parent's layout order
+      if (contains(legs[node], l)) keep.push_back(l);
+    for (uint32_t l : legs[node])
+      if (contains(legs[sib], l)) close.push_back(l);  // ascending
     layout[node] = keep;
     layout[node].insert(layout[node].end(), close.begin(), close.end());
   }
@@ -564,15 +571,16 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     op.config = select_config(op.fa, op.fb, op.kc);
     // Tensor-core path (complex64 only): dense, K-contiguous intermediate A,
     // shapes the 128 x (2N) x (2K) real tiles cover exactly.
-    // Only compute-bound ops: intensity MNK / (MK + NK + MN) >= 32 complex MACs
-    // per element moved (HBM-bound skinny ops stay on the streaming kernels,
-    // which move 5x fewer bytes than the split + GEMM path).
+    // Ops with intensity MNK / (MK + NK + MN) >= 6 complex MACs per element
+    // moved: above that the CUDA-core kernels are FMA-bound while the tensor
+    // path (A read once, split in smem) stays near the HBM roofline; below it
+    // the streaming kernels win.
     const double Md = std::ldexp(1.0, op.fa), Nd = std::ldexp(1.0, op.fb),
                  Kd = std::ldexp(1.0, op.kc);
     const double intensity = Md * Nd * Kd / (Md * Kd + Nd * Kd + Md * Nd);
     const bool tc_ok = c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) &&
-                       !op.a_leaf && op.fa >= 7 && op.fb >= 3 && op.kc >= 4 &&
-                       intensity >= 32.0 &&
+                       !op.a_leaf && op.fa >= 7 && op.fb >= 5 && op.kc >= 4 &&
+                       intensity >= 6.0 &&
                        (uint64_t{op.nb} << (op.fa + op.fb + op.kc)) >= (uint64_t{1} << 26);
     if (tc_ok) op.config = kTcConfig;
     // m / n bit orders: free legs by increasing address in the output layout;
@@ -616,6 +624,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       const auto ns = strides_of(n_legs, out_layout);
       op.o_ncontig = op.config != kGenericConfig;
       for (size_t b = 0; b < ns.size(); ++b) op.o_ncontig &= ns[b] == (uint64_t{1} << b);
+      const auto ms = strides_of(m_legs, out_layout);
+      op.o_mcontig = !ms.empty() && ms[0] == 1;
     }
 
     // sliced legs carried by leaf operands: offsets per set bit of the slice
@@ -659,11 +669,10 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       op.out_base = arena_off[node];
     }
     if (op.config == kTcConfig && op.nb > 0) {
-      // scratch: TF32 residuals of A's table + B̂ hi/lo (2N x 2K floats each)
+      // scratch: B̂ hi/lo (2N x 2K floats per item each)
       op.a_entries = ti.distinct[op.child_a];
-      const uint64_t a_lo = op.a_entries << (op.fa + op.kc);
       const uint64_t bhat = uint64_t{op.nb} << (op.fb + op.kc + 1);
-      op.scratch_elems = a_lo + 2 * bhat;
+      op.scratch_elems = 2 * bhat;  // B̂ hi / lo (A is split in shared memory)
       op.scratch_off = alloc(op.scratch_elems, node);
       release(op.scratch_off, op.scratch_elems);  // free again once the op is done
     }

@@ -69,6 +69,7 @@ struct Op {
   uint64_t scratch_elems = 0;
   bool a_kcontig = false;          // A rows are K-contiguous (tak(k) == k)
   bool o_ncontig = false;          // output n index is contiguous (ton(n) == n)
+  bool o_mcontig = false;          // output m bit 0 has stride 1
   // exact algorithmic counts per slice (tensor.cpp:132-148)
   uint64_t mults = 0, adds = 0, rw = 0;
 };

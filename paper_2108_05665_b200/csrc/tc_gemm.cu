@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -34,8 +35,6 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;        // floats per stage row (128 B: one swizzle row)
-constexpr int kStages = 2;
-constexpr int kThreads = 192;  // warp0 TMA, warp1 MMA, warps 2-5 epilogue
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -132,44 +131,83 @@ struct TcParams {
   uint64_t out_item;         // complex elements per output entry
   TcTable tom, ton;          // m / n -> output offset (complex elements)
   int accumulate;
+  int n_contig;              // ton(n) = ton(n0) + (n - n0) within every tile
+  int m_contig;              // tom(m + 1) = tom(m) + 1: lanes (rows) store coalesced
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
-    tc_gemm_3xtf32(const __grid_constant__ CUtensorMap map_ahi,
-                   const __grid_constant__ CUtensorMap map_alo,
-                   const __grid_constant__ CUtensorMap map_bhi,
-                   const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  return __uint_as_float(h);
+}
+
+// ---- persistent warp-specialised variant -------------------------------------
+//
+// One CTA per SM loops over output tiles (item, m-tile, n-tile; n fastest so
+// co-resident CTAs share A tiles in L2). Ten warps:
+//   warp 0     TMA producer: raw A, B̂hi, B̂lo stages into an S-deep smem ring
+//   warp 1     MMA issuer: 3 x (BK/8) tcgen05.mma per stage into one of two
+//              TMEM accumulators (double buffered across tiles)
+//   warps 2-5  converters: split each landed A stage into TF32 hi / lo in smem
+//   warps 6-9  epilogue: tcgen05.ld the finished accumulator, scatter complex
+//              results, release the accumulator — overlapping the next tile's
+//              main loop.
+// The ring depth S is chosen so the stages fill ~220 KB of shared memory.
+constexpr int kPThreads = 320;
+constexpr int kMaxStages = 8;
+constexpr int kMaxAcc = 8;          // TMEM accumulator buffers
+constexpr int kMaxTonCache = 2048;  // output column offsets cached in smem
+
+__global__ void __launch_bounds__(kPThreads, 1)
+    tc_gemm_persistent(const __grid_constant__ CUtensorMap map_a,
+                       const __grid_constant__ CUtensorMap map_bhi,
+                       const __grid_constant__ CUtensorMap map_blo, const TcParams p,
+                       int n_stages) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte aligned carve-up: per stage Ahi | Alo (BM x 128 B), Bhi | Blo (bn x 128 B)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
   const int a_bytes = kBM * kBK * 4;
   const int b_bytes = p.bn * kBK * 4;
   const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * stage_bytes);
-  uint64_t* empty = full + kStages;
-  uint64_t* accum = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + n_stages * stage_bytes);
+  uint64_t* conv = full + kMaxStages;
+  uint64_t* empty = conv + kMaxStages;
+  uint64_t* acc_full = empty + kMaxStages;
+  uint64_t* acc_empty = acc_full + kMaxAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kMaxAcc);
+  uint32_t* ton_s = tmem_slot + 4;  // output column offsets of all n (if N <= 2048)
+  float* stage_out = reinterpret_cast<float*>(ton_s + kMaxTonCache);  // 4 x 32 x 33 floats
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint64_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
-  const uint64_t tiles_m = (p.M + kBM - 1) / kBM;
-  const uint64_t tile = blockIdx.x;
-  const int tn = static_cast<int>(tile % tiles_n);
-  const int tm = static_cast<int>((tile / tiles_n) % tiles_m);
-  const uint32_t item = static_cast<uint32_t>(tile / (tiles_n * tiles_m));
-  const int m0 = tm * kBM, n0 = tn * p.bn;
-  const int a_row0 = static_cast<int>((p.ia ? p.ia[item] : item) * static_cast<uint64_t>(p.M)) + m0;
-  const int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
+  const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
+  const uint32_t tiles_m = (p.M + kBM - 1) / kBM;
+  const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
   const int k_stages = p.Kr / kBK;
+  uint32_t buf_cols = 32;
+  while (buf_cols < static_cast<uint32_t>(p.bn)) buf_cols <<= 1;
+  // accumulator ring: as many buffers as fit in TMEM's 512 columns (2..8), so
+  // short-K tiles keep the MMA busy while earlier tiles drain
+  const uint32_t n_acc = min(static_cast<uint32_t>(kMaxAcc), 512u / buf_cols);
   uint32_t tmem_cols = 32;
-  while (tmem_cols < static_cast<uint32_t>(p.bn)) tmem_cols <<= 1;
+  while (tmem_cols < n_acc * buf_cols) tmem_cols <<= 1;
+  const int n_cols = p.Nr / 2;
+  const bool ton_cached = n_cols <= kMaxTonCache;
+  if (ton_cached)
+    for (int n = threadIdx.x; n < n_cols; n += blockDim.x) ton_s[n] = p.ton(n);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < n_stages; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 128);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (uint32_t b = 0; b < n_acc; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -183,68 +221,165 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---- TMA producer ----
-    for (int s = 0; s < k_stages; ++s) {
-      const int st = s % kStages;
-      if (s >= kStages) mbar_wait(&empty[st], ((s / kStages) - 1) & 1);
-      uint8_t* sp = base + st * stage_bytes;
-      mbar_expect_tx(&full[st], stage_bytes);
-      const int kc = s * kBK;
-      tma_load_2d(sp, &map_ahi, &full[st], kc, a_row0);
-      tma_load_2d(sp + a_bytes, &map_alo, &full[st], kc, a_row0);
-      tma_load_2d(sp + 2 * a_bytes, &map_bhi, &full[st], kc, b_row0);
-      tma_load_2d(sp + 2 * a_bytes + b_bytes, &map_blo, &full[st], kc, b_row0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---- MMA issuer ----
-    // instruction descriptor: D f32, A/B tf32, K-major, N = bn, M = 128
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                           (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
-    for (int s = 0; s < k_stages; ++s) {
-      const int st = s % kStages;
-      mbar_wait(&full[st], (s / kStages) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sp = smem_u32(base + st * stage_bytes);
-      const uint32_t ahi = sp, alo = sp + a_bytes, bhi = sp + 2 * a_bytes,
-                     blo = sp + 2 * a_bytes + b_bytes;
-#pragma unroll
-      for (int kk = 0; kk < kBK / 8; ++kk) {  // tf32 MMA K = 8 (32 bytes)
-        const uint32_t off = kk * 32;
-        const uint32_t acc0 = (s > 0 || kk > 0) ? 1u : 0u;
-        mma_tf32(tmem, sw128_desc(alo + off), sw128_desc(bhi + off), idesc, acc0);
-        mma_tf32(tmem, sw128_desc(ahi + off), sw128_desc(blo + off), idesc, 1u);
-        mma_tf32(tmem, sw128_desc(ahi + off), sw128_desc(bhi + off), idesc, 1u);
-      }
-      mma_commit(&empty[st]);  // stage consumed once these MMAs retire
-    }
-    mma_commit(accum);
-  } else if (warp >= 2) {
-    // ---- epilogue: TMEM -> registers -> complex scatter ----
-    mbar_wait(accum, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int quarter = warp % 4;  // TMEM lane quarter this warp may access
-    const int r = quarter * 32 + lane;
-    const int m = m0 + r;
-    float2* O = p.out + (p.out_rows ? uint64_t{p.out_rows[item]} : uint64_t{item}) * p.out_item;
-    const uint32_t om = m < p.M ? p.tom(m) : 0u;
-    for (int c0 = 0; c0 < p.bn; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
-      if (m >= p.M) continue;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int nr = n0 + c0 + 2 * j;
-        if (nr >= p.Nr) break;
-        float2 val = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-        float2* dst = O + om + p.ton(nr >> 1);
-        if (p.accumulate) {
-          const float2 old = *dst;
-          val.x += old.x;
-          val.y += old.y;
+  auto tile_coords = [&](uint64_t t, uint32_t& item, int& m0, int& n0) {
+    n0 = static_cast<int>(t % tiles_n) * p.bn;
+    m0 = static_cast<int>((t / tiles_n) % tiles_m) * kBM;
+    item = static_cast<uint32_t>(t / (uint64_t{tiles_n} * tiles_m));
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer ----
+      uint64_t g = 0;
+      uint32_t cached_item = ~0u, a_entry = 0;
+      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        uint32_t item;
+        int m0, n0;
+        tile_coords(t, item, m0, n0);
+        if (item != cached_item) {  // items change every tiles_m * tiles_n tiles
+          cached_item = item;
+          a_entry = p.ia ? p.ia[item] : item;
         }
-        *dst = val;
+        const int a_row0 = static_cast<int>(a_entry * static_cast<uint64_t>(p.M)) + m0;
+        const int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
+        for (int s = 0; s < k_stages; ++s, ++g) {
+          const int st = static_cast<int>(g % n_stages);
+          if (g >= static_cast<uint64_t>(n_stages))
+            mbar_wait(&empty[st], static_cast<uint32_t>((g / n_stages) - 1) & 1);
+          uint8_t* sp = base + st * stage_bytes;
+          mbar_expect_tx(&full[st], a_bytes + 2 * b_bytes);
+          tma_load_2d(sp, &map_a, &full[st], s * kBK, a_row0);
+          tma_load_2d(sp + 2 * a_bytes, &map_bhi, &full[st], s * kBK, b_row0);
+          tma_load_2d(sp + 2 * a_bytes + b_bytes, &map_blo, &full[st], s * kBK, b_row0);
+        }
       }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                             (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
+      uint64_t g = 0, it = 0;
+      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const uint32_t tb = static_cast<uint32_t>(it % n_acc);
+        if (it >= n_acc) mbar_wait(&acc_empty[tb], static_cast<uint32_t>((it / n_acc) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dacc = tmem + tb * buf_cols;
+        for (int s = 0; s < k_stages; ++s, ++g) {
+          const int st = static_cast<int>(g % n_stages);
+          mbar_wait(&conv[st], static_cast<uint32_t>(g / n_stages) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sp = smem_u32(base + st * stage_bytes);
+          const uint32_t ahi = sp, alo = sp + a_bytes, bhi = sp + 2 * a_bytes,
+                         blo = sp + 2 * a_bytes + b_bytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint32_t acc0 = (s > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(dacc, sw128_desc(alo + off), sw128_desc(bhi + off), idesc, acc0);
+            mma_tf32(dacc, sw128_desc(ahi + off), sw128_desc(blo + off), idesc, 1u);
+            mma_tf32(dacc, sw128_desc(ahi + off), sw128_desc(bhi + off), idesc, 1u);
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(&acc_full[tb]);
+      }
+    }
+  } else if (warp < 6) {  // ---- converters ----
+    const int ct = threadIdx.x - 64;
+    uint64_t g = 0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int s = 0; s < k_stages; ++s, ++g) {
+        const int st = static_cast<int>(g % n_stages);
+        mbar_wait(&full[st], static_cast<uint32_t>(g / n_stages) & 1);
+        float4* hi = reinterpret_cast<float4*>(base + st * stage_bytes);
+        float4* lo = reinterpret_cast<float4*>(base + st * stage_bytes + a_bytes);
+#pragma unroll
+        for (int i = 0; i < (kBM * kBK * 4) / 16 / 128; ++i) {
+          const int e = ct + i * 128;
+          const float4 v = hi[e];
+          const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+          hi[e] = h;
+          lo[e] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&conv[st]);
+      }
+    }
+  } else {  // ---- epilogue ----
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    uint64_t it = 0;
+    uint32_t cached_item = ~0u;
+    uint64_t out_entry = 0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      uint32_t item;
+      int m0, n0;
+      tile_coords(t, item, m0, n0);
+      const uint32_t tb = static_cast<uint32_t>(it % n_acc);
+      mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + r;
+      if (item != cached_item) {
+        cached_item = item;
+        out_entry = p.out_rows ? uint64_t{p.out_rows[item]} : uint64_t{item};
+      }
+      float2* O = p.out + out_entry * p.out_item;
+      const uint32_t om = m < p.M ? p.tom(m) : 0u;
+      for (int c0 = 0; c0 < p.bn; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
+        const int cols = min(16, (p.bn - c0) / 2);
+        const int nb0 = (n0 + c0) / 2;  // first complex column of this chunk
+        if (!p.m_contig) {
+          // Output rows are not adjacent in memory: transpose the warp's
+          // 32 rows x `cols` complex chunk through shared memory so that
+          // consecutive lanes write consecutive columns of a row.
+          float* buf = stage_out + (warp - 6) * 32 * 33;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
+          __syncwarp();
+          const int per_row_shift = 31 - __clz(cols);  // cols is a power of two
+          for (int e = lane; e < 32 * cols; e += 32) {
+            const int row = e >> per_row_shift, cj = e & (cols - 1);
+            const uint32_t row_om = __shfl_sync(0xffffffffu, om, row);
+            if (m0 + quarter * 32 + row >= p.M) continue;
+            float2 val = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
+            float2* dst = O + row_om + (ton_cached ? ton_s[nb0 + cj] : p.ton(nb0 + cj));
+            if (p.accumulate) {
+              const float2 old = *dst;
+              val.x += old.x;
+              val.y += old.y;
+            }
+            *dst = val;
+          }
+          __syncwarp();
+          continue;
+        }
+        if (m >= p.M) continue;
+        if (p.n_contig && !p.accumulate) {
+          // the chunk's columns are consecutive in the output: 16-byte stores
+          float4* dst = reinterpret_cast<float4*>(O + om + (ton_cached ? ton_s[nb0] : p.ton(nb0)));
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (2 * j < cols)
+              dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j >= cols) break;
+            float2 val = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+            float2* dst = O + om + (ton_cached ? ton_s[nb0 + j] : p.ton(nb0 + j));
+            if (p.accumulate) {
+              const float2 old = *dst;
+              val.x += old.x;
+              val.y += old.y;
+            }
+            *dst = val;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&acc_empty[tb]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -252,19 +387,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(tmem_cols));
-  }
-}
-
-// hi = rna_tf32(x) in place, lo = x - hi
-__global__ void split_tf32_kernel(float* x, float* lo, uint64_t n) {
-  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n;
-       i += uint64_t{gridDim.x} * blockDim.x) {
-    const float v = x[i];
-    uint32_t h;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
-    const float hf = __uint_as_float(h);
-    x[i] = hf;
-    lo[i] = v - hf;
   }
 }
 
@@ -322,27 +444,19 @@ CUtensorMap make_map(const float* base, uint64_t cols, uint64_t rows, uint32_t b
 
 }  // namespace
 
-size_t tc_smem_bytes(int bn) {
-  return 1024 + kStages * (2 * kBM * kBK * 4 + 2 * bn * kBK * 4) + 64;
-}
-
 int tc_tile_n(int Nr) { return Nr >= 256 ? 256 : Nr; }
 
 void tc_contract(const TcOp& op, cudaStream_t st) {
   const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb, K = uint64_t{1} << op.kc;
   const uint64_t Nr = 2 * N, Kr = 2 * K;
-  // 1) split A (the child's table, dead after this op) in place: hi | lo
-  const uint64_t a_floats = 2 * op.a_entries * M * K;
-  const int blocks = 148 * 8;
-  split_tf32_kernel<<<blocks, 256, 0, st>>>(op.a, op.a_lo, a_floats);
-  // 2) B̂ hi / lo
+  // 1) B̂ hi / lo (small: per item 2N x 2K floats); A is split in the kernel
+  const int blocks = static_cast<int>(std::min<uint64_t>(148 * 8, (uint64_t{op.nb} * N * K + 255) / 256));
   TcTable tbn{op.tbn_lo, op.tbn_hi, op.tbn_bits}, tbk{op.tbk_lo, op.tbk_hi, op.tbk_bits};
   build_bhat_kernel<<<blocks, 256, 0, st>>>(op.b, op.b_item, op.ib, op.b_slice, tbn, tbk, op.fb,
                                             op.kc, op.nb, op.bhat_hi, op.bhat_lo);
-  // 3) GEMM
+  // 2) GEMM
   const int bn = tc_tile_n(static_cast<int>(Nr));
-  const CUtensorMap mahi = make_map(op.a, Kr, op.a_entries * M, kBM);
-  const CUtensorMap malo = make_map(op.a_lo, Kr, op.a_entries * M, kBM);
+  const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM);
   const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{op.nb} * Nr, bn);
   const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{op.nb} * Nr, bn);
   TcParams p;
@@ -358,15 +472,29 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   p.tom = TcTable{op.tom_lo, op.tom_hi, op.tom_bits};
   p.ton = TcTable{op.ton_lo, op.ton_hi, op.ton_bits};
   p.accumulate = op.accumulate;
-  const size_t smem = tc_smem_bytes(bn);
+  p.n_contig = op.n_contig;
+  p.m_contig = op.m_contig;
+  // persistent: one CTA per SM, ring depth filling ~220 KB of shared memory
+  const int stage_bytes = 2 * kBM * kBK * 4 + 2 * bn * kBK * 4;
+  // align + barriers/tmem slot/tom bits (< 768 B) + ton cache
+  constexpr int kExtra = 1024 + 768 + 4 * kMaxTonCache + 4 * 4 * 32 * 33;
+  const int n_stages = std::max(2, std::min(kMaxStages, (224 * 1024 - kExtra) / stage_bytes));
+  const size_t smem = kExtra + static_cast<size_t>(n_stages) * stage_bytes;
   static size_t smem_set = 0;
+  static int n_sms = 0;
   if (smem > smem_set) {
-    cudaFuncSetAttribute(tc_gemm_3xtf32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tc_gemm_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     smem_set = smem;
   }
+  if (!n_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * op.nb;
-  tc_gemm_3xtf32<<<static_cast<unsigned>(tiles), kThreads, smem, st>>>(mahi, malo, mbhi, mblo, p);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));
+  tc_gemm_persistent<<<grid, kPThreads, smem, st>>>(ma, mbhi, mblo, p, n_stages);
 }
 
 }  // namespace mtcg

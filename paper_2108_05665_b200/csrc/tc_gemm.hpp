@@ -8,15 +8,14 @@
 namespace mtcg {
 
 // One dense batched contraction on the tensor cores. A must be an
-// intermediate table ([entry][M][K] complex, K-contiguous rows); its entries
-// are rounded to TF32 in place (A is dead after its parent's op) and their
-// residuals written to a_lo. B̂ hi/lo are built in bhat_hi/bhat_lo.
+// intermediate table ([entry][M][K] complex, K-contiguous rows), read raw and
+// split into TF32 hi/lo inside the kernel. B̂ hi/lo are built in
+// bhat_hi/bhat_lo (scratch).
 struct TcOp {
   int fa, fb, kc;                 // log2 M, N, K
   uint32_t nb;                    // items
   uint64_t a_entries;             // entries in A's table
-  float* a;                       // A table (floats, interleaved complex)
-  float* a_lo;                    // scratch: a_entries * M * 2K floats
+  const float* a;                 // A table (floats, interleaved complex)
   const uint32_t* ia;
   const float2* b;                // B operand table base
   uint64_t b_item, b_slice;
@@ -31,10 +30,11 @@ struct TcOp {
   const uint32_t *tom_lo, *tom_hi, *ton_lo, *ton_hi;
   int tom_bits, ton_bits;
   int accumulate;
+  int n_contig;                   // output n index contiguous (vector epilogue stores)
+  int m_contig;                   // output m index contiguous (row-per-lane stores coalesce)
 };
 
 void tc_contract(const TcOp& op, cudaStream_t st);
-size_t tc_smem_bytes(int bn);
 int tc_tile_n(int n_real);
 
 }  // namespace mtcg
