@@ -78,11 +78,18 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        self.first = ""
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            self.proc = None
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # wait for the first sample: nvidia-smi's start-up (NVML init) must
+            # not overlap the timed region
+            self.first = self.proc.stdout.readline()
         except Exception:  # noqa: BLE001
             self.proc = None
         return self
@@ -330,6 +337,9 @@ def run_engine(args):
     cp = eng.compile(problem, 0, opts)
     S = cp.n_slices
     s0, s1 = S * rank // world, S * (rank + 1) // world
+    # one dedicated (non-legacy) stream for the engine's graph launches, the
+    # NCCL reduce and the timing events
+    torch.cuda.set_stream(torch.cuda.Stream())
     stream = torch.cuda.current_stream().cuda_stream
     acc = cp.new_accumulator()
 
@@ -347,18 +357,19 @@ def run_engine(args):
     if world > 1:
         dist.barrier()
     launches0 = eng.launches
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        start.record()
-        for _ in range(args.steps):
+        marks[0].record()
+        for i in range(args.steps):
             xeb = step()
-        end.record()
+            marks[i + 1].record()
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = eng.launches - launches0
-    t_ms = start.elapsed_time(end)
+    t_ms = marks[0].elapsed_time(marks[-1])
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -428,6 +439,8 @@ def run_engine(args):
                     "includes": "host planning + tuple index, H2D leaves/tables, all slices, "
                                 "D2H amplitudes + fan-out, XEB"},
             "gpu_launches": launches,
+            "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms),
+                        "max": max(step_ms), "all": [round(x, 2) for x in step_ms]},
             "clocks": clk.summary(),
         }
         print(json.dumps(line))

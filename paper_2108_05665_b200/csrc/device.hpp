@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -25,8 +26,28 @@ struct DevicePlan {
   uint32_t* d_index = nullptr;
   uint64_t* d_slice_strides = nullptr;  // per op: S strides for A then B
   uint32_t* d_row_mult = nullptr;
+  double* d_xeb_part = nullptr;         // fused-XEB block partials (device)
+  double* h_xeb_part = nullptr;         // ... and their pinned host copy
   std::vector<uint64_t> op_slice_off;   // word offset of each op's strides
   uint64_t leaf_root_slice_off = 0;
+  // Instantiated CUDA graphs of whole slice ranges, keyed by
+  // (s0, s1, accumulator, accumulate): a step is one graph launch.
+  struct GraphKey {
+    uint64_t s0, s1;
+    void* acc;
+    bool accumulate;
+    bool operator<(const GraphKey& o) const {
+      if (s0 != o.s0) return s0 < o.s0;
+      if (s1 != o.s1) return s1 < o.s1;
+      if (acc != o.acc) return acc < o.acc;
+      return accumulate < o.accumulate;
+    }
+  };
+  struct GraphEntry {
+    void* exec = nullptr;   // cudaGraphExec_t
+    uint64_t kernels = 0;   // device launches replayed per graph launch
+  };
+  std::map<GraphKey, GraphEntry> graphs;
   ~DevicePlan();
 };
 

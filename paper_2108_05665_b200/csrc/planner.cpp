@@ -504,6 +504,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
 
   timer.mark("shapes+sched");
   // --- ops ------------------------------------------------------------------------
+  // smallest log2 N sent to the tensor cores (MTCG_TC_MIN_FB overrides; tuning)
+  const int tc_min_fb = std::getenv("MTCG_TC_MIN_FB") ? std::atoi(std::getenv("MTCG_TC_MIN_FB")) : 4;
   c.node_contractions.assign(n, 0);
   for (int node : sched) {
     const int l = p.node_left[node], r = p.node_right[node];
@@ -579,10 +581,23 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
                  Kd = std::ldexp(1.0, op.kc);
     const double intensity = Md * Nd * Kd / (Md * Kd + Nd * Kd + Md * Nd);
     const bool tc_ok = c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) &&
-                       !op.a_leaf && op.fa >= 7 && op.fb >= 5 && op.kc >= 4 &&
+                       !op.a_leaf && op.fa >= 7 && op.fb >= tc_min_fb && op.kc >= 4 &&
                        intensity >= 6.0 &&
                        (uint64_t{op.nb} << (op.fa + op.fb + op.kc)) >= (uint64_t{1} << 26);
-    if (tc_ok) op.config = kTcConfig;
+    // MTCG_TC_ONLY=<node>[,<node>...] restricts the tensor path (diagnostics)
+    const char* tc_only = std::getenv("MTCG_TC_ONLY");
+    bool tc_listed = true;
+    if (tc_only) {
+      tc_listed = false;
+      for (const char* s = tc_only; *s;) {
+        char* end = nullptr;
+        const long v = std::strtol(s, &end, 10);
+        if (end == s) break;
+        tc_listed |= v == node;
+        s = *end ? end + 1 : end;
+      }
+    }
+    if (tc_ok && tc_listed) op.config = kTcConfig;
     // m / n bit orders: free legs by increasing address in the output layout;
     // the tensor-core path walks A rows in A's memory order instead (TMA rows)
     std::vector<uint32_t> m_legs = by_out_addr(fa_legs);

@@ -11,21 +11,26 @@
 // hi = rna_tf32(x) and lo = x - hi (exact), and Ĉ = Âhi B̂hi + Âhi B̂lo +
 // Âlo B̂hi (3xTF32; the dropped lo·lo term is < 2^-22 |ab|).
 //
-// Kernel: one CTA per 128 x BN output tile (BN <= 256 real columns), K in
-// 32-float (128-byte) stages: TMA (SWIZZLE_128B) loads the four operand tiles
-// into a 2-stage smem ring guarded by mbarriers; one elected thread issues
-// 3 x 4 tcgen05.mma.kind::tf32 per stage into a TMEM accumulator and
-// tcgen05.commit frees the stage; four epilogue warps tcgen05.ld the
-// accumulator and scatter complex results through the output offset tables
-// (the parent's layout / the root accumulator), optionally accumulating.
+// Kernel (tc_gemm_persistent): one persistent CTA per SM walks 128 x BN output
+// tiles (BN <= 256 real columns), K in 32-float (128-byte) stages. TMA
+// (SWIZZLE_128B) lands raw A and B̂ hi/lo in an mbarrier-guarded smem ring;
+// converter warps split A into TF32 hi/lo in place; one elected thread issues
+// 3 x 4 tcgen05.mma.kind::tf32 per stage into a ring of TMEM accumulators and
+// tcgen05.commit frees the stage; epilogue warps tcgen05.ld finished
+// accumulators and scatter complex results through the output offset tables
+// (the parent's layout / the root accumulator), optionally accumulating,
+// while the next tiles' main loop runs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "tc_gemm.hpp"
 
@@ -133,7 +138,15 @@ struct TcParams {
   int accumulate;
   int n_contig;              // ton(n) = ton(n0) + (n - n0) within every tile
   int m_contig;              // tom(m + 1) = tom(m) + 1: lanes (rows) store coalesced
+  int transpose;             // epilogue transposes 32-row chunks through smem
+  unsigned long long* dbg;   // MTCG_TC_TRACE: per-tile role timestamps of CTA 0
 };
+
+// Role timestamps of CTA 0's first kTraceTiles tiles (MTCG_TC_TRACE=<node>).
+constexpr int kTraceTiles = 256;
+__device__ __forceinline__ void trace(const TcParams& p, uint64_t it, int slot) {
+  if (p.dbg && blockIdx.x == 0 && it < kTraceTiles) p.dbg[it * 8 + slot] = clock64();
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -145,19 +158,28 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(h);
 }
 
+// Same rounding (to nearest, ties away from zero, on the magnitude) with two
+// integer ALU ops instead of the low-throughput conversion; identical for
+// every finite input whose rounding does not overflow.
+__device__ __forceinline__ float tf32_rna_alu(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
 // ---- persistent warp-specialised variant -------------------------------------
 //
 // One CTA per SM loops over output tiles (item, m-tile, n-tile; n fastest so
-// co-resident CTAs share A tiles in L2). Ten warps:
-//   warp 0     TMA producer: raw A, B̂hi, B̂lo stages into an S-deep smem ring
-//   warp 1     MMA issuer: 3 x (BK/8) tcgen05.mma per stage into one of two
-//              TMEM accumulators (double buffered across tiles)
-//   warps 2-5  converters: split each landed A stage into TF32 hi / lo in smem
-//   warps 6-9  epilogue: tcgen05.ld the finished accumulator, scatter complex
-//              results, release the accumulator — overlapping the next tile's
-//              main loop.
+// co-resident CTAs share A tiles in L2). Warps:
+//   warp 0      TMA producer: raw A, B̂hi, B̂lo stages into an S-deep smem ring
+//   warp 1      MMA issuer: 3 x (BK/8) tcgen05.mma per stage into a ring of up
+//               to 8 TMEM accumulators
+//   warps 2-5   converters: split each landed A stage into TF32 hi / lo in smem
+//   warps 6-13  epilogue, two warpgroups taking alternate tiles: tcgen05.ld a
+//               finished accumulator, scatter complex results, release it —
+//               overlapping later tiles' main loops (short-K tiles are
+//               epilogue-bound; MTCG_TC_TRACE=<node> prints role timestamps).
 // The ring depth S is chosen so the stages fill ~220 KB of shared memory.
-constexpr int kPThreads = 320;
+constexpr int kEpiGroups = 2;       // epilogue warpgroups (alternate tiles)
+constexpr int kPThreads = 192 + 128 * kEpiGroups;
 constexpr int kMaxStages = 8;
 constexpr int kMaxAcc = 8;          // TMEM accumulator buffers
 constexpr int kMaxTonCache = 2048;  // output column offsets cached in smem
@@ -178,8 +200,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* acc_full = empty + kMaxStages;
   uint64_t* acc_empty = acc_full + kMaxAcc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kMaxAcc);
-  uint32_t* ton_s = tmem_slot + 4;  // output column offsets of all n (if N <= 2048)
-  float* stage_out = reinterpret_cast<float*>(ton_s + kMaxTonCache);  // 4 x 32 x 33 floats
+  // output column offsets of all n (if N <= kMaxTonCache), then the epilogue's
+  // transpose buffers (8 warps x 32 x 33 floats) when output rows are strided
+  uint32_t* ton_s = tmem_slot + 4;
+  float* stage_out = reinterpret_cast<float*>(ton_s + min(p.Nr / 2, kMaxTonCache));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
@@ -231,10 +255,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
     if (lane == 0) {  // ---- TMA producer ----
       uint64_t g = 0;
       uint32_t cached_item = ~0u, a_entry = 0;
-      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      uint64_t pit = 0;
+      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++pit) {
         uint32_t item;
         int m0, n0;
         tile_coords(t, item, m0, n0);
+        trace(p, pit, 0);
         if (item != cached_item) {  // items change every tiles_m * tiles_n tiles
           cached_item = item;
           a_entry = p.ia ? p.ia[item] : item;
@@ -251,6 +277,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           tma_load_2d(sp + 2 * a_bytes, &map_bhi, &full[st], s * kBK, b_row0);
           tma_load_2d(sp + 2 * a_bytes + b_bytes, &map_blo, &full[st], s * kBK, b_row0);
         }
+        trace(p, pit, 1);
       }
     }
   } else if (warp == 1) {
@@ -261,6 +288,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
         const uint32_t tb = static_cast<uint32_t>(it % n_acc);
         if (it >= n_acc) mbar_wait(&acc_empty[tb], static_cast<uint32_t>((it / n_acc) - 1) & 1);
+        trace(p, it, 2);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dacc = tmem + tb * buf_cols;
         for (int s = 0; s < k_stages; ++s, ++g) {
@@ -281,22 +309,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
           mma_commit(&empty[st]);
         }
         mma_commit(&acc_full[tb]);
+        trace(p, it, 3);
       }
     }
   } else if (warp < 6) {  // ---- converters ----
     const int ct = threadIdx.x - 64;
-    uint64_t g = 0;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    uint64_t g = 0, cit = 0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++cit) {
       for (int s = 0; s < k_stages; ++s, ++g) {
         const int st = static_cast<int>(g % n_stages);
         mbar_wait(&full[st], static_cast<uint32_t>(g / n_stages) & 1);
+        if (ct == 0 && s == 0) trace(p, cit, 4);
         float4* hi = reinterpret_cast<float4*>(base + st * stage_bytes);
         float4* lo = reinterpret_cast<float4*>(base + st * stage_bytes + a_bytes);
 #pragma unroll
         for (int i = 0; i < (kBM * kBK * 4) / 16 / 128; ++i) {
           const int e = ct + i * 128;
           const float4 v = hi[e];
-          const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+          const float4 h = make_float4(tf32_rna_alu(v.x), tf32_rna_alu(v.y), tf32_rna_alu(v.z),
+                                       tf32_rna_alu(v.w));
           hi[e] = h;
           lo[e] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
@@ -304,32 +335,44 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_arrive(&conv[st]);
       }
     }
-  } else {  // ---- epilogue ----
-    const int quarter = warp % 4;
+  } else {  // ---- epilogue: kEpiGroups warpgroups take alternate tiles ----
+    const int eg = (warp - 6) / 4;  // epilogue group
+    const int quarter = warp % 4;   // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
-    uint64_t it = 0;
-    uint32_t cached_item = ~0u;
-    uint64_t out_entry = 0;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      uint32_t item;
-      int m0, n0;
-      tile_coords(t, item, m0, n0);
+    // the group's first tile; the next tile's row offset is fetched while the
+    // current one drains so the dependent table loads overlap the wait
+    uint64_t t = blockIdx.x + uint64_t{static_cast<uint32_t>(eg)} * gridDim.x;
+    uint64_t it = eg;
+    uint32_t item = 0, nxt_item = 0;
+    int m0 = 0, n0 = 0, nxt_m0 = 0, nxt_n0 = 0;
+    uint32_t om = 0, nxt_om = 0;
+    uint64_t out_entry = 0, nxt_out = 0;
+    auto fetch = [&](uint64_t tt) {
+      tile_coords(tt, nxt_item, nxt_m0, nxt_n0);
+      nxt_om = nxt_m0 + r < p.M ? p.tom(nxt_m0 + r) : 0u;
+      nxt_out = p.out_rows ? uint64_t{p.out_rows[nxt_item]} : uint64_t{nxt_item};
+    };
+    if (t < tiles) fetch(t);
+    for (; t < tiles; t += kEpiGroups * uint64_t{gridDim.x}, it += kEpiGroups) {
+      item = nxt_item;
+      m0 = nxt_m0;
+      n0 = nxt_n0;
+      om = nxt_om;
+      out_entry = nxt_out;
+      if (t + kEpiGroups * uint64_t{gridDim.x} < tiles) fetch(t + kEpiGroups * uint64_t{gridDim.x});
       const uint32_t tb = static_cast<uint32_t>(it % n_acc);
       mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
+      if (warp == 6 && lane == 0) trace(p, it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + r;
-      if (item != cached_item) {
-        cached_item = item;
-        out_entry = p.out_rows ? uint64_t{p.out_rows[item]} : uint64_t{item};
-      }
       float2* O = p.out + out_entry * p.out_item;
-      const uint32_t om = m < p.M ? p.tom(m) : 0u;
+      (void)item;
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
         const int cols = min(16, (p.bn - c0) / 2);
         const int nb0 = (n0 + c0) / 2;  // first complex column of this chunk
-        if (!p.m_contig) {
+        if (p.transpose) {
           // Output rows are not adjacent in memory: transpose the warp's
           // 32 rows x `cols` complex chunk through shared memory so that
           // consecutive lanes write consecutive columns of a row.
@@ -380,6 +423,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&acc_empty[tb]);
+      if (warp == 6 && lane == 0) trace(p, it, 6);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -454,8 +498,20 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   TcTable tbn{op.tbn_lo, op.tbn_hi, op.tbn_bits}, tbk{op.tbk_lo, op.tbk_hi, op.tbk_bits};
   build_bhat_kernel<<<blocks, 256, 0, st>>>(op.b, op.b_item, op.ib, op.b_slice, tbn, tbk, op.fb,
                                             op.kc, op.nb, op.bhat_hi, op.bhat_lo);
-  // 2) GEMM
+  // 2) GEMM: persistent, one CTA per SM; smem = ring + ton cache + transpose
+  // buffers; keep >= 2 stages (halve the n tile if needed)
+  // Short output rows (<= 32 complex per tile row) that are strided in memory
+  // are transposed through smem in the epilogue; longer rows are written per
+  // lane with vector stores.
   const int bn = tc_tile_n(static_cast<int>(Nr));
+  const bool transpose = !op.m_contig && bn <= 64;
+  const int extra = 1024 + 768 + 4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) +
+                    (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
+  constexpr int kSmemMax = 227 * 1024;
+  auto stage_of = [](int b) { return 2 * kBM * kBK * 4 + 2 * b * kBK * 4; };
+  const int stage_bytes = stage_of(bn);
+  const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
+  const size_t smem = extra + static_cast<size_t>(n_stages) * stage_bytes;
   const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM);
   const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{op.nb} * Nr, bn);
   const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{op.nb} * Nr, bn);
@@ -474,12 +530,7 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   p.accumulate = op.accumulate;
   p.n_contig = op.n_contig;
   p.m_contig = op.m_contig;
-  // persistent: one CTA per SM, ring depth filling ~220 KB of shared memory
-  const int stage_bytes = 2 * kBM * kBK * 4 + 2 * bn * kBK * 4;
-  // align + barriers/tmem slot/tom bits (< 768 B) + ton cache
-  constexpr int kExtra = 1024 + 768 + 4 * kMaxTonCache + 4 * 4 * 32 * 33;
-  const int n_stages = std::max(2, std::min(kMaxStages, (224 * 1024 - kExtra) / stage_bytes));
-  const size_t smem = kExtra + static_cast<size_t>(n_stages) * stage_bytes;
+  p.transpose = transpose ? 1 : 0;
   static size_t smem_set = 0;
   static int n_sms = 0;
   if (smem > smem_set) {
@@ -494,7 +545,33 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   }
   const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * op.nb;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));
+  p.dbg = nullptr;
+  const char* tr = std::getenv("MTCG_TC_TRACE");
+  const bool tracing = tr && std::atoi(tr) == op.node;
+  if (tracing) {
+    cudaMalloc(&p.dbg, sizeof(unsigned long long) * kTraceTiles * 8);
+    cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * kTraceTiles * 8, st);
+  }
   tc_gemm_persistent<<<grid, kPThreads, smem, st>>>(ma, mbhi, mblo, p, n_stages);
+  if (tracing) {
+    std::vector<unsigned long long> h(kTraceTiles * 8);
+    cudaMemcpyAsync(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    cudaFree(p.dbg);
+    const unsigned long long t0 = h[0];
+    std::fprintf(stderr, "[tc trace node %d] stages=%d bn=%d tiles=%llu grid=%u n_acc<=%d\n",
+                 op.node, n_stages, bn, static_cast<unsigned long long>(tiles), grid, kMaxAcc);
+    std::fprintf(stderr, " tile  prod0  prod1  conv(full) mma0  mma1  epi0  epi1   (cycles from tile0 prod0)\n");
+    for (int i = 0; i < kTraceTiles; ++i) {
+      if (!h[i * 8]) break;
+      if (i < 24 || i % 32 == 0)
+        std::fprintf(stderr, " %4d %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", i,
+                     (long long)(h[i * 8] - t0), (long long)(h[i * 8 + 1] - t0),
+                     (long long)(h[i * 8 + 4] - t0), (long long)(h[i * 8 + 2] - t0),
+                     (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 5] - t0),
+                     (long long)(h[i * 8 + 6] - t0));
+    }
+  }
 }
 
 }  // namespace mtcg

@@ -12,6 +12,7 @@ namespace mtcg {
 // split into TF32 hi/lo inside the kernel. B̂ hi/lo are built in
 // bhat_hi/bhat_lo (scratch).
 struct TcOp {
+  int node;                       // plan node (diagnostics)
   int fa, fb, kc;                 // log2 M, N, K
   uint32_t nb;                    // items
   uint64_t a_entries;             // entries in A's table
