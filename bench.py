@@ -380,16 +380,31 @@ def run_engine(args):
     mults = int(cp.info.mults)
 
     # ---- end to end through the public API: host inputs -> device -> host ----
+    trace = bool(os.environ.get("BENCH_E2E_TRACE"))
+
     def e2e_step():
+        t = [time.perf_counter()]
         cpe = eng.compile(problem, 0, opts)
         acc_e = cpe.new_accumulator()
+        t.append(time.perf_counter())
         cpe.run(s0, s1, acc_e.data_ptr(), accumulate=False, stream=stream)
         if world > 1:
             dist.reduce(acc_e, dst=0)
+        t.append(time.perf_counter())
         if rank == 0:
             r = cpe.fetch(acc_e.data_ptr(), stream=stream, node_contractions=False)
+            t.append(time.perf_counter())
             eng.linear_xeb_amplitudes(n_qubits, r.amplitudes)
+            t.append(time.perf_counter())
         torch.cuda.synchronize()
+        t.append(time.perf_counter())
+        del acc_e
+        t.append(time.perf_counter())
+        del cpe
+        t.append(time.perf_counter())
+        if trace:
+            print("e2e step ms: " + " ".join(f"{1e3 * (b - a):.1f}" for a, b in zip(t, t[1:])),
+                  file=sys.stderr)
 
     e2e_steps = max(1, min(args.steps, 5))
     e2e_step()

@@ -44,7 +44,34 @@ struct Engine {
   uint64_t launches = 0;
   void* arena = nullptr;
   uint64_t arena_bytes = 0;
+  void* pinned = nullptr;        // host staging for H2D/D2H (grown on demand)
+  uint64_t pinned_bytes = 0;
+  void* scratch = nullptr;       // device scratch for linear_xeb inputs
+  uint64_t scratch_bytes = 0;
+  // Device blobs of destroyed plans, reused by later uploads: cudaFree
+  // synchronises the device and was measured to stall for 100s of ms.
+  std::vector<std::pair<void*, uint64_t>> blob_pool;
 };
+
+namespace {
+constexpr size_t kBlobPoolMax = 8;
+
+void* blob_get(Engine* e, uint64_t bytes) {
+  size_t best = e->blob_pool.size();
+  for (size_t i = 0; i < e->blob_pool.size(); ++i) {
+    const uint64_t sz = e->blob_pool[i].second;
+    if (sz >= bytes && sz <= 2 * bytes + (1 << 20) &&
+        (best == e->blob_pool.size() || sz < e->blob_pool[best].second))
+      best = i;
+  }
+  if (best < e->blob_pool.size()) {
+    void* p = e->blob_pool[best].first;
+    e->blob_pool.erase(e->blob_pool.begin() + best);
+    return p;
+  }
+  return nullptr;
+}
+}  // namespace
 
 #define CK(x)                                                                  \
   do {                                                                         \
@@ -284,7 +311,11 @@ __global__ void __launch_bounds__(256, 2)
   for (int n = threadIdx.x; n < N; n += blockDim.x) ono[n] = op.ton(n);
   __syncthreads();
   const uint64_t M = uint64_t{1} << op.fa;
-  const uint64_t base = uint64_t{blockIdx.x} * (256 * RPT) + threadIdx.x;
+  // each block streams several row chunks of its item (amortising the B /
+  // offset-table setup above over more bytes)
+  const uint64_t n_chunks = (M + 256 * RPT - 1) / (256 * RPT);
+  for (uint64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+  const uint64_t base = chunk * (256 * RPT) + threadIdx.x;
   const T* rows[RPT];
   bool live[RPT];
 #pragma unroll
@@ -348,6 +379,7 @@ __global__ void __launch_bounds__(256, 2)
       }
     }
   }
+  }  // chunk loop
 }
 
 // ---- one thread per output element ---------------------------------------------
@@ -506,7 +538,10 @@ void launch_rows_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
   // rows per thread: amortise B reads over more rows when N is small
   constexpr int RPT = sizeof(R) == 8 ? 1 : (N <= 4 ? 4 : 2);
   const uint64_t M = uint64_t{1} << op.fa;
-  const unsigned gx = static_cast<unsigned>((M + 256 * RPT - 1) / (256 * RPT));
+  const uint64_t n_chunks = (M + 256 * RPT - 1) / (256 * RPT);
+  // ~16 blocks per SM in total; each loops over n_chunks / gx chunks
+  const uint64_t want = std::max<uint64_t>(1, (148 * 16 + op.nb - 1) / op.nb);
+  const unsigned gx = static_cast<unsigned>(std::min<uint64_t>(n_chunks, want));
   const unsigned gy = std::min<uint32_t>(op.nb, 65535u);
   const unsigned gz = (op.nb + gy - 1) / gy;
   contract_rows<R, K, N, RPT><<<dim3(gx, gy, gz), 256, 0, st>>>(op);
@@ -691,6 +726,9 @@ void engine_destroy(Engine* e) {
   if (!e) return;
   cudaSetDevice(e->device);
   if (e->arena) cudaFree(e->arena);
+  if (e->scratch) cudaFree(e->scratch);
+  for (auto& [p, sz] : e->blob_pool) cudaFree(p);
+  if (e->pinned) cudaFreeHost(e->pinned);
   cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -703,11 +741,34 @@ DevicePlan::~DevicePlan() {
   if (engine) cudaSetDevice(engine->device);
   for (auto& [k, g] : graphs)
     if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
-  if (h_xeb_part) cudaFreeHost(h_xeb_part);
-  if (d_xeb_part) cudaFree(d_xeb_part);
-  for (void* p : {d_leaves, static_cast<void*>(d_tables), static_cast<void*>(d_index),
-                  static_cast<void*>(d_slice_strides), static_cast<void*>(d_row_mult)})
-    if (p) cudaFree(p);
+  if (d_blob) {
+    if (engine) {
+      engine->blob_pool.emplace_back(d_blob, blob_bytes);
+      if (engine->blob_pool.size() > kBlobPoolMax) {
+        cudaFree(engine->blob_pool.front().first);
+        engine->blob_pool.erase(engine->blob_pool.begin());
+      }
+    } else {
+      cudaFree(d_blob);
+    }
+  }
+}
+
+// Pinned host staging owned by the engine (grown on demand): every H2D/D2H
+// of the one-shot path goes through it, so copies are truly asynchronous.
+void* engine_pinned(Engine* e, uint64_t bytes) {
+  if (e->pinned_bytes < bytes) {
+    if (e->pinned) {
+      CK(cudaStreamSynchronize(e->stream));
+      CK(cudaFreeHost(e->pinned));
+      e->pinned = nullptr;
+      e->pinned_bytes = 0;
+    }
+    const uint64_t want = std::max<uint64_t>(bytes, 1 << 20);
+    CK(cudaMallocHost(&e->pinned, want));
+    e->pinned_bytes = want;
+  }
+  return e->pinned;
 }
 
 std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
@@ -717,16 +778,44 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
   dp->c = std::move(c);
   Compiled& cc = dp->c;
   const size_t eb = cc.elem_bytes;
-  // leaves in the plan precision
-  CK(cudaMalloc(&dp->d_leaves, std::max<size_t>(cc.leaf_elems * eb, 16)));
+  // One device allocation and one copy for everything the plan keeps
+  // resident: leaves (in the plan precision) | offset tables | index arrays |
+  // row multiplicities | XEB partials.
+  auto up = [](uint64_t x) { return (x + 255) / 256 * 256; };
+  const uint64_t o_leaves = 0;
+  const uint64_t o_tables = up(o_leaves + std::max<uint64_t>(cc.leaf_elems * eb, 16));
+  const uint64_t o_index = up(o_tables + 4 * std::max<size_t>(cc.table_blob.size(), 1));
+  const uint64_t o_mult = up(o_index + 4 * std::max<size_t>(cc.index_blob.size(), 1));
+  const uint64_t o_xeb = up(o_mult + 4 * std::max<size_t>(cc.row_mult.size(), 1));
+  const uint64_t total = up(o_xeb + sizeof(double) * 2 * kXebBlocks);
+  uint8_t* h = static_cast<uint8_t*>(engine_pinned(e, total));
+  CK(cudaStreamSynchronize(e->stream));  // staging may still feed an earlier copy
   if (cc.precision == MTCG_C64) {
-    std::vector<float> tmp(2 * cc.leaf_elems);
-    for (size_t i = 0; i < tmp.size(); ++i) tmp[i] = static_cast<float>(cc.leaf_values[i]);
-    CK(cudaMemcpy(dp->d_leaves, tmp.data(), tmp.size() * sizeof(float), cudaMemcpyHostToDevice));
+    float* f = reinterpret_cast<float*>(h + o_leaves);
+    for (uint64_t i = 0; i < 2 * cc.leaf_elems; ++i) f[i] = static_cast<float>(cc.leaf_values[i]);
   } else {
-    CK(cudaMemcpy(dp->d_leaves, cc.leaf_values.data(), cc.leaf_values.size() * sizeof(double),
-                  cudaMemcpyHostToDevice));
+    std::memcpy(h + o_leaves, cc.leaf_values.data(), cc.leaf_values.size() * sizeof(double));
   }
+  std::memcpy(h + o_tables, cc.table_blob.data(), 4 * cc.table_blob.size());
+  std::memcpy(h + o_index, cc.index_blob.data(), 4 * cc.index_blob.size());
+  std::memcpy(h + o_mult, cc.row_mult.data(), 4 * cc.row_mult.size());
+  dp->d_blob = blob_get(e, total);
+  if (dp->d_blob) {
+    // a pooled blob may still be read by work its old plan queued on any
+    // stream (cudaFree would have waited for it too)
+    CK(cudaDeviceSynchronize());
+  } else {
+    CK(cudaMalloc(&dp->d_blob, total));
+  }
+  dp->blob_bytes = total;
+  CK(cudaMemcpyAsync(dp->d_blob, h, o_xeb, cudaMemcpyHostToDevice, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  uint8_t* d = static_cast<uint8_t*>(dp->d_blob);
+  dp->d_leaves = d + o_leaves;
+  dp->d_tables = reinterpret_cast<uint32_t*>(d + o_tables);
+  dp->d_index = reinterpret_cast<uint32_t*>(d + o_index);
+  dp->d_row_mult = reinterpret_cast<uint32_t*>(d + o_mult);
+  dp->d_xeb_part = reinterpret_cast<double*>(d + o_xeb);
   if (cc.arena_elems) {
     const uint64_t need = cc.arena_elems * eb;
     if (e->arena_bytes < need) {
@@ -741,18 +830,6 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
     }
     dp->d_arena = e->arena;
   }
-  CK(cudaMalloc(&dp->d_tables, std::max<size_t>(cc.table_blob.size(), 1) * 4));
-  if (!cc.table_blob.empty())
-    CK(cudaMemcpy(dp->d_tables, cc.table_blob.data(), cc.table_blob.size() * 4,
-                  cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&dp->d_index, std::max<size_t>(cc.index_blob.size(), 1) * 4));
-  if (!cc.index_blob.empty())
-    CK(cudaMemcpy(dp->d_index, cc.index_blob.data(), cc.index_blob.size() * 4,
-                  cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&dp->d_row_mult, std::max<size_t>(cc.row_mult.size(), 1) * 4));
-  if (!cc.row_mult.empty())
-    CK(cudaMemcpy(dp->d_row_mult, cc.row_mult.data(), cc.row_mult.size() * 4,
-                  cudaMemcpyHostToDevice));
   return dp;
 }
 
@@ -833,12 +910,9 @@ double xeb_device(DevicePlan& dp, const void* d_acc, int n_qubits, void* stream)
   const int r_out = static_cast<int>(c.out_legs.size());
   const uint64_t total = c.n_rows << r_out;
   const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, kXebBlocks)));
-  // partials: preallocated per plan (device + pinned host), no allocation on
-  // the timed path
-  if (!dp.d_xeb_part) {
-    CK(cudaMalloc(&dp.d_xeb_part, sizeof(double) * 2 * kXebBlocks));
-    CK(cudaMallocHost(&dp.h_xeb_part, sizeof(double) * 2 * kXebBlocks));
-  }
+  // partials: preallocated in the plan's blob; read back through the
+  // engine's pinned staging — no allocation on the timed path
+  double* h_part = static_cast<double*>(engine_pinned(dp.engine, sizeof(double) * 2 * kXebBlocks));
   if (c.precision == MTCG_C64)
     xeb_acc_kernel<float2><<<blocks, 256, 0, st>>>(static_cast<const float2*>(d_acc),
                                                    dp.d_row_mult, c.n_rows, r_out, dp.d_xeb_part);
@@ -846,10 +920,10 @@ double xeb_device(DevicePlan& dp, const void* d_acc, int n_qubits, void* stream)
     xeb_acc_kernel<double2><<<blocks, 256, 0, st>>>(static_cast<const double2*>(d_acc),
                                                     dp.d_row_mult, c.n_rows, r_out, dp.d_xeb_part);
   dp.engine->launches++;
-  CK(cudaMemcpyAsync(dp.h_xeb_part, dp.d_xeb_part, sizeof(double) * 2 * blocks,
+  CK(cudaMemcpyAsync(h_part, dp.d_xeb_part, sizeof(double) * 2 * blocks,
                      cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  const std::vector<double> part(dp.h_xeb_part, dp.h_xeb_part + 2 * blocks);
+  const std::vector<double> part(h_part, h_part + 2 * blocks);
   const double count = static_cast<double>(c.n_requests) * static_cast<double>(c.row_elems);
   return std::ldexp(finish_partials(part) / count, n_qubits) - 1.0;
 }
@@ -858,25 +932,41 @@ double xeb_probs(Engine* e, const double* probs, uint64_t count, int n_qubits, b
   CK(cudaSetDevice(e->device));
   cudaStream_t st = e->stream;
   const uint64_t words = amplitudes ? 2 * count : count;
-  double* d_in = nullptr;
-  double* d_part = nullptr;
-  int* d_neg = nullptr;
-  const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, 592)));
-  CK(cudaMallocAsync(&d_in, sizeof(double) * words, st));
-  CK(cudaMallocAsync(&d_part, sizeof(double) * 2 * blocks, st));
-  CK(cudaMallocAsync(&d_neg, sizeof(int), st));
+  const int blocks = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((count + 255) / 256, kXebBlocks)));
+  // device scratch: [inputs | partials | negative flag], cached on the engine
+  const uint64_t in_bytes = (sizeof(double) * words + 255) / 256 * 256;
+  const uint64_t need = in_bytes + sizeof(double) * 2 * kXebBlocks + 256;
+  if (e->scratch_bytes < need) {
+    if (e->scratch) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaFree(e->scratch));
+      e->scratch = nullptr;
+      e->scratch_bytes = 0;
+    }
+    CK(cudaMalloc(&e->scratch, need));
+    e->scratch_bytes = need;
+  }
+  uint8_t* base = static_cast<uint8_t*>(e->scratch);
+  double* d_in = reinterpret_cast<double*>(base);
+  double* d_part = reinterpret_cast<double*>(base + in_bytes);
+  int* d_neg = reinterpret_cast<int*>(base + in_bytes + sizeof(double) * 2 * kXebBlocks);
+  // inputs go through pinned staging (one host memcpy + one async DMA)
+  uint8_t* h = static_cast<uint8_t*>(engine_pinned(e, std::max<uint64_t>(sizeof(double) * words, need - in_bytes)));
+  CK(cudaStreamSynchronize(st));
+  std::memcpy(h, probs, sizeof(double) * words);
   CK(cudaMemsetAsync(d_neg, 0, sizeof(int), st));
-  CK(cudaMemcpyAsync(d_in, probs, sizeof(double) * words, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_in, h, sizeof(double) * words, cudaMemcpyHostToDevice, st));
   xeb_probs_kernel<<<blocks, 256, 0, st>>>(d_in, count, amplitudes ? 1 : 0, d_part, d_neg);
   e->launches++;
-  std::vector<double> part(2 * blocks);
-  int neg = 0;
-  CK(cudaMemcpyAsync(part.data(), d_part, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(&neg, d_neg, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaFreeAsync(d_in, st));
-  CK(cudaFreeAsync(d_part, st));
-  CK(cudaFreeAsync(d_neg, st));
+  CK(cudaGetLastError());
+  // partials + flag back through the same staging (the H2D above is ordered
+  // before this D2H on the stream, so reusing the buffer is safe)
+  CK(cudaMemcpyAsync(h, d_part, sizeof(double) * 2 * kXebBlocks + sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  const double* hp = reinterpret_cast<const double*>(h);
+  std::vector<double> part(hp, hp + 2 * blocks);
+  int neg = 0;
+  std::memcpy(&neg, h + sizeof(double) * 2 * kXebBlocks, sizeof(int));
   if (neg) throw DataError("negative probability");
   return std::ldexp(finish_partials(part) / static_cast<double>(count), n_qubits) - 1.0;
 }
@@ -896,8 +986,11 @@ void device_free(Engine* e, void* p) {
 void copy_to_host(Engine* e, void* dst, const void* src, uint64_t bytes, void* stream) {
   CK(cudaSetDevice(e->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->stream;
-  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+  void* h = engine_pinned(e, bytes);
+  CK(cudaStreamSynchronize(e->stream));
+  CK(cudaMemcpyAsync(h, src, bytes, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  std::memcpy(dst, h, bytes);
 }
 
 }  // namespace mtcg

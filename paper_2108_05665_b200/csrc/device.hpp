@@ -24,10 +24,10 @@ struct DevicePlan {
   void* d_arena = nullptr;
   uint32_t* d_tables = nullptr;
   uint32_t* d_index = nullptr;
-  uint64_t* d_slice_strides = nullptr;  // per op: S strides for A then B
   uint32_t* d_row_mult = nullptr;
   double* d_xeb_part = nullptr;         // fused-XEB block partials (device)
-  double* h_xeb_part = nullptr;         // ... and their pinned host copy
+  void* d_blob = nullptr;               // one allocation behind the pointers above
+  uint64_t blob_bytes = 0;
   std::vector<uint64_t> op_slice_off;   // word offset of each op's strides
   uint64_t leaf_root_slice_off = 0;
   // Instantiated CUDA graphs of whole slice ranges, keyed by
