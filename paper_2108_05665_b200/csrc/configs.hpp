@@ -34,6 +34,11 @@ constexpr int kTileK128 = 8;
 constexpr int kRowsConfig = 11;
 // tcgen05 3xTF32 complex GEMM (dense ops, complex64 only; tc_gemm.cu).
 constexpr int kTcConfig = 12;
+// Row-streaming kernel over groups of items that share their A entry: each
+// A row is read once and multiplied by every item's B of the group.
+constexpr int kRowsGroupedConfig = 13;
+// shared-memory budget for one group's B blocks (bytes)
+constexpr int kGroupSmemBytes = 48 * 1024;
 
 inline int select_config(int fa, int fb, int kc = 0) {
   // fa >= fb by construction (A is the side with more free legs).

@@ -160,6 +160,9 @@ struct DevOp {
   int accumulate;           // root: add into the accumulator
   int a_kcontig;            // rows kernel: A rows K-contiguous
   int o_ncontig;            // rows kernel: output n contiguous
+  const uint32_t* grp_items;  // grouped rows kernel: items ordered by A entry
+  const uint32_t* grp_start;  // ... CSR offsets per group
+  uint32_t n_groups, grp_max;
 };
 
 // ---- tiled batched contraction -------------------------------------------------
@@ -382,6 +385,116 @@ __global__ void __launch_bounds__(256, 2)
   }  // chunk loop
 }
 
+// ---- skinny contractions over groups of items sharing one A entry ---------------
+//
+// The items of a group differ only in B (and the output): each thread loads
+// its RPT A rows once (K complex each, in registers), then loops over the
+// group's items with every item's K x N block of B resident in shared memory.
+// A is read from HBM once per distinct entry instead of once per item. Per
+// output the k loop runs in the same order as contract_rows, so results are
+// identical to it (and C128 stays bit-identical to the reference).
+
+template <class R, int K, int N, int RPT>
+__global__ void __launch_bounds__(256, 2)
+    contract_rows_grouped(const DevOp<typename V2<R>::T> op) {
+  using T = typename V2<R>::T;
+  using V4 = typename Vec4<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Bs = reinterpret_cast<T*>(smem_raw);                  // [g][K][N]
+  uint32_t* kao = reinterpret_cast<uint32_t*>(Bs + op.grp_max * K * N);
+  uint32_t* ono = kao + K;
+  uint32_t* items = ono + N;                               // [g]
+  const uint64_t group = blockIdx.y + uint64_t{gridDim.y} * blockIdx.z;
+  if (group >= op.n_groups) return;
+  const uint32_t g0 = __ldg(op.grp_start + group);
+  const int g = static_cast<int>(__ldg(op.grp_start + group + 1) - g0);
+  for (int i = threadIdx.x; i < g; i += blockDim.x) items[i] = __ldg(op.grp_items + g0 + i);
+  __syncthreads();
+  const uint32_t item0 = items[0];
+  const T* A = op.a + uint64_t{op.ia ? __ldg(op.ia + item0) : item0} * op.a_item + op.a_slice;
+  for (int e = threadIdx.x; e < g * K * N; e += blockDim.x) {
+    const int i = e / (K * N), r = e - i * (K * N);
+    const int k = r / N, n = r - k * N;
+    const uint32_t it = items[i];
+    const T* B = op.b + uint64_t{op.ib ? __ldg(op.ib + it) : it} * op.b_item + op.b_slice;
+    Bs[e] = B[op.tbn(n) + op.tbk(k)];
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) kao[k] = op.tak(k);
+  for (int n = threadIdx.x; n < N; n += blockDim.x) ono[n] = op.ton(n);
+  __syncthreads();
+  const uint64_t M = uint64_t{1} << op.fa;
+  const uint64_t n_chunks = (M + 256 * RPT - 1) / (256 * RPT);
+  for (uint64_t chunk = blockIdx.x; chunk < n_chunks; chunk += gridDim.x) {
+    const uint64_t base = chunk * (256 * RPT) + threadIdx.x;
+    bool live[RPT];
+    uint32_t mo[RPT];
+    T av[RPT][K];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      const uint64_t m = base + j * 256;
+      live[j] = m < M;
+      const T* row = A + (live[j] ? op.tam(m) : 0u);
+      mo[j] = live[j] ? op.tom(m) : 0u;
+      if (K >= 2 && op.a_kcontig) {
+#pragma unroll
+        for (int kk = 0; kk < K; kk += 2) {
+          const V4 v = live[j] ? *reinterpret_cast<const V4*>(row + kk) : V4{};
+          av[j][kk] = T{v.x, v.y};
+          av[j][kk + 1] = T{v.z, v.w};
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) av[j][kk] = live[j] ? row[kao[kk]] : czero<T>();
+      }
+    }
+    // per item, per pair of n: one 16-byte broadcast B load feeds 8 x RPT
+    // FMAs (the shared-memory pipe, not the FMA pipe, bounds smaller ratios)
+    constexpr int NP = N >= 2 ? 2 : 1;
+    for (int i = 0; i < g; ++i) {
+      const uint32_t it = items[i];
+      T* O = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + it)} : it) * op.out_item;
+      const T* Bi = Bs + i * K * N;
+#pragma unroll
+      for (int n0 = 0; n0 < N; n0 += NP) {
+        T acc[RPT][NP];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          T bv[NP];
+          if (NP == 2) {
+            const V4 v = *reinterpret_cast<const V4*>(Bi + kk * N + n0);
+            bv[0] = T{v.x, v.y};
+            bv[NP - 1] = T{v.z, v.w};
+          } else {
+            bv[0] = Bi[kk * N + n0];
+          }
+#pragma unroll
+          for (int j = 0; j < RPT; ++j)
+#pragma unroll
+            for (int n = 0; n < NP; ++n) {
+              if (kk == 0) acc[j][n] = czero<T>();
+              cmac(acc[j][n], av[j][kk], bv[n], kk == 0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+          if (!live[j]) continue;
+          T* dst = O + mo[j];
+          if (NP == 2 && op.o_ncontig && !op.accumulate) {
+            *reinterpret_cast<V4*>(dst + n0) =
+                V4{acc[j][0].x, acc[j][0].y, acc[j][NP - 1].x, acc[j][NP - 1].y};
+          } else {
+#pragma unroll
+            for (int n = 0; n < NP; ++n) {
+              T* d = dst + ono[n0 + n];
+              *d = op.accumulate ? cadd(*d, acc[j][n]) : acc[j][n];
+            }
+          }
+        }
+      }
+    }
+  }  // chunk loop
+}
+
 // ---- one thread per output element ---------------------------------------------
 
 template <class R>
@@ -570,10 +683,58 @@ void launch_rows(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
   }
 }
 
+template <class R, int K, int N>
+void launch_rows_grouped_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
+  using T = typename V2<R>::T;
+  // rows per thread: RPT x K complex of A in registers
+  constexpr int RA = sizeof(R) == 8 ? 16 : 32;
+  constexpr int RPT0 = RA / K;
+  constexpr int RPT = RPT0 < 1 ? 1 : (RPT0 > 8 ? 8 : RPT0);
+  const size_t smem = sizeof(T) * op.grp_max * K * N + sizeof(uint32_t) * (K + N + op.grp_max);
+  auto kern = contract_rows_grouped<R, K, N, RPT>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            kGroupSmemBytes + 48 * 1024));
+    attr_set = true;
+  }
+  const uint64_t M = uint64_t{1} << op.fa;
+  const uint64_t n_chunks = (M + 256 * RPT - 1) / (256 * RPT);
+  const uint64_t want = std::max<uint64_t>(1, (148 * 16 + op.n_groups - 1) / op.n_groups);
+  const unsigned gx = static_cast<unsigned>(std::min<uint64_t>(n_chunks, want));
+  const unsigned gy = std::min<uint32_t>(op.n_groups, 65535u);
+  const unsigned gz = (op.n_groups + gy - 1) / gy;
+  kern<<<dim3(gx, gy, gz), 256, smem, st>>>(op);
+}
+
+template <class R, int K>
+void launch_rows_grouped_k(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
+  switch (op.fb) {
+    case 0: return launch_rows_grouped_kn<R, K, 1>(op, st);
+    case 1: return launch_rows_grouped_kn<R, K, 2>(op, st);
+    case 2: return launch_rows_grouped_kn<R, K, 4>(op, st);
+    case 3: return launch_rows_grouped_kn<R, K, 8>(op, st);
+    default: return launch_rows_grouped_kn<R, K, 16>(op, st);
+  }
+}
+
+template <class R>
+void launch_rows_grouped(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
+  switch (op.kc) {
+    case 0: return launch_rows_grouped_k<R, 1>(op, st);
+    case 1: return launch_rows_grouped_k<R, 2>(op, st);
+    case 2: return launch_rows_grouped_k<R, 4>(op, st);
+    case 3: return launch_rows_grouped_k<R, 8>(op, st);
+    case 4: return launch_rows_grouped_k<R, 16>(op, st);
+    default: return launch_rows_grouped_k<R, 32>(op, st);
+  }
+}
+
 template <class R>
 void launch_op(const DevOp<typename V2<R>::T>& op, int config, cudaStream_t st) {
   switch (config) {
     case kRowsConfig: return launch_rows<R>(op, st);
+    case kRowsGroupedConfig: return launch_rows_grouped<R>(op, st);
     case 1: return launch_tile<R, 128, 64, 8, 4>(op, st);
     case 2: return launch_tile<R, 128, 32, 8, 2>(op, st);
     case 3: return launch_tile<R, 128, 16, 4, 2>(op, st);
@@ -646,6 +807,10 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
       d.n_fast = op.store_n_fast ? 1 : 0;
       d.a_kcontig = op.a_kcontig ? 1 : 0;
       d.o_ncontig = op.o_ncontig ? 1 : 0;
+      d.grp_items = dp.d_index + op.grp_items_off;
+      d.grp_start = dp.d_index + op.grp_start_off;
+      d.n_groups = op.grp_start.empty() ? 0 : static_cast<uint32_t>(op.grp_start.size() - 1);
+      d.grp_max = op.grp_max;
       d.accumulate = op.root ? acc_flag : 0;
       if constexpr (sizeof(R) == 4) {
         if (op.config == kTcConfig) {

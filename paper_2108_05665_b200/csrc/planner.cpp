@@ -598,6 +598,33 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       }
     }
     if (tc_ok && tc_listed) op.config = kTcConfig;
+    // Items that share their A entry (a distinct A rank feeding several
+    // distinct ranks of this node) are grouped so each A row streams from HBM
+    // once for the whole group; for rows-shaped ops this beats both the
+    // per-item rows kernel (A re-read per item) and the tensor path (which
+    // re-reads A per item too). MTCG_NO_GROUP=1 disables it (A/B tuning).
+    if (op.nb >= 2 && op.fb <= 4 && op.kc <= 5 && op.fa >= 8 &&
+        (op.config == kRowsConfig || op.config == kTcConfig) && !std::getenv("MTCG_NO_GROUP")) {
+      std::vector<uint32_t> order(op.nb);
+      std::iota(order.begin(), order.end(), 0u);
+      std::stable_sort(order.begin(), order.end(),
+                       [&](uint32_t x, uint32_t y) { return op.ia[x] < op.ia[y]; });
+      std::vector<uint32_t> start{0};
+      uint32_t gmax = 0;
+      for (uint32_t i = 1; i <= op.nb; ++i)
+        if (i == op.nb || op.ia[order[i]] != op.ia[order[i - 1]]) {
+          gmax = std::max(gmax, i - start.back());
+          start.push_back(i);
+        }
+      const uint64_t groups = start.size() - 1;
+      const uint64_t b_bytes = (uint64_t{gmax} << (op.fb + op.kc)) * c.elem_bytes;
+      if (2 * op.nb >= 3 * groups && b_bytes <= kGroupSmemBytes) {
+        op.config = kRowsGroupedConfig;
+        op.grp_items = std::move(order);
+        op.grp_start = std::move(start);
+        op.grp_max = gmax;
+      }
+    }
     // m / n bit orders: free legs by increasing address in the output layout;
     // the tensor-core path walks A rows in A's memory order instead (TMA rows)
     std::vector<uint32_t> m_legs = by_out_addr(fa_legs);
@@ -738,6 +765,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       put_table(*t);
     op.ia_off = put_index(op.ia);
     op.ib_off = put_index(op.ib);
+    op.grp_items_off = put_index(op.grp_items);
+    op.grp_start_off = put_index(op.grp_start);
     op.out_rows_off = put_index(op.out_rows);
   }
   if (c.has_leaf_root) {
@@ -745,6 +774,18 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     c.leaf_root.rows_off = put_index(c.leaf_root.row_value);
   }
   timer.mark("blobs");
+  if (std::getenv("MTCG_DUMP_OPS")) {
+    for (const Op& op : c.ops) {
+      std::vector<uint32_t> a(op.ia), b(op.ib);
+      std::sort(a.begin(), a.end());
+      std::sort(b.begin(), b.end());
+      const auto da = std::unique(a.begin(), a.end()) - a.begin();
+      const auto db = std::unique(b.begin(), b.end()) - b.begin();
+      std::fprintf(stderr, "[mtcg] op node %d M2^%d N2^%d K2^%d batch %u distinct_a %ld distinct_b %ld cfg %d%s\n",
+                   op.node, op.fa, op.fb, op.kc, op.nb, (long)da, (long)db, op.config,
+                   op.root ? " root" : "");
+    }
+  }
   return c;
 }
 

@@ -63,6 +63,11 @@ struct Op {
   bool store_n_fast = true;        // epilogue lane order
   std::vector<uint32_t> out_rows;  // root: item -> accumulator row
   uint64_t out_rows_off = 0;
+  // grouped rows kernel: items sharing one A entry, CSR by A entry
+  std::vector<uint32_t> grp_items;  // item ids ordered by A entry
+  std::vector<uint32_t> grp_start;  // n_groups + 1 offsets into grp_items
+  uint32_t grp_max = 0;             // largest group
+  uint64_t grp_items_off = 0, grp_start_off = 0;
   int config = 0;                  // kernel tile configuration
   uint64_t a_entries = 0;          // tensor-core path: entries in A's table
   uint64_t scratch_off = 0;        // tensor-core path: arena scratch (elements)

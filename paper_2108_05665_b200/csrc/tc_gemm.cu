@@ -40,6 +40,7 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;        // floats per stage row (128 B: one swizzle row)
+static_assert(kBK == 32, "mma_stage issues exactly 4 k-steps of 8 per stage");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -117,6 +118,45 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// One stage (BK = 32 floats = 4 k-steps of 8) of the 3xTF32 product into one
+// accumulator: per k-step lo*hi, hi*lo, hi*hi; descriptors advance 32 bytes
+// (+2 in the encoded address) per k-step. Issued by one elected lane of a
+// converged warp; `acc` = 0 starts a fresh accumulation.
+__device__ __forceinline__ void mma_stage(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi,
+                                          uint64_t blo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b64 ah1, ah2, ah3, al1, al2, al3, bh1, bh2, bh3, bl1, bl2, bl3;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "add.s64 ah1, %1, 2;\n\tadd.s64 ah2, %1, 4;\n\tadd.s64 ah3, %1, 6;\n\t"
+      "add.s64 al1, %2, 2;\n\tadd.s64 al2, %2, 4;\n\tadd.s64 al3, %2, 6;\n\t"
+      "add.s64 bh1, %3, 2;\n\tadd.s64 bh2, %3, 4;\n\tadd.s64 bh3, %3, 6;\n\t"
+      "add.s64 bl1, %4, 2;\n\tadd.s64 bl2, %4, 4;\n\tadd.s64 bl3, %4, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, bh1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, bl1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, bh1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al2, bh2, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah2, bl2, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah2, bh2, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al3, bh3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah3, bl3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah3, bh3, %5, 1;\n\t}" ::"r"(d),
+      "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
 struct TcTable {
   const uint32_t* lo;
   const uint32_t* hi;
@@ -190,7 +230,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
                        const __grid_constant__ CUtensorMap map_blo, const TcParams p,
                        int n_stages) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+  // 1024-byte aligned ring base; pointer arithmetic on the __shared__ array
+  // (not an integer round trip) keeps the shared address space visible to the
+  // compiler, so smem accesses below compile to LDS/STS rather than generic
+  // LD/ST through L1.
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int a_bytes = kBM * kBK * 4;
   const int b_bytes = p.bn * kBK * 4;
   const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
@@ -280,37 +324,30 @@ __global__ void __launch_bounds__(kPThreads, 1)
         trace(p, pit, 1);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer ----
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                             (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
-      uint64_t g = 0, it = 0;
-      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-        const uint32_t tb = static_cast<uint32_t>(it % n_acc);
-        if (it >= n_acc) mbar_wait(&acc_empty[tb], static_cast<uint32_t>((it / n_acc) - 1) & 1);
-        trace(p, it, 2);
+  } else if (warp == 1) {  // ---- MMA issuer: the whole warp loops, one lane issues ----
+    // (a single-thread branch makes ptxas wrap every tcgen05.mma in an
+    // elect/R2UR loop: ~147 cycles per MMA instead of the ~40-cycle shared-
+    // memory operand-read floor of a 128 x N x 8 tf32 MMA; tools/mma_bench.cu)
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                           (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
+    uint64_t g = 0, it = 0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const uint32_t tb = static_cast<uint32_t>(it % n_acc);
+      if (it >= n_acc) mbar_wait(&acc_empty[tb], static_cast<uint32_t>((it / n_acc) - 1) & 1);
+      if (lane == 0) trace(p, it, 2);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dacc = tmem + tb * buf_cols;
+      for (int s = 0; s < k_stages; ++s, ++g) {
+        const int st = static_cast<int>(g % n_stages);
+        mbar_wait(&conv[st], static_cast<uint32_t>(g / n_stages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dacc = tmem + tb * buf_cols;
-        for (int s = 0; s < k_stages; ++s, ++g) {
-          const int st = static_cast<int>(g % n_stages);
-          mbar_wait(&conv[st], static_cast<uint32_t>(g / n_stages) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sp = smem_u32(base + st * stage_bytes);
-          const uint32_t ahi = sp, alo = sp + a_bytes, bhi = sp + 2 * a_bytes,
-                         blo = sp + 2 * a_bytes + b_bytes;
-#pragma unroll
-          for (int kk = 0; kk < kBK / 8; ++kk) {
-            const uint32_t off = kk * 32;
-            const uint32_t acc0 = (s > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32(dacc, sw128_desc(alo + off), sw128_desc(bhi + off), idesc, acc0);
-            mma_tf32(dacc, sw128_desc(ahi + off), sw128_desc(blo + off), idesc, 1u);
-            mma_tf32(dacc, sw128_desc(ahi + off), sw128_desc(bhi + off), idesc, 1u);
-          }
-          mma_commit(&empty[st]);
-        }
-        mma_commit(&acc_full[tb]);
-        trace(p, it, 3);
+        const uint32_t sp = smem_u32(base + st * stage_bytes);
+        mma_stage(dacc, sw128_desc(sp), sw128_desc(sp + a_bytes), sw128_desc(sp + 2 * a_bytes),
+                  sw128_desc(sp + 2 * a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
+        mma_commit_elect(&empty[st]);
       }
+      mma_commit_elect(&acc_full[tb]);
+      if (lane == 0) trace(p, it, 3);
     }
   } else if (warp < 6) {  // ---- converters ----
     const int ct = threadIdx.x - 64;
