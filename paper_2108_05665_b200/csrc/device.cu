@@ -833,7 +833,12 @@ void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool ac
           t.tbk_lo = d.tbk.lo;
           t.tbk_hi = d.tbk.hi;
           t.tbk_bits = d.tbk.lo_bits;
-          const uint64_t bhat_elems = uint64_t{op.nb} << (op.fb + op.kc + 1);
+          t.grp_items = op.grp_max ? d.grp_items : nullptr;
+          t.grp_start = op.grp_max ? d.grp_start : nullptr;
+          t.n_groups = op.grp_max ? d.n_groups : 0;
+          t.slots = op.grp_max;
+          const uint64_t units = op.grp_max ? uint64_t{d.n_groups} * op.grp_max : op.nb;
+          const uint64_t bhat_elems = units << (op.fb + op.kc + 1);
           t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off);
           t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + bhat_elems);
           t.out = reinterpret_cast<float2*>(d.out);

@@ -577,13 +577,55 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     // moved: above that the CUDA-core kernels are FMA-bound while the tensor
     // path (A read once, split in smem) stays near the HBM roofline; below it
     // the streaming kernels win.
-    const double Md = std::ldexp(1.0, op.fa), Nd = std::ldexp(1.0, op.fb),
+    // Items that share their A entry (a distinct A rank feeding several
+    // distinct ranks of this node) form groups (CSR by A entry) so each A row
+    // streams from HBM once per group: the group is one GEMM whose N is the
+    // concatenation of its items' B blocks (N_eff = slots x N, slots = the
+    // largest group, padded so 2 N_eff is a multiple of 32 for the tensor
+    // path). MTCG_NO_GROUP=1 disables grouping (A/B tuning).
+    std::vector<uint32_t> g_order, g_start;
+    uint32_t g_max = 0;
+    if (op.nb >= 2 && !std::getenv("MTCG_NO_GROUP")) {
+      g_order.resize(op.nb);
+      std::iota(g_order.begin(), g_order.end(), 0u);
+      std::stable_sort(g_order.begin(), g_order.end(),
+                       [&](uint32_t x, uint32_t y) { return op.ia[x] < op.ia[y]; });
+      g_start.push_back(0);
+      for (uint32_t i = 1; i <= op.nb; ++i)
+        if (i == op.nb || op.ia[g_order[i]] != op.ia[g_order[i - 1]]) {
+          g_max = std::max(g_max, i - g_start.back());
+          g_start.push_back(i);
+        }
+      if (2 * uint64_t{op.nb} < 3 * (g_start.size() - 1)) {  // < 1.5 items per group
+        g_order.clear();
+        g_start.clear();
+        g_max = 0;
+      }
+    }
+    const bool grouped = g_max > 0;
+    // tensor-path slots per group: 2 N x slots a multiple of 32 real columns
+    uint32_t tc_slots = g_max;
+    if (grouped && op.fb < 4) {
+      const uint32_t q = 16u >> op.fb;  // slots per 32 real columns
+      tc_slots = (g_max + q - 1) / q * q;
+    }
+    // Tensor-core path (complex64 only): dense, K-contiguous intermediate A,
+    // shapes the 128 x (2N) x (2K) real tiles cover exactly.
+    // Ops with intensity MNK / (MK + NK + MN) >= 6 complex MACs per element
+    // moved: above that the CUDA-core kernels are FMA-bound while the tensor
+    // path (A read once, split in smem) stays near the HBM roofline; below it
+    // the streaming kernels win. Grouped ops are judged on N_eff and need
+    // M >= 4096 (short groups are dominated by per-unit epilogue/B̂ setup).
+    const int fb_eff = grouped ? op.fb + static_cast<int>(std::ceil(std::log2(double(tc_slots))))
+                               : op.fb;
+    const double Md = std::ldexp(1.0, op.fa), Nd = std::ldexp(1.0, fb_eff),
                  Kd = std::ldexp(1.0, op.kc);
     const double intensity = Md * Nd * Kd / (Md * Kd + Nd * Kd + Md * Nd);
+    const uint64_t units = grouped ? uint64_t{g_start.size() - 1} : op.nb;
     const bool tc_ok = c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) &&
-                       !op.a_leaf && op.fa >= 7 && op.fb >= tc_min_fb && op.kc >= 4 &&
-                       intensity >= 6.0 &&
-                       (uint64_t{op.nb} << (op.fa + op.fb + op.kc)) >= (uint64_t{1} << 26);
+                       !op.a_leaf && op.fa >= 7 && fb_eff >= tc_min_fb && op.kc >= 4 &&
+                       fb_eff <= 12 && intensity >= 6.0 && (!grouped || op.fa >= 12) &&
+                       (units << (op.fa + fb_eff + op.kc)) >= (uint64_t{1} << 26);
     // MTCG_TC_ONLY=<node>[,<node>...] restricts the tensor path (diagnostics)
     const char* tc_only = std::getenv("MTCG_TC_ONLY");
     bool tc_listed = true;
@@ -597,33 +639,17 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         s = *end ? end + 1 : end;
       }
     }
-    if (tc_ok && tc_listed) op.config = kTcConfig;
-    // Items that share their A entry (a distinct A rank feeding several
-    // distinct ranks of this node) are grouped so each A row streams from HBM
-    // once for the whole group; for rows-shaped ops this beats both the
-    // per-item rows kernel (A re-read per item) and the tensor path (which
-    // re-reads A per item too). MTCG_NO_GROUP=1 disables it (A/B tuning).
-    if (op.nb >= 2 && op.fb <= 4 && op.kc <= 5 && op.fa >= 8 &&
-        (op.config == kRowsConfig || op.config == kTcConfig) && !std::getenv("MTCG_NO_GROUP")) {
-      std::vector<uint32_t> order(op.nb);
-      std::iota(order.begin(), order.end(), 0u);
-      std::stable_sort(order.begin(), order.end(),
-                       [&](uint32_t x, uint32_t y) { return op.ia[x] < op.ia[y]; });
-      std::vector<uint32_t> start{0};
-      uint32_t gmax = 0;
-      for (uint32_t i = 1; i <= op.nb; ++i)
-        if (i == op.nb || op.ia[order[i]] != op.ia[order[i - 1]]) {
-          gmax = std::max(gmax, i - start.back());
-          start.push_back(i);
-        }
-      const uint64_t groups = start.size() - 1;
-      const uint64_t b_bytes = (uint64_t{gmax} << (op.fb + op.kc)) * c.elem_bytes;
-      if (2 * op.nb >= 3 * groups && b_bytes <= kGroupSmemBytes) {
-        op.config = kRowsGroupedConfig;
-        op.grp_items = std::move(order);
-        op.grp_start = std::move(start);
-        op.grp_max = gmax;
-      }
+    if (tc_ok && tc_listed) {
+      op.config = kTcConfig;
+      if (grouped) op.grp_max = tc_slots;
+    } else if (grouped && op.fb <= 4 && op.kc <= 5 && op.fa >= 8 &&
+               ((uint64_t{g_max} << (op.fb + op.kc)) * c.elem_bytes) <= kGroupSmemBytes) {
+      op.config = kRowsGroupedConfig;
+      op.grp_max = g_max;
+    }
+    if (op.grp_max) {
+      op.grp_items = std::move(g_order);
+      op.grp_start = std::move(g_start);
     }
     // m / n bit orders: free legs by increasing address in the output layout;
     // the tensor-core path walks A rows in A's memory order instead (TMA rows)
@@ -713,7 +739,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     if (op.config == kTcConfig && op.nb > 0) {
       // scratch: B̂ hi/lo (2N x 2K floats per item each)
       op.a_entries = ti.distinct[op.child_a];
-      const uint64_t bhat = uint64_t{op.nb} << (op.fb + op.kc + 1);
+      const uint64_t units = op.grp_max ? uint64_t{op.grp_start.size() - 1} * op.grp_max : op.nb;
+      const uint64_t bhat = units << (op.fb + op.kc + 1);
       op.scratch_elems = 2 * bhat;  // B̂ hi / lo (A is split in shared memory)
       op.scratch_off = alloc(op.scratch_elems, node);
       release(op.scratch_off, op.scratch_elems);  // free again once the op is done

@@ -89,21 +89,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
          (uint64_t{1} << 46) | (uint64_t{2} << 61);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -180,6 +165,13 @@ struct TcParams {
   int m_contig;              // tom(m + 1) = tom(m) + 1: lanes (rows) store coalesced
   int transpose;             // epilogue transposes 32-row chunks through smem
   unsigned long long* dbg;   // MTCG_TC_TRACE: per-tile role timestamps of CTA 0
+  // grouped mode (slots > 0): unit = group of items sharing the A entry;
+  // complex column c of a unit -> item grp_items[grp_start[u] + (c >> fb)],
+  // item column c & (2^fb - 1)
+  const uint32_t* grp_items;
+  const uint32_t* grp_start;
+  int slots;
+  int fb;
 };
 
 // Role timestamps of CTA 0's first kTraceTiles tiles (MTCG_TC_TRACE=<node>).
@@ -192,15 +184,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  return __uint_as_float(h);
-}
-
-// Same rounding (to nearest, ties away from zero, on the magnitude) with two
-// integer ALU ops instead of the low-throughput conversion; identical for
-// every finite input whose rounding does not overflow.
+// cvt.rna.tf32.f32 rounding (to nearest, ties away from zero, on the
+// magnitude) with two integer ALU ops instead of the low-throughput
+// conversion; identical for every finite input whose rounding does not
+// overflow.
 __device__ __forceinline__ float tf32_rna_alu(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
@@ -223,6 +210,7 @@ constexpr int kPThreads = 192 + 128 * kEpiGroups;
 constexpr int kMaxStages = 8;
 constexpr int kMaxAcc = 8;          // TMEM accumulator buffers
 constexpr int kMaxTonCache = 2048;  // output column offsets cached in smem
+constexpr int kMaxBn = 256;         // real columns per tile
 
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_persistent(const __grid_constant__ CUtensorMap map_a,
@@ -247,7 +235,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // output column offsets of all n (if N <= kMaxTonCache), then the epilogue's
   // transpose buffers (8 warps x 32 x 33 floats) when output rows are strided
   uint32_t* ton_s = tmem_slot + 4;
-  float* stage_out = reinterpret_cast<float*>(ton_s + min(p.Nr / 2, kMaxTonCache));
+  const int n_item_cols = p.slots ? (1 << p.fb) : p.Nr / 2;  // columns of one item
+  // per epilogue group: output offset of each complex column of its tile
+  // (ton_s is 8-byte aligned; an even count keeps coff_s 8-byte aligned)
+  int64_t* coff_s = reinterpret_cast<int64_t*>(ton_s + ((min(n_item_cols, kMaxTonCache) + 1) & ~1));
+  float* stage_out = reinterpret_cast<float*>(coff_s + kEpiGroups * (kMaxBn / 2));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
@@ -261,10 +253,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint32_t n_acc = min(static_cast<uint32_t>(kMaxAcc), 512u / buf_cols);
   uint32_t tmem_cols = 32;
   while (tmem_cols < n_acc * buf_cols) tmem_cols <<= 1;
-  const int n_cols = p.Nr / 2;
-  const bool ton_cached = n_cols <= kMaxTonCache;
+  const bool ton_cached = n_item_cols <= kMaxTonCache;
   if (ton_cached)
-    for (int n = threadIdx.x; n < n_cols; n += blockDim.x) ton_s[n] = p.ton(n);
+    for (int n = threadIdx.x; n < n_item_cols; n += blockDim.x) ton_s[n] = p.ton(n);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
@@ -305,9 +296,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         int m0, n0;
         tile_coords(t, item, m0, n0);
         trace(p, pit, 0);
-        if (item != cached_item) {  // items change every tiles_m * tiles_n tiles
+        if (item != cached_item) {  // units change every tiles_m * tiles_n tiles
           cached_item = item;
-          a_entry = p.ia ? p.ia[item] : item;
+          const uint32_t first = p.slots ? p.grp_items[p.grp_start[item]] : item;
+          a_entry = p.ia ? p.ia[first] : first;
         }
         const int a_row0 = static_cast<int>(a_entry * static_cast<uint64_t>(p.M)) + m0;
         const int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
@@ -376,39 +368,66 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const int eg = (warp - 6) / 4;  // epilogue group
     const int quarter = warp % 4;   // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
-    // the group's first tile; the next tile's row offset is fetched while the
-    // current one drains so the dependent table loads overlap the wait
+    int64_t* coff = coff_s + eg * (kMaxBn / 2);
+    // Output offset of complex column r of a tile (unit u, first real column
+    // n0), -1 for a padding slot: depends only on (u, n0), so it is
+    // recomputed (dependent index loads) only when that key changes.
+    auto col_offset = [&](uint32_t u, int n0c) -> int64_t {
+      if (r >= p.bn / 2) return -1;
+      const int c = n0c + r;
+      uint32_t item = u;
+      int n = c;
+      if (p.slots) {
+        const uint32_t g0 = p.grp_start[u], g = p.grp_start[u + 1] - g0;
+        const uint32_t slot = static_cast<uint32_t>(c) >> p.fb;
+        if (slot >= g) return -1;
+        item = p.grp_items[g0 + slot];
+        n = c & ((1 << p.fb) - 1);
+      }
+      const uint64_t entry = p.out_rows ? uint64_t{p.out_rows[item]} : uint64_t{item};
+      return static_cast<int64_t>(entry * p.out_item + (ton_cached ? ton_s[n] : p.ton(n)));
+    };
+    // the group's first tile; the next tile's row offset (and column offsets
+    // when its key changes) is fetched while the current one drains
     uint64_t t = blockIdx.x + uint64_t{static_cast<uint32_t>(eg)} * gridDim.x;
     uint64_t it = eg;
-    uint32_t item = 0, nxt_item = 0;
-    int m0 = 0, n0 = 0, nxt_m0 = 0, nxt_n0 = 0;
+    uint32_t nxt_unit = 0;
+    int m0 = 0, nxt_m0 = 0, nxt_n0 = 0;
     uint32_t om = 0, nxt_om = 0;
-    uint64_t out_entry = 0, nxt_out = 0;
+    uint64_t key = ~uint64_t{0}, nxt_key = ~uint64_t{0}, table_key = ~uint64_t{0};
+    int64_t my_coff = -1, nxt_coff = -1;
     auto fetch = [&](uint64_t tt) {
-      tile_coords(tt, nxt_item, nxt_m0, nxt_n0);
+      tile_coords(tt, nxt_unit, nxt_m0, nxt_n0);
       nxt_om = nxt_m0 + r < p.M ? p.tom(nxt_m0 + r) : 0u;
-      nxt_out = p.out_rows ? uint64_t{p.out_rows[nxt_item]} : uint64_t{nxt_item};
+      const uint64_t k = (uint64_t{nxt_unit} << 16) | static_cast<uint32_t>(nxt_n0);
+      if (k != nxt_key) {
+        nxt_key = k;
+        nxt_coff = col_offset(nxt_unit, nxt_n0 / 2);
+      }
     };
     if (t < tiles) fetch(t);
     for (; t < tiles; t += kEpiGroups * uint64_t{gridDim.x}, it += kEpiGroups) {
-      item = nxt_item;
       m0 = nxt_m0;
-      n0 = nxt_n0;
       om = nxt_om;
-      out_entry = nxt_out;
+      key = nxt_key;
+      my_coff = nxt_coff;
       if (t + kEpiGroups * uint64_t{gridDim.x} < tiles) fetch(t + kEpiGroups * uint64_t{gridDim.x});
+      if (key != table_key) {  // uniform across the group
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));  // readers of the old table done
+        if (r < kMaxBn / 2) coff[r] = my_coff;
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));
+        table_key = key;
+      }
       const uint32_t tb = static_cast<uint32_t>(it % n_acc);
       mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
       if (warp == 6 && lane == 0) trace(p, it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + r;
-      float2* O = p.out + out_entry * p.out_item;
-      (void)item;
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
         const int cols = min(16, (p.bn - c0) / 2);
-        const int nb0 = (n0 + c0) / 2;  // first complex column of this chunk
+        const int cc = c0 / 2;  // first complex column of this chunk in the tile
         if (p.transpose) {
           // Output rows are not adjacent in memory: transpose the warp's
           // 32 rows x `cols` complex chunk through shared memory so that
@@ -421,9 +440,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int e = lane; e < 32 * cols; e += 32) {
             const int row = e >> per_row_shift, cj = e & (cols - 1);
             const uint32_t row_om = __shfl_sync(0xffffffffu, om, row);
-            if (m0 + quarter * 32 + row >= p.M) continue;
+            const int64_t co = coff[cc + cj];
+            if (m0 + quarter * 32 + row >= p.M || co < 0) continue;
             float2 val = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
-            float2* dst = O + row_om + (ton_cached ? ton_s[nb0 + cj] : p.ton(nb0 + cj));
+            float2* dst = p.out + co + row_om;
             if (p.accumulate) {
               const float2 old = *dst;
               val.x += old.x;
@@ -436,19 +456,25 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         if (m >= p.M) continue;
         if (p.n_contig && !p.accumulate) {
-          // the chunk's columns are consecutive in the output: 16-byte stores
-          float4* dst = reinterpret_cast<float4*>(O + om + (ton_cached ? ton_s[nb0] : p.ton(nb0)));
+          // column pairs are consecutive in the output (and in one item):
+          // 16-byte stores
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (2 * j < cols)
-              dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                   __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          for (int j = 0; j < 8; ++j) {
+            if (2 * j >= cols) break;
+            const int64_t co = coff[cc + 2 * j];
+            if (co < 0) continue;
+            *reinterpret_cast<float4*>(p.out + co + om) =
+                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             if (j >= cols) break;
+            const int64_t co = coff[cc + j];
+            if (co < 0) continue;
             float2 val = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-            float2* dst = O + om + (ton_cached ? ton_s[nb0 + j] : p.ton(nb0 + j));
+            float2* dst = p.out + co + om;
             if (p.accumulate) {
               const float2 old = *dst;
               val.x += old.x;
@@ -471,18 +497,32 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
-// B̂ (2N x 2K floats per item, K-major) from the B operand, split hi/lo.
+// B̂ (2N x 2K floats per item, K-major) from the B operand, split hi/lo. In
+// grouped mode unit u holds `slots` item blocks (items grp_items[grp_start[u]
+// + slot], zero blocks past the group's size), so a unit's B̂ is one
+// (slots * 2N) x 2K matrix.
 __global__ void build_bhat_kernel(const float2* b, uint64_t b_item, const uint32_t* ib,
                                   uint64_t b_slice, TcTable tbn, TcTable tbk, int fb, int kc,
-                                  uint32_t nb, float* bhi, float* blo) {
+                                  uint32_t units, uint32_t slots, const uint32_t* grp_items,
+                                  const uint32_t* grp_start, float* bhi, float* blo) {
   const uint64_t N = uint64_t{1} << fb, K = uint64_t{1} << kc;
-  const uint64_t total = uint64_t{nb} * N * K;
+  const uint64_t per_unit = uint64_t{slots ? slots : 1u};
+  const uint64_t total = uint64_t{units} * per_unit * N * K;
   for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
        e += uint64_t{gridDim.x} * blockDim.x) {
-    const uint64_t k = e % K, n = (e / K) % N, item = e / (K * N);
-    const float2 v = b[uint64_t{ib ? ib[item] : (uint32_t)item} * b_item + b_slice + tbn(n) + tbk(k)];
+    const uint64_t k = e % K, n = (e / K) % N, blk = e / (K * N);  // blk = unit * slots + slot
+    float2 v = make_float2(0.f, 0.f);
+    uint32_t item = static_cast<uint32_t>(blk);
+    bool live = true;
+    if (slots) {
+      const uint32_t u = static_cast<uint32_t>(blk / slots), slot = static_cast<uint32_t>(blk % slots);
+      const uint32_t g0 = grp_start[u];
+      live = g0 + slot < grp_start[u + 1];
+      if (live) item = grp_items[g0 + slot];
+    }
+    if (live) v = b[uint64_t{ib ? ib[item] : item} * b_item + b_slice + tbn(n) + tbk(k)];
     const float q[4] = {v.x, -v.y, v.y, v.x};  // row 2n: [br, -bi]; row 2n+1: [bi, br]
-    const uint64_t r0 = (item * 2 * N + 2 * n) * (2 * K) + 2 * k;
+    const uint64_t r0 = (blk * 2 * N + 2 * n) * (2 * K) + 2 * k;
     const uint64_t r1 = r0 + 2 * K;
     const uint64_t idx[4] = {r0, r0 + 1, r1, r1 + 1};
 #pragma unroll
@@ -529,12 +569,15 @@ int tc_tile_n(int Nr) { return Nr >= 256 ? 256 : Nr; }
 
 void tc_contract(const TcOp& op, cudaStream_t st) {
   const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb, K = uint64_t{1} << op.kc;
-  const uint64_t Nr = 2 * N, Kr = 2 * K;
-  // 1) B̂ hi / lo (small: per item 2N x 2K floats); A is split in the kernel
-  const int blocks = static_cast<int>(std::min<uint64_t>(148 * 8, (uint64_t{op.nb} * N * K + 255) / 256));
+  // units: items, or groups of items sharing the A entry (N_eff = slots x N)
+  const uint32_t units = op.slots ? op.n_groups : op.nb;
+  const uint64_t Nr = 2 * N * (op.slots ? op.slots : 1u), Kr = 2 * K;
+  // 1) B̂ hi / lo (small: per unit 2N_eff x 2K floats); A is split in the kernel
+  const int blocks = static_cast<int>(std::min<uint64_t>(148 * 8, (uint64_t{units} * Nr / 2 * K + 255) / 256));
   TcTable tbn{op.tbn_lo, op.tbn_hi, op.tbn_bits}, tbk{op.tbk_lo, op.tbk_hi, op.tbk_bits};
   build_bhat_kernel<<<blocks, 256, 0, st>>>(op.b, op.b_item, op.ib, op.b_slice, tbn, tbk, op.fb,
-                                            op.kc, op.nb, op.bhat_hi, op.bhat_lo);
+                                            op.kc, units, op.slots, op.grp_items, op.grp_start,
+                                            op.bhat_hi, op.bhat_lo);
   // 2) GEMM: persistent, one CTA per SM; smem = ring + ton cache + transpose
   // buffers; keep >= 2 stages (halve the n tile if needed)
   // Short output rows (<= 32 complex per tile row) that are strided in memory
@@ -542,7 +585,8 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   // lane with vector stores.
   const int bn = tc_tile_n(static_cast<int>(Nr));
   const bool transpose = !op.m_contig && bn <= 64;
-  const int extra = 1024 + 768 + 4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) +
+  const int extra = 1024 + 768 + 4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) + 8 +
+                    8 * kEpiGroups * (kMaxBn / 2) +
                     (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
   constexpr int kSmemMax = 227 * 1024;
   auto stage_of = [](int b) { return 2 * kBM * kBK * 4 + 2 * b * kBK * 4; };
@@ -550,22 +594,26 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
   const size_t smem = extra + static_cast<size_t>(n_stages) * stage_bytes;
   const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM);
-  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{op.nb} * Nr, bn);
-  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{op.nb} * Nr, bn);
+  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn);
+  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn);
   TcParams p;
   p.M = static_cast<int>(M);
   p.Nr = static_cast<int>(Nr);
   p.Kr = static_cast<int>(Kr);
   p.bn = bn;
-  p.nb = op.nb;
+  p.nb = units;
   p.ia = op.ia;
+  p.grp_items = op.grp_items;
+  p.grp_start = op.grp_start;
+  p.slots = static_cast<int>(op.slots);
+  p.fb = op.fb;
   p.out = op.out;
   p.out_rows = op.out_rows;
   p.out_item = op.out_item;
   p.tom = TcTable{op.tom_lo, op.tom_hi, op.tom_bits};
   p.ton = TcTable{op.ton_lo, op.ton_hi, op.ton_bits};
   p.accumulate = op.accumulate;
-  p.n_contig = op.n_contig;
+  p.n_contig = op.n_contig && (op.slots == 0 || op.fb >= 1);
   p.m_contig = op.m_contig;
   p.transpose = transpose ? 1 : 0;
   static size_t smem_set = 0;
@@ -580,7 +628,7 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * op.nb;
+  const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * units;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));
   p.dbg = nullptr;
   const char* tr = std::getenv("MTCG_TC_TRACE");

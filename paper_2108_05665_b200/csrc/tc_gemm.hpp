@@ -23,7 +23,7 @@ struct TcOp {
   const uint32_t* ib;
   const uint32_t *tbn_lo, *tbn_hi, *tbk_lo, *tbk_hi;
   int tbn_bits, tbk_bits;
-  float* bhat_hi;                 // scratch: nb * 2N * 2K floats
+  float* bhat_hi;                 // scratch: units * 2N_eff * 2K floats
   float* bhat_lo;
   float2* out;
   const uint32_t* out_rows;
@@ -33,6 +33,12 @@ struct TcOp {
   int accumulate;
   int n_contig;                   // output n index contiguous (vector epilogue stores)
   int m_contig;                   // output m index contiguous (row-per-lane stores coalesce)
+  // Grouped mode (slots > 0): items sharing an A entry are one GEMM whose N
+  // is the concatenation of `slots` item B blocks (padded with zero blocks).
+  const uint32_t* grp_items;      // items ordered by A entry
+  const uint32_t* grp_start;      // n_groups + 1 offsets
+  uint32_t n_groups;
+  uint32_t slots;
 };
 
 void tc_contract(const TcOp& op, cudaStream_t st);
