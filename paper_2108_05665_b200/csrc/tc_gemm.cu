@@ -39,8 +39,10 @@ namespace mtcg {
 namespace {
 
 constexpr int kBM = 128;
-constexpr int kBK = 32;        // floats per stage row (128 B: one swizzle row)
-static_assert(kBK == 32, "mma_stage issues exactly 4 k-steps of 8 per stage");
+// Stage width BK (floats of K per stage row): 32 (128-byte rows, SWIZZLE_128B,
+// 4 MMA k-steps) or 16 (64-byte rows, SWIZZLE_64B, 2 k-steps). The narrow
+// stage halves the ring's granularity so wide tiles (whose 32-float stages
+// only fit twice in shared memory) keep 4 stages in flight.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -82,11 +84,15 @@ __device__ __forceinline__ void tma_load_2d(void* smem, const CUtensorMap* map, 
       : "memory");
 }
 
-// K-major, SWIZZLE_128B smem matrix descriptor (8-row atoms of 128 B rows;
-// stride between atoms 1024 B; sm100 descriptor version 1).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t{(saddr >> 4) & 0x3FFFu}) | (uint64_t{1} << 16) | (uint64_t{64} << 32) |
-         (uint64_t{1} << 46) | (uint64_t{2} << 61);
+// K-major swizzled smem matrix descriptor (sm100 descriptor version 1):
+// BK = 32: SWIZZLE_128B (layout 2), 8-row atoms of 128 B rows, 1024 B apart;
+// BK = 16: SWIZZLE_64B (layout 4), 8-row atoms of 64 B rows, 512 B apart.
+template <int BK>
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+  constexpr uint64_t sbo = BK * 4 * 8 / 16;  // atom stride, 16-byte units
+  constexpr uint64_t layout = BK == 32 ? 2 : 4;
+  return (uint64_t{(saddr >> 4) & 0x3FFFu}) | (uint64_t{1} << 16) | (sbo << 32) |
+         (uint64_t{1} << 46) | (layout << 61);
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -130,6 +136,25 @@ __device__ __forceinline__ void mma_stage(uint32_t d, uint64_t ahi, uint64_t alo
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al3, bh3, %5, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah3, bl3, %5, 1;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah3, bh3, %5, 1;\n\t}" ::"r"(d),
+      "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc));
+}
+
+// Two k-steps (a 16-float stage).
+__device__ __forceinline__ void mma_stage2(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi,
+                                           uint64_t blo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b64 ah1, al1, bh1, bl1;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "add.s64 ah1, %1, 2;\n\tadd.s64 al1, %2, 2;\n\t"
+      "add.s64 bh1, %3, 2;\n\tadd.s64 bl1, %4, 2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, bh1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, bl1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, bh1, %5, 1;\n\t}" ::"r"(d),
       "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc));
 }
 
@@ -207,11 +232,12 @@ __device__ __forceinline__ float tf32_rna_alu(float x) {
 // The ring depth S is chosen so the stages fill ~220 KB of shared memory.
 constexpr int kEpiGroups = 2;       // epilogue warpgroups (alternate tiles)
 constexpr int kPThreads = 192 + 128 * kEpiGroups;
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 12;
 constexpr int kMaxAcc = 8;          // TMEM accumulator buffers
 constexpr int kMaxTonCache = 2048;  // output column offsets cached in smem
 constexpr int kMaxBn = 256;         // real columns per tile
 
+template <int BK>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_persistent(const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ CUtensorMap map_bhi,
@@ -223,8 +249,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // compiler, so smem accesses below compile to LDS/STS rather than generic
   // LD/ST through L1.
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int a_bytes = kBM * kBK * 4;
-  const int b_bytes = p.bn * kBK * 4;
+  const int a_bytes = kBM * BK * 4;
+  const int b_bytes = p.bn * BK * 4;
   const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(base + n_stages * stage_bytes);
   uint64_t* conv = full + kMaxStages;
@@ -245,7 +271,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
   const uint32_t tiles_m = (p.M + kBM - 1) / kBM;
   const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
-  const int k_stages = p.Kr / kBK;
+  const int k_stages = p.Kr / BK;
   uint32_t buf_cols = 32;
   while (buf_cols < static_cast<uint32_t>(p.bn)) buf_cols <<= 1;
   // accumulator ring: as many buffers as fit in TMEM's 512 columns (2..8), so
@@ -309,9 +335,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
             mbar_wait(&empty[st], static_cast<uint32_t>((g / n_stages) - 1) & 1);
           uint8_t* sp = base + st * stage_bytes;
           mbar_expect_tx(&full[st], a_bytes + 2 * b_bytes);
-          tma_load_2d(sp, &map_a, &full[st], s * kBK, a_row0);
-          tma_load_2d(sp + 2 * a_bytes, &map_bhi, &full[st], s * kBK, b_row0);
-          tma_load_2d(sp + 2 * a_bytes + b_bytes, &map_blo, &full[st], s * kBK, b_row0);
+          tma_load_2d(sp, &map_a, &full[st], s * BK, a_row0);
+          tma_load_2d(sp + 2 * a_bytes, &map_bhi, &full[st], s * BK, b_row0);
+          tma_load_2d(sp + 2 * a_bytes + b_bytes, &map_blo, &full[st], s * BK, b_row0);
         }
         trace(p, pit, 1);
       }
@@ -334,8 +360,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_wait(&conv[st], static_cast<uint32_t>(g / n_stages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sp = smem_u32(base + st * stage_bytes);
-        mma_stage(dacc, sw128_desc(sp), sw128_desc(sp + a_bytes), sw128_desc(sp + 2 * a_bytes),
-                  sw128_desc(sp + 2 * a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
+        if constexpr (BK == 32)
+          mma_stage(dacc, sw_desc<BK>(sp), sw_desc<BK>(sp + a_bytes), sw_desc<BK>(sp + 2 * a_bytes),
+                    sw_desc<BK>(sp + 2 * a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
+        else
+          mma_stage2(dacc, sw_desc<BK>(sp), sw_desc<BK>(sp + a_bytes), sw_desc<BK>(sp + 2 * a_bytes),
+                     sw_desc<BK>(sp + 2 * a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
         mma_commit_elect(&empty[st]);
       }
       mma_commit_elect(&acc_full[tb]);
@@ -352,7 +382,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         float4* hi = reinterpret_cast<float4*>(base + st * stage_bytes);
         float4* lo = reinterpret_cast<float4*>(base + st * stage_bytes + a_bytes);
 #pragma unroll
-        for (int i = 0; i < (kBM * kBK * 4) / 16 / 128; ++i) {
+        for (int i = 0; i < (kBM * BK * 4) / 16 / 128; ++i) {
           const int e = ct + i * 128;
           const float4 v = hi[e];
           const float4 h = make_float4(tf32_rna_alu(v.x), tf32_rna_alu(v.y), tf32_rna_alu(v.z),
@@ -549,15 +579,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-CUtensorMap make_map(const float* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+CUtensorMap make_map(const float* base, uint64_t cols, uint64_t rows, uint32_t box_rows, int bk) {
   CUtensorMap m;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * sizeof(float)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(bk), box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return m;
@@ -565,7 +596,10 @@ CUtensorMap make_map(const float* base, uint64_t cols, uint64_t rows, uint32_t b
 
 }  // namespace
 
-int tc_tile_n(int Nr) { return Nr >= 256 ? 256 : Nr; }
+int tc_tile_n(int Nr) {
+  static const int cap = std::getenv("MTCG_TC_BN") ? std::atoi(std::getenv("MTCG_TC_BN")) : 256;
+  return Nr >= cap ? cap : Nr;
+}
 
 void tc_contract(const TcOp& op, cudaStream_t st) {
   const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb, K = uint64_t{1} << op.kc;
@@ -589,13 +623,17 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
                     8 * kEpiGroups * (kMaxBn / 2) +
                     (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
   constexpr int kSmemMax = 227 * 1024;
-  auto stage_of = [](int b) { return 2 * kBM * kBK * 4 + 2 * b * kBK * 4; };
-  const int stage_bytes = stage_of(bn);
+  auto stage_of = [&](int bk) { return 2 * kBM * bk * 4 + 2 * bn * bk * 4; };
+  // 32-float stages unless only 2 of them fit (MTCG_TC_BK overrides)
+  static const int bk_env = std::getenv("MTCG_TC_BK") ? std::atoi(std::getenv("MTCG_TC_BK")) : 0;
+  const int bk = bk_env == 16 || bk_env == 32 ? bk_env
+                 : (kSmemMax - extra) / stage_of(32) >= 3 ? 32 : 16;
+  const int stage_bytes = stage_of(bk);
   const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
   const size_t smem = extra + static_cast<size_t>(n_stages) * stage_bytes;
-  const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM);
-  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn);
-  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn);
+  const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM, bk);
+  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn, bk);
+  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn, bk);
   TcParams p;
   p.M = static_cast<int>(M);
   p.Nr = static_cast<int>(Nr);
@@ -616,12 +654,12 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   p.n_contig = op.n_contig && (op.slots == 0 || op.fb >= 1);
   p.m_contig = op.m_contig;
   p.transpose = transpose ? 1 : 0;
-  static size_t smem_set = 0;
+  static size_t smem_set[2] = {0, 0};
   static int n_sms = 0;
-  if (smem > smem_set) {
-    cudaFuncSetAttribute(tc_gemm_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    smem_set = smem;
+  auto kern = bk == 32 ? tc_gemm_persistent<32> : tc_gemm_persistent<16>;
+  if (smem > smem_set[bk == 32]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    smem_set[bk == 32] = smem;
   }
   if (!n_sms) {
     int dev = 0;
@@ -637,15 +675,15 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
     cudaMalloc(&p.dbg, sizeof(unsigned long long) * kTraceTiles * 8);
     cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * kTraceTiles * 8, st);
   }
-  tc_gemm_persistent<<<grid, kPThreads, smem, st>>>(ma, mbhi, mblo, p, n_stages);
+  kern<<<grid, kPThreads, smem, st>>>(ma, mbhi, mblo, p, n_stages);
   if (tracing) {
     std::vector<unsigned long long> h(kTraceTiles * 8);
     cudaMemcpyAsync(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     cudaFree(p.dbg);
     const unsigned long long t0 = h[0];
-    std::fprintf(stderr, "[tc trace node %d] stages=%d bn=%d tiles=%llu grid=%u n_acc<=%d\n",
-                 op.node, n_stages, bn, static_cast<unsigned long long>(tiles), grid, kMaxAcc);
+    std::fprintf(stderr, "[tc trace node %d] bk=%d stages=%d bn=%d tiles=%llu grid=%u n_acc<=%d\n",
+                 op.node, bk, n_stages, bn, static_cast<unsigned long long>(tiles), grid, kMaxAcc);
     std::fprintf(stderr, " tile  prod0  prod1  conv(full) mma0  mma1  epi0  epi1   (cycles from tile0 prod0)\n");
     for (int i = 0; i < kTraceTiles; ++i) {
       if (!h[i * 8]) break;
