@@ -808,9 +808,11 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       std::sort(b.begin(), b.end());
       const auto da = std::unique(a.begin(), a.end()) - a.begin();
       const auto db = std::unique(b.begin(), b.end()) - b.begin();
-      std::fprintf(stderr, "[mtcg] op node %d M2^%d N2^%d K2^%d batch %u distinct_a %ld distinct_b %ld cfg %d%s\n",
-                   op.node, op.fa, op.fb, op.kc, op.nb, (long)da, (long)db, op.config,
-                   op.root ? " root" : "");
+      std::fprintf(stderr,
+                   "[mtcg] op node %d M2^%d N2^%d K2^%d batch %u distinct_a %ld distinct_b %ld cfg %d"
+                   " slots %u kcontig %d ncontig %d mcontig %d%s\n",
+                   op.node, op.fa, op.fb, op.kc, op.nb, (long)da, (long)db, op.config, op.grp_max,
+                   op.a_kcontig, op.o_ncontig, op.o_mcontig, op.root ? " root" : "");
     }
   }
   return c;

@@ -158,6 +158,49 @@ __device__ __forceinline__ void mma_stage2(uint32_t d, uint64_t ahi, uint64_t al
       "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc));
 }
 
+// "Wide" 3xTF32 stage for tiles with bn <= 128: B̂hi and B̂lo stage buffers
+// are adjacent, i.e. one K-major [B̂hi; B̂lo] matrix of 2 bn rows, so
+//   D[0:2bn]  (+)= Âhi [B̂hi; B̂lo]^T   (one MMA, N = 2 bn)
+//   D[0:bn]    += Âlo B̂hi^T          (N = bn)
+// and the epilogue adds the two halves: 2 MMAs and 2 A-operand reads per
+// k-step instead of 3 (shared-memory bandwidth bounds these small tiles).
+template <int KSTEPS>
+__device__ __forceinline__ void mma_stage_wide(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi,
+                                               uint32_t idesc2, uint32_t idesc1, uint32_t acc) {
+  static_assert(KSTEPS == 2 || KSTEPS == 4, "stage width");
+  if constexpr (KSTEPS == 4) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        ".reg .b64 ah1, ah2, ah3, al1, al2, al3, bh1, bh2, bh3;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 ah1, %1, 2;\n\tadd.s64 ah2, %1, 4;\n\tadd.s64 ah3, %1, 6;\n\t"
+        "add.s64 al1, %2, 2;\n\tadd.s64 al2, %2, 4;\n\tadd.s64 al3, %2, 6;\n\t"
+        "add.s64 bh1, %3, 2;\n\tadd.s64 bh2, %3, 4;\n\tadd.s64 bh3, %3, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, bh1, %4, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, bh1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah2, bh2, %4, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al2, bh2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah3, bh3, %4, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al3, bh3, %5, 1;\n\t}" ::"r"(d),
+        "l"(ahi), "l"(alo), "l"(bhi), "r"(idesc2), "r"(idesc1), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        ".reg .b64 ah1, al1, bh1;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 ah1, %1, 2;\n\tadd.s64 al1, %2, 2;\n\tadd.s64 bh1, %3, 2;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %3, %4, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah1, bh1, %4, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al1, bh1, %5, 1;\n\t}" ::"r"(d),
+        "l"(ahi), "l"(alo), "l"(bhi), "r"(idesc2), "r"(idesc1), "r"(acc));
+  }
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -263,8 +306,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint32_t* ton_s = tmem_slot + 4;
   const int n_item_cols = p.slots ? (1 << p.fb) : p.Nr / 2;  // columns of one item
   // per epilogue group: output offset of each complex column of its tile
-  // (ton_s is 8-byte aligned; an even count keeps coff_s 8-byte aligned)
-  int64_t* coff_s = reinterpret_cast<int64_t*>(ton_s + ((min(n_item_cols, kMaxTonCache) + 1) & ~1));
+  // (ton_s is 16-byte aligned; a count rounded to 4 keeps coff_s 16-byte
+  // aligned for the epilogue's LDS.128)
+  int64_t* coff_s = reinterpret_cast<int64_t*>(ton_s + ((min(n_item_cols, kMaxTonCache) + 3) & ~3));
   float* stage_out = reinterpret_cast<float*>(coff_s + kEpiGroups * (kMaxBn / 2));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -272,8 +316,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint32_t tiles_m = (p.M + kBM - 1) / kBM;
   const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
   const int k_stages = p.Kr / BK;
+  // wide mode (bn <= 128): each accumulator holds [hi-B half | lo-B half]
+  const bool wide = p.bn <= 128;
+  const uint32_t acc_cols = wide ? 2 * p.bn : p.bn;
   uint32_t buf_cols = 32;
-  while (buf_cols < static_cast<uint32_t>(p.bn)) buf_cols <<= 1;
+  while (buf_cols < acc_cols) buf_cols <<= 1;
   // accumulator ring: as many buffers as fit in TMEM's 512 columns (2..8), so
   // short-K tiles keep the MMA busy while earlier tiles drain
   const uint32_t n_acc = min(static_cast<uint32_t>(kMaxAcc), 512u / buf_cols);
@@ -348,6 +395,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // memory operand-read floor of a 128 x N x 8 tf32 MMA; tools/mma_bench.cu)
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
                            (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
+    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) |
+                            (static_cast<uint32_t>((2 * p.bn) >> 3) << 17) | ((kBM >> 4) << 24);
     uint64_t g = 0, it = 0;
     for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const uint32_t tb = static_cast<uint32_t>(it % n_acc);
@@ -360,7 +409,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_wait(&conv[st], static_cast<uint32_t>(g / n_stages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sp = smem_u32(base + st * stage_bytes);
-        if constexpr (BK == 32)
+        if (wide)
+          mma_stage_wide<BK / 8>(dacc, sw_desc<BK>(sp), sw_desc<BK>(sp + a_bytes),
+                                 sw_desc<BK>(sp + 2 * a_bytes), idesc2, idesc, s > 0 ? 1u : 0u);
+        else if constexpr (BK == 32)
           mma_stage(dacc, sw_desc<BK>(sp), sw_desc<BK>(sp + a_bytes), sw_desc<BK>(sp + 2 * a_bytes),
                     sw_desc<BK>(sp + 2 * a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
         else
@@ -455,22 +507,29 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int m = m0 + r;
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
-        const int cols = min(16, (p.bn - c0) / 2);
+        const uint32_t taddr = tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c0;
+        tmem_ld32(taddr, v);
+        if (wide) {  // + the Âhi B̂lo half
+          uint32_t w[32];
+          tmem_ld32(taddr + p.bn, w);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+        }
+        // bn is a multiple of 32 real columns: every chunk is 16 complex columns
         const int cc = c0 / 2;  // first complex column of this chunk in the tile
         if (p.transpose) {
           // Output rows are not adjacent in memory: transpose the warp's
-          // 32 rows x `cols` complex chunk through shared memory so that
+          // 32 rows x 16 complex chunk through shared memory so that
           // consecutive lanes write consecutive columns of a row.
           float* buf = stage_out + (warp - 6) * 32 * 33;
 #pragma unroll
           for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
           __syncwarp();
-          const int per_row_shift = 31 - __clz(cols);  // cols is a power of two
-          for (int e = lane; e < 32 * cols; e += 32) {
-            const int row = e >> per_row_shift, cj = e & (cols - 1);
+          const int64_t co = coff[cc + (lane & 15)];
+#pragma unroll 4
+          for (int e = lane; e < 32 * 16; e += 32) {
+            const int row = e >> 4, cj = e & 15;
             const uint32_t row_om = __shfl_sync(0xffffffffu, om, row);
-            const int64_t co = coff[cc + cj];
             if (m0 + quarter * 32 + row >= p.M || co < 0) continue;
             float2 val = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
             float2* dst = p.out + co + row_om;
@@ -485,33 +544,39 @@ __global__ void __launch_bounds__(kPThreads, 1)
           continue;
         }
         if (m >= p.M) continue;
+        // the chunk's 16 column offsets (uniform across lanes): 8 LDS.128
+        // up front, then back-to-back predicated stores
+        int64_t co[16];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const longlong2 t = reinterpret_cast<const longlong2*>(coff + cc)[j];
+          co[2 * j] = t.x;
+          co[2 * j + 1] = t.y;
+        }
         if (p.n_contig && !p.accumulate) {
           // column pairs are consecutive in the output (and in one item):
           // 16-byte stores
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (2 * j >= cols) break;
-            const int64_t co = coff[cc + 2 * j];
-            if (co < 0) continue;
-            *reinterpret_cast<float4*>(p.out + co + om) =
-                make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-          }
-        } else {
+          for (int j = 0; j < 8; ++j)
+            if (co[2 * j] >= 0)
+              *reinterpret_cast<float4*>(p.out + co[2 * j] + om) =
+                  make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+        } else if (!p.accumulate) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j >= cols) break;
-            const int64_t co = coff[cc + j];
-            if (co < 0) continue;
-            float2 val = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-            float2* dst = p.out + co + om;
-            if (p.accumulate) {
-              const float2 old = *dst;
-              val.x += old.x;
-              val.y += old.y;
-            }
-            *dst = val;
-          }
+          for (int j = 0; j < 16; ++j)
+            if (co[j] >= 0)
+              p.out[co[j] + om] = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        } else {
+          float2 old[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (co[j] >= 0) old[j] = p.out[co[j] + om];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (co[j] >= 0)
+              p.out[co[j] + om] = make_float2(old[j].x + __uint_as_float(v[2 * j]),
+                                              old[j].y + __uint_as_float(v[2 * j + 1]));
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -619,7 +684,7 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   // lane with vector stores.
   const int bn = tc_tile_n(static_cast<int>(Nr));
   const bool transpose = !op.m_contig && bn <= 64;
-  const int extra = 1024 + 768 + 4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) + 8 +
+  const int extra = 1024 + 768 + 4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) + 16 +
                     8 * kEpiGroups * (kMaxBn / 2) +
                     (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
   constexpr int kSmemMax = 227 * 1024;
