@@ -14,7 +14,8 @@ import threading
 from . import _abi as A
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libmtcg.so")
+# MTCG_LIB_PATH loads another build of the library instead (A/B tuning runs)
+LIB_PATH = os.environ.get("MTCG_LIB_PATH") or os.path.join(PKG_DIR, "libmtcg.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 _lib = None

@@ -210,6 +210,17 @@ __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 struct TcTable {
   const uint32_t* lo;
   const uint32_t* hi;
@@ -353,10 +364,31 @@ __global__ void __launch_bounds__(kPThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  auto tile_coords = [&](uint64_t t, uint32_t& item, int& m0, int& n0) {
-    n0 = static_cast<int>(t % tiles_n) * p.bn;
-    m0 = static_cast<int>((t / tiles_n) % tiles_m) * kBM;
-    item = static_cast<uint32_t>(t / (uint64_t{tiles_n} * tiles_m));
+  // Tile t = (unit, m-tile, n-tile) with n fastest. Each role walks tiles
+  // t0, t0 + step, ... : the step is decomposed once in the same mixed radix
+  // and added with carries (no 64-bit divisions per tile, which cost several
+  // hundred cycles on the producer's critical path).
+  struct TileWalk {
+    uint32_t n, m, u, dn, dm, du, tn, tm;
+    __device__ void init(uint64_t t0, uint64_t step, uint32_t tn_, uint32_t tm_) {
+      tn = tn_;
+      tm = tm_;
+      n = static_cast<uint32_t>(t0 % tn);
+      m = static_cast<uint32_t>((t0 / tn) % tm);
+      u = static_cast<uint32_t>(t0 / (uint64_t{tn} * tm));
+      dn = static_cast<uint32_t>(step % tn);
+      dm = static_cast<uint32_t>((step / tn) % tm);
+      du = static_cast<uint32_t>(step / (uint64_t{tn} * tm));
+    }
+    __device__ void advance() {
+      n += dn;
+      uint32_t c = n >= tn;
+      n -= c ? tn : 0u;
+      m += dm + c;
+      c = m >= tm;
+      m -= c ? tm : 0u;
+      u += du + c;
+    }
   };
 
   if (warp == 0) {
@@ -364,10 +396,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
       uint64_t g = 0;
       uint32_t cached_item = ~0u, a_entry = 0;
       uint64_t pit = 0;
-      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++pit) {
-        uint32_t item;
-        int m0, n0;
-        tile_coords(t, item, m0, n0);
+      TileWalk w;
+      w.init(blockIdx.x, gridDim.x, tiles_n, tiles_m);
+      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++pit, w.advance()) {
+        const uint32_t item = w.u;
+        const int m0 = static_cast<int>(w.m) * kBM, n0 = static_cast<int>(w.n) * p.bn;
         trace(p, pit, 0);
         if (item != cached_item) {  // units change every tiles_m * tiles_n tiles
           cached_item = item;
@@ -478,8 +511,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint32_t om = 0, nxt_om = 0;
     uint64_t key = ~uint64_t{0}, nxt_key = ~uint64_t{0}, table_key = ~uint64_t{0};
     int64_t my_coff = -1, nxt_coff = -1;
-    auto fetch = [&](uint64_t tt) {
-      tile_coords(tt, nxt_unit, nxt_m0, nxt_n0);
+    TileWalk w;  // walks the group's tiles one fetch ahead
+    w.init(t, kEpiGroups * uint64_t{gridDim.x}, tiles_n, tiles_m);
+    auto fetch = [&]() {
+      nxt_unit = w.u;
+      nxt_m0 = static_cast<int>(w.m) * kBM;
+      nxt_n0 = static_cast<int>(w.n) * p.bn;
+      w.advance();
       nxt_om = nxt_m0 + r < p.M ? p.tom(nxt_m0 + r) : 0u;
       const uint64_t k = (uint64_t{nxt_unit} << 16) | static_cast<uint32_t>(nxt_n0);
       if (k != nxt_key) {
@@ -487,13 +525,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
         nxt_coff = col_offset(nxt_unit, nxt_n0 / 2);
       }
     };
-    if (t < tiles) fetch(t);
+    if (t < tiles) fetch();
     for (; t < tiles; t += kEpiGroups * uint64_t{gridDim.x}, it += kEpiGroups) {
       m0 = nxt_m0;
       om = nxt_om;
       key = nxt_key;
       my_coff = nxt_coff;
-      if (t + kEpiGroups * uint64_t{gridDim.x} < tiles) fetch(t + kEpiGroups * uint64_t{gridDim.x});
+      if (t + kEpiGroups * uint64_t{gridDim.x} < tiles) fetch();
       if (key != table_key) {  // uniform across the group
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));  // readers of the old table done
         if (r < kMaxBn / 2) coff[r] = my_coff;
@@ -505,19 +543,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (warp == 6 && lane == 0) trace(p, it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + r;
+      const uint32_t tacc = tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16);
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
-        uint32_t v[32];
-        const uint32_t taddr = tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16) + c0;
-        tmem_ld32(taddr, v);
-        if (wide) {  // + the Âhi B̂lo half
-          uint32_t w[32];
-          tmem_ld32(taddr + p.bn, w);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
-        }
         // bn is a multiple of 32 real columns: every chunk is 16 complex columns
         const int cc = c0 / 2;  // first complex column of this chunk in the tile
         if (p.transpose) {
+          uint32_t v[32];
+          tmem_ld32(tacc + c0, v);
+          if (wide) {  // + the Âhi B̂lo half
+            uint32_t w[32];
+            tmem_ld32(tacc + c0 + p.bn, w);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+          }
           // Output rows are not adjacent in memory: transpose the warp's
           // 32 rows x 16 complex chunk through shared memory so that
           // consecutive lanes write consecutive columns of a row.
@@ -543,40 +581,49 @@ __global__ void __launch_bounds__(kPThreads, 1)
           __syncwarp();
           continue;
         }
-        if (m >= p.M) continue;
-        // the chunk's 16 column offsets (uniform across lanes): 8 LDS.128
-        // up front, then back-to-back predicated stores
-        int64_t co[16];
+        // row per lane, 8 complex columns at a time (bounded register use)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const longlong2 t = reinterpret_cast<const longlong2*>(coff + cc)[j];
-          co[2 * j] = t.x;
-          co[2 * j + 1] = t.y;
-        }
-        if (p.n_contig && !p.accumulate) {
-          // column pairs are consecutive in the output (and in one item):
-          // 16-byte stores
+        for (int h = 0; h < 2; ++h) {
+          uint32_t v[16];
+          tmem_ld16(tacc + c0 + 16 * h, v);
+          if (wide) {
+            uint32_t w[16];
+            tmem_ld16(tacc + c0 + 16 * h + p.bn, w);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (co[2 * j] >= 0)
-              *reinterpret_cast<float4*>(p.out + co[2 * j] + om) =
-                  make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-        } else if (!p.accumulate) {
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+          }
+          if (m >= p.M) continue;
+          // the 8 column offsets (uniform across lanes): 4 LDS.128 up front,
+          // then back-to-back predicated stores
+          int64_t co[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (co[j] >= 0)
-              p.out[co[j] + om] = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
-        } else {
-          float2 old[16];
+          for (int j = 0; j < 4; ++j) {
+            const longlong2 t2 = reinterpret_cast<const longlong2*>(coff + cc + 8 * h)[j];
+            co[2 * j] = t2.x;
+            co[2 * j + 1] = t2.y;
+          }
+          if (p.n_contig && !p.accumulate) {
+            // column pairs are consecutive in the output (and in one item)
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (co[j] >= 0) old[j] = p.out[co[j] + om];
+            for (int j = 0; j < 4; ++j)
+              if (co[2 * j] >= 0)
+                *reinterpret_cast<float4*>(p.out + co[2 * j] + om) =
+                    make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          } else if (!p.accumulate) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (co[j] >= 0)
-              p.out[co[j] + om] = make_float2(old[j].x + __uint_as_float(v[2 * j]),
-                                              old[j].y + __uint_as_float(v[2 * j + 1]));
+            for (int j = 0; j < 8; ++j)
+              if (co[j] >= 0)
+                p.out[co[j] + om] = make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (co[j] >= 0) {
+                const float2 old = p.out[co[j] + om];
+                p.out[co[j] + om] = make_float2(old.x + __uint_as_float(v[2 * j]),
+                                                old.y + __uint_as_float(v[2 * j + 1]));
+              }
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
