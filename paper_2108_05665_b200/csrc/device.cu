@@ -152,7 +152,16 @@ struct DevOp {
   const uint32_t* ib;
   const uint32_t* out_rows; // root: item -> accumulator row, else null
   uint64_t a_item, b_item, out_item;
-  uint64_t a_slice, b_slice;  // slice projection offsets (elements)
+  uint64_t a_slice, b_slice;  // slice projection offsets (elements): resolved on device
+  // Slice parameters live in device memory so one captured slice graph
+  // serves every slice: cur = {slice index, root accumulates}, and a leaf
+  // operand's projection offset is the sum of its per-bit strides over the
+  // set bits of the slice index (multieval.cpp:322-329).
+  const uint64_t* a_sstr;   // per-bit strides (null: operand not sliced)
+  const uint64_t* b_sstr;
+  const uint32_t* cur;
+  int s_bits;
+  int root;
   DTable tam, tak, tbn, tbk, tom, ton;
   uint32_t nb;
   int fa, fb, kc;
@@ -165,11 +174,34 @@ struct DevOp {
   uint32_t n_groups, grp_max;
 };
 
+__device__ __forceinline__ uint64_t slice_offset_dev(const uint64_t* str, int bits, uint32_t s) {
+  uint64_t o = 0;
+  for (int b = 0; b < bits; ++b)
+    if (s >> b & 1) o += __ldg(str + b);
+  return o;
+}
+
+// Fill the slice-dependent fields of a kernel's private copy of its DevOp.
+template <class T>
+__device__ __forceinline__ void resolve_slice(DevOp<T>& op) {
+  const uint32_t s = __ldg(op.cur);
+  op.a_slice = op.a_sstr ? slice_offset_dev(op.a_sstr, op.s_bits, s) : 0;
+  op.b_slice = op.b_sstr ? slice_offset_dev(op.b_sstr, op.s_bits, s) : 0;
+  op.accumulate = op.root ? static_cast<int>(__ldg(op.cur + 1)) : 0;
+}
+
+__global__ void set_slice_kernel(uint32_t* cur, uint32_t s, uint32_t accumulate) {
+  cur[0] = s;
+  cur[1] = accumulate;
+}
+
 // ---- tiled batched contraction -------------------------------------------------
 
 template <class R, int TM, int TN, int RM, int RN, int TK>
 __global__ void __launch_bounds__((TM / RM) * (TN / RN))
-    contract_tile(const DevOp<typename V2<R>::T> op) {
+    contract_tile(const DevOp<typename V2<R>::T> op_in) {
+  DevOp<typename V2<R>::T> op = op_in;
+  resolve_slice(op);
   using T = typename V2<R>::T;
   constexpr int NT = (TM / RM) * (TN / RN);
   constexpr int TXN = TN / RN;  // threads along n
@@ -292,7 +324,9 @@ struct Vec4<double2> {
 
 template <class R, int K, int N, int RPT>
 __global__ void __launch_bounds__(256, 2)
-    contract_rows(const DevOp<typename V2<R>::T> op) {
+    contract_rows(const DevOp<typename V2<R>::T> op_in) {
+  DevOp<typename V2<R>::T> op = op_in;
+  resolve_slice(op);
   // RPT rows per thread computed together: each B row (N complex, one
   // broadcast smem read per element) feeds RPT x N multiply-adds; K streams
   // in chunks of KC so A never occupies more than RPT x KC registers.
@@ -396,7 +430,9 @@ __global__ void __launch_bounds__(256, 2)
 
 template <class R, int K, int N, int RPT>
 __global__ void __launch_bounds__(256, 2)
-    contract_rows_grouped(const DevOp<typename V2<R>::T> op) {
+    contract_rows_grouped(const DevOp<typename V2<R>::T> op_in) {
+  DevOp<typename V2<R>::T> op = op_in;
+  resolve_slice(op);
   using T = typename V2<R>::T;
   using V4 = typename Vec4<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -499,7 +535,9 @@ __global__ void __launch_bounds__(256, 2)
 
 template <class R>
 __global__ void __launch_bounds__(256)
-    contract_generic(const DevOp<typename V2<R>::T> op) {
+    contract_generic(const DevOp<typename V2<R>::T> op_in) {
+  DevOp<typename V2<R>::T> op = op_in;
+  resolve_slice(op);
   using T = typename V2<R>::T;
   const int r_out = op.fa + op.fb;
   const uint64_t total = uint64_t{op.nb} << r_out;
@@ -523,8 +561,11 @@ __global__ void __launch_bounds__(256)
 
 template <class T>
 __global__ void leaf_root(const T* leaves, uint64_t item, const uint32_t* row_value,
-                          uint64_t rows, int r_out, DTable tout, uint64_t slice_off,
-                          T* acc, int accumulate) {
+                          uint64_t rows, int r_out, DTable tout, const uint64_t* sstr, int s_bits,
+                          const uint32_t* cur, T* acc) {
+  const uint32_t s = __ldg(cur);
+  const uint64_t slice_off = sstr ? slice_offset_dev(sstr, s_bits, s) : 0;
+  const int accumulate = static_cast<int>(__ldg(cur + 1));
   const uint64_t total = rows << r_out;
   const uint64_t omask = (uint64_t{1} << r_out) - 1;
   for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
@@ -761,120 +802,132 @@ DTable dtable(const uint32_t* blob, const SplitTable& t) {
   return d;
 }
 
-uint64_t slice_offset(const std::vector<uint64_t>& strides, uint64_t s) {
-  uint64_t off = 0;
-  for (size_t b = 0; b < strides.size(); ++b)
-    if (s >> b & 1) off += strides[b];
-  return off;
-}
 
+// Launches one slice's ops; the slice index and the root's accumulate flag
+// are read by the kernels from dp.d_cur (set by set_slice_kernel), so this
+// launch sequence is the same for every slice and is captured once.
 template <class R>
-void run_slices_t(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
-                  cudaStream_t st, cudaEvent_t* op_events = nullptr) {
+void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st, cudaEvent_t* op_events = nullptr) {
   using T = typename V2<R>::T;
   Compiled& c = dp.c;
   T* arena = static_cast<T*>(dp.d_arena);
   const T* leaves = static_cast<const T*>(dp.d_leaves);
   T* acc = static_cast<T*>(d_acc);
-  for (uint64_t s = s0; s < s1; ++s) {
-    const int acc_flag = (accumulate || s > s0) ? 1 : 0;
-    for (size_t oi = 0; oi < c.ops.size(); ++oi) {
-      const Op& op = c.ops[oi];
-      if (op.nb == 0) continue;
-      if (op_events) CK(cudaEventRecord(op_events[2 * oi], st));
-      DevOp<T> d;
-      d.a = op.a_leaf ? leaves + op.a_base : arena + op.a_base;
-      d.b = op.b_leaf ? leaves + op.b_base : arena + op.b_base;
-      d.out = op.root ? acc : arena + op.out_base;
-      d.ia = dp.d_index + op.ia_off;
-      d.ib = dp.d_index + op.ib_off;
-      d.out_rows = op.root ? dp.d_index + op.out_rows_off : nullptr;
-      d.a_item = op.a_item;
-      d.b_item = op.b_item;
-      d.out_item = op.out_item;
-      d.a_slice = op.a_leaf ? slice_offset(op.a_slice_stride, s) : 0;
-      d.b_slice = op.b_leaf ? slice_offset(op.b_slice_stride, s) : 0;
-      d.tam = dtable(dp.d_tables, op.tam);
-      d.tak = dtable(dp.d_tables, op.tak);
-      d.tbn = dtable(dp.d_tables, op.tbn);
-      d.tbk = dtable(dp.d_tables, op.tbk);
-      d.tom = dtable(dp.d_tables, op.tom);
-      d.ton = dtable(dp.d_tables, op.ton);
-      d.nb = op.nb;
-      d.fa = op.fa;
-      d.fb = op.fb;
-      d.kc = op.kc;
-      d.n_fast = op.store_n_fast ? 1 : 0;
-      d.a_kcontig = op.a_kcontig ? 1 : 0;
-      d.o_ncontig = op.o_ncontig ? 1 : 0;
-      d.grp_items = dp.d_index + op.grp_items_off;
-      d.grp_start = dp.d_index + op.grp_start_off;
-      d.n_groups = op.grp_start.empty() ? 0 : static_cast<uint32_t>(op.grp_start.size() - 1);
-      d.grp_max = op.grp_max;
-      d.accumulate = op.root ? acc_flag : 0;
-      if constexpr (sizeof(R) == 4) {
-        if (op.config == kTcConfig) {
-          TcOp t;
-          t.node = op.node;
-          t.fa = op.fa;
-          t.fb = op.fb;
-          t.kc = op.kc;
-          t.nb = op.nb;
-          t.a_entries = op.a_entries;
-          t.a = reinterpret_cast<const float*>(arena + op.a_base);
-          t.ia = d.ia;
-          t.b = reinterpret_cast<const float2*>(d.b);
-          t.b_item = op.b_item;
-          t.b_slice = d.b_slice;
-          t.ib = d.ib;
-          t.tbn_lo = d.tbn.lo;
-          t.tbn_hi = d.tbn.hi;
-          t.tbn_bits = d.tbn.lo_bits;
-          t.tbk_lo = d.tbk.lo;
-          t.tbk_hi = d.tbk.hi;
-          t.tbk_bits = d.tbk.lo_bits;
-          t.grp_items = op.grp_max ? d.grp_items : nullptr;
-          t.grp_start = op.grp_max ? d.grp_start : nullptr;
-          t.n_groups = op.grp_max ? d.n_groups : 0;
-          t.slots = op.grp_max;
-          const uint64_t units = op.grp_max ? uint64_t{d.n_groups} * op.grp_max : op.nb;
-          const uint64_t bhat_elems = units << (op.fb + op.kc + 1);
-          t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off);
-          t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + bhat_elems);
-          t.out = reinterpret_cast<float2*>(d.out);
-          t.out_rows = d.out_rows;
-          t.out_item = op.out_item;
-          t.tom_lo = d.tom.lo;
-          t.tom_hi = d.tom.hi;
-          t.tom_bits = d.tom.lo_bits;
-          t.ton_lo = d.ton.lo;
-          t.ton_hi = d.ton.hi;
-          t.ton_bits = d.ton.lo_bits;
-          t.accumulate = d.accumulate;
-          t.n_contig = op.o_ncontig ? 1 : 0;
-          t.m_contig = op.o_mcontig ? 1 : 0;
-          tc_contract(t, st);
-          dp.engine->launches += 2;  // B̂ build + GEMM
-          if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
-          continue;
-        }
+  auto sstr = [&](int64_t off) -> const uint64_t* { return off < 0 ? nullptr : dp.d_sstr + off; };
+  for (size_t oi = 0; oi < c.ops.size(); ++oi) {
+    const Op& op = c.ops[oi];
+    if (op.nb == 0) continue;
+    if (op_events) CK(cudaEventRecord(op_events[2 * oi], st));
+    DevOp<T> d;
+    d.a = op.a_leaf ? leaves + op.a_base : arena + op.a_base;
+    d.b = op.b_leaf ? leaves + op.b_base : arena + op.b_base;
+    d.out = op.root ? acc : arena + op.out_base;
+    d.ia = dp.d_index + op.ia_off;
+    d.ib = dp.d_index + op.ib_off;
+    d.out_rows = op.root ? dp.d_index + op.out_rows_off : nullptr;
+    d.a_item = op.a_item;
+    d.b_item = op.b_item;
+    d.out_item = op.out_item;
+    d.a_slice = d.b_slice = 0;
+    d.a_sstr = sstr(dp.a_str_off[oi]);
+    d.b_sstr = sstr(dp.b_str_off[oi]);
+    d.cur = dp.d_cur;
+    d.s_bits = dp.s_bits;
+    d.root = op.root ? 1 : 0;
+    d.tam = dtable(dp.d_tables, op.tam);
+    d.tak = dtable(dp.d_tables, op.tak);
+    d.tbn = dtable(dp.d_tables, op.tbn);
+    d.tbk = dtable(dp.d_tables, op.tbk);
+    d.tom = dtable(dp.d_tables, op.tom);
+    d.ton = dtable(dp.d_tables, op.ton);
+    d.nb = op.nb;
+    d.fa = op.fa;
+    d.fb = op.fb;
+    d.kc = op.kc;
+    d.n_fast = op.store_n_fast ? 1 : 0;
+    d.a_kcontig = op.a_kcontig ? 1 : 0;
+    d.o_ncontig = op.o_ncontig ? 1 : 0;
+    d.grp_items = dp.d_index + op.grp_items_off;
+    d.grp_start = dp.d_index + op.grp_start_off;
+    d.n_groups = op.grp_start.empty() ? 0 : static_cast<uint32_t>(op.grp_start.size() - 1);
+    d.grp_max = op.grp_max;
+    d.accumulate = 0;
+    if constexpr (sizeof(R) == 4) {
+      if (op.config == kTcConfig) {
+        TcOp t;
+        t.node = op.node;
+        t.fa = op.fa;
+        t.fb = op.fb;
+        t.kc = op.kc;
+        t.nb = op.nb;
+        t.a_entries = op.a_entries;
+        t.a = reinterpret_cast<const float*>(arena + op.a_base);
+        t.ia = d.ia;
+        t.b = reinterpret_cast<const float2*>(d.b);
+        t.b_item = op.b_item;
+        t.b_sstr = d.b_sstr;
+        t.s_bits = d.s_bits;
+        t.cur = d.cur;
+        t.root = d.root;
+        t.ib = d.ib;
+        t.tbn_lo = d.tbn.lo;
+        t.tbn_hi = d.tbn.hi;
+        t.tbn_bits = d.tbn.lo_bits;
+        t.tbk_lo = d.tbk.lo;
+        t.tbk_hi = d.tbk.hi;
+        t.tbk_bits = d.tbk.lo_bits;
+        t.grp_items = op.grp_max ? d.grp_items : nullptr;
+        t.grp_start = op.grp_max ? d.grp_start : nullptr;
+        t.n_groups = op.grp_max ? d.n_groups : 0;
+        t.slots = op.grp_max;
+        const uint64_t units = op.grp_max ? uint64_t{d.n_groups} * op.grp_max : op.nb;
+        const uint64_t bhat_elems = units << (op.fb + op.kc + 1);
+        t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off);
+        t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + bhat_elems);
+        t.out = reinterpret_cast<float2*>(d.out);
+        t.out_rows = d.out_rows;
+        t.out_item = op.out_item;
+        t.tom_lo = d.tom.lo;
+        t.tom_hi = d.tom.hi;
+        t.tom_bits = d.tom.lo_bits;
+        t.ton_lo = d.ton.lo;
+        t.ton_hi = d.ton.hi;
+        t.ton_bits = d.ton.lo_bits;
+        t.n_contig = op.o_ncontig ? 1 : 0;
+        t.m_contig = op.o_mcontig ? 1 : 0;
+        tc_contract(t, st);
+        dp.engine->launches += 2;  // B̂ build + GEMM
+        if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
+        continue;
       }
-      launch_op<R>(d, op.config, st);
-      dp.engine->launches++;
-      if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
     }
-    if (c.has_leaf_root && c.n_rows > 0) {
-      const LeafRoot& lr = c.leaf_root;
-      const int r_out = static_cast<int>(c.out_legs.size());
-      const uint64_t total = c.n_rows << r_out;
-      const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, kSmSlots * 4);
-      leaf_root<T><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
-          leaves + c.slot_base[lr.slot], lr.item, dp.d_index + lr.rows_off, c.n_rows, r_out,
-          dtable(dp.d_tables, lr.tout), slice_offset(lr.slice_stride, s), acc, acc_flag);
-      dp.engine->launches++;
-    }
+    launch_op<R>(d, op.config, st);
+    dp.engine->launches++;
+    if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
+  }
+  if (c.has_leaf_root && c.n_rows > 0) {
+    const LeafRoot& lr = c.leaf_root;
+    const int r_out = static_cast<int>(c.out_legs.size());
+    const uint64_t total = c.n_rows << r_out;
+    const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, kSmSlots * 4);
+    leaf_root<T><<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        leaves + c.slot_base[lr.slot], lr.item, dp.d_index + lr.rows_off, c.n_rows, r_out,
+        dtable(dp.d_tables, lr.tout), sstr(dp.lr_str_off), dp.s_bits, dp.d_cur, acc);
+    dp.engine->launches++;
   }
   CK(cudaGetLastError());
+}
+
+void launch_slice(DevicePlan& dp, void* d_acc, cudaStream_t st, cudaEvent_t* op_events = nullptr) {
+  if (dp.c.precision == MTCG_C64)
+    launch_slice_ops<float>(dp, d_acc, st, op_events);
+  else
+    launch_slice_ops<double>(dp, d_acc, st, op_events);
+}
+
+void set_slice(DevicePlan& dp, uint64_t s, bool accumulate, cudaStream_t st) {
+  set_slice_kernel<<<1, 1, 0, st>>>(dp.d_cur, static_cast<uint32_t>(s), accumulate ? 1u : 0u);
+  dp.engine->launches++;
 }
 
 }  // namespace
@@ -956,7 +1009,25 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
   const uint64_t o_tables = up(o_leaves + std::max<uint64_t>(cc.leaf_elems * eb, 16));
   const uint64_t o_index = up(o_tables + 4 * std::max<size_t>(cc.table_blob.size(), 1));
   const uint64_t o_mult = up(o_index + 4 * std::max<size_t>(cc.index_blob.size(), 1));
-  const uint64_t o_xeb = up(o_mult + 4 * std::max<size_t>(cc.row_mult.size(), 1));
+  // per-bit slice strides of sliced leaf operands
+  std::vector<uint64_t> sstr;
+  auto put_strides = [&](const std::vector<uint64_t>& v) -> int64_t {
+    if (std::none_of(v.begin(), v.end(), [](uint64_t x) { return x != 0; })) return -1;
+    const int64_t off = static_cast<int64_t>(sstr.size());
+    sstr.insert(sstr.end(), v.begin(), v.end());
+    return off;
+  };
+  dp->s_bits = static_cast<int>(cc.sliced.size());
+  dp->a_str_off.assign(cc.ops.size(), -1);
+  dp->b_str_off.assign(cc.ops.size(), -1);
+  for (size_t i = 0; i < cc.ops.size(); ++i) {
+    if (cc.ops[i].a_leaf) dp->a_str_off[i] = put_strides(cc.ops[i].a_slice_stride);
+    if (cc.ops[i].b_leaf) dp->b_str_off[i] = put_strides(cc.ops[i].b_slice_stride);
+  }
+  if (cc.has_leaf_root) dp->lr_str_off = put_strides(cc.leaf_root.slice_stride);
+  const uint64_t o_sstr = up(o_mult + 4 * std::max<size_t>(cc.row_mult.size(), 1));
+  const uint64_t o_cur = up(o_sstr + 8 * std::max<size_t>(sstr.size(), 1));
+  const uint64_t o_xeb = up(o_cur + 8);
   const uint64_t total = up(o_xeb + sizeof(double) * 2 * kXebBlocks);
   uint8_t* h = static_cast<uint8_t*>(engine_pinned(e, total));
   CK(cudaStreamSynchronize(e->stream));  // staging may still feed an earlier copy
@@ -969,6 +1040,8 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
   std::memcpy(h + o_tables, cc.table_blob.data(), 4 * cc.table_blob.size());
   std::memcpy(h + o_index, cc.index_blob.data(), 4 * cc.index_blob.size());
   std::memcpy(h + o_mult, cc.row_mult.data(), 4 * cc.row_mult.size());
+  std::memcpy(h + o_sstr, sstr.data(), 8 * sstr.size());
+  std::memset(h + o_cur, 0, 8);
   dp->d_blob = blob_get(e, total);
   if (dp->d_blob) {
     // a pooled blob may still be read by work its old plan queued on any
@@ -985,6 +1058,8 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
   dp->d_tables = reinterpret_cast<uint32_t*>(d + o_tables);
   dp->d_index = reinterpret_cast<uint32_t*>(d + o_index);
   dp->d_row_mult = reinterpret_cast<uint32_t*>(d + o_mult);
+  dp->d_sstr = reinterpret_cast<uint64_t*>(d + o_sstr);
+  dp->d_cur = reinterpret_cast<uint32_t*>(d + o_cur);
   dp->d_xeb_part = reinterpret_cast<double*>(d + o_xeb);
   if (cc.arena_elems) {
     const uint64_t need = cc.arena_elems * eb;
@@ -1007,51 +1082,47 @@ void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accu
                 void* stream) {
   CK(cudaSetDevice(dp.engine->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
-  auto issue = [&] {
-    if (dp.c.precision == MTCG_C64)
-      run_slices_t<float>(dp, s0, s1, d_acc, accumulate, st);
-    else
-      run_slices_t<double>(dp, s0, s1, d_acc, accumulate, st);
-  };
-  // Replay the range as one CUDA graph (captured on first use): the device
-  // runs the ~200 launches per slice back to back with no host involvement.
-  // MTCG_NO_GRAPHS=1 issues the launches directly.
-  if (std::getenv("MTCG_NO_GRAPHS")) {
-    issue();
-    return;
-  }
-  const DevicePlan::GraphKey key{s0, s1, d_acc, accumulate};
-  auto it = dp.graphs.find(key);
-  if (it == dp.graphs.end()) {
-    // first use: issue directly (one-shot evaluations never pay for capture)
-    dp.graphs.emplace(key, DevicePlan::GraphEntry{});
-    issue();
-    return;
-  }
-  if (!it->second.exec) {  // second use: capture once, replay from now on
-    const uint64_t before = dp.engine->launches;
-    cudaGraph_t graph = nullptr;
-    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    try {
-      issue();
-    } catch (...) {
-      cudaStreamEndCapture(st, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      throw;
+  if (s0 >= s1) return;
+  // One slice's launches are captured as a CUDA graph on first use (per
+  // accumulator) and replayed for every slice after a set-slice kernel: the
+  // host issues 2 launches per slice. MTCG_NO_GRAPHS=1 launches directly.
+  const bool graphs = !std::getenv("MTCG_NO_GRAPHS");
+  DevicePlan::GraphEntry* ge = nullptr;
+  if (graphs) {
+    auto it = dp.graphs.find(d_acc);
+    if (it == dp.graphs.end()) {
+      const uint64_t before = dp.engine->launches;
+      cudaGraph_t graph = nullptr;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        launch_slice(dp, d_acc, st);
+      } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      CK(cudaStreamEndCapture(st, &graph));
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ierr = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CK(ierr);
+      DevicePlan::GraphEntry e;
+      e.exec = exec;
+      e.kernels = dp.engine->launches - before;
+      dp.engine->launches = before;  // counted when replayed
+      it = dp.graphs.emplace(d_acc, e).first;
     }
-    CK(cudaStreamEndCapture(st, &graph));
-    cudaGraphExec_t exec = nullptr;
-    const cudaError_t ierr = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    CK(ierr);
-    DevicePlan::GraphEntry e;
-    e.exec = exec;
-    e.kernels = dp.engine->launches - before;
-    dp.engine->launches = before;  // counted when replayed
-    it->second = e;
+    ge = &it->second;
   }
-  CK(cudaGraphLaunch(static_cast<cudaGraphExec_t>(it->second.exec), st));
-  dp.engine->launches += it->second.kernels;
+  for (uint64_t s = s0; s < s1; ++s) {
+    set_slice(dp, s, accumulate || s > s0, st);
+    if (ge) {
+      CK(cudaGraphLaunch(static_cast<cudaGraphExec_t>(ge->exec), st));
+      dp.engine->launches += ge->kernels;
+    } else {
+      launch_slice(dp, d_acc, st);
+    }
+  }
 }
 
 void time_ops(DevicePlan& dp, uint64_t slice, void* d_acc, bool accumulate, void* stream,
@@ -1061,10 +1132,8 @@ void time_ops(DevicePlan& dp, uint64_t slice, void* d_acc, bool accumulate, void
   const size_t n = dp.c.ops.size();
   std::vector<cudaEvent_t> ev(2 * n);
   for (auto& e : ev) CK(cudaEventCreate(&e));
-  if (dp.c.precision == MTCG_C64)
-    run_slices_t<float>(dp, slice, slice + 1, d_acc, accumulate, st, ev.data());
-  else
-    run_slices_t<double>(dp, slice, slice + 1, d_acc, accumulate, st, ev.data());
+  set_slice(dp, slice, accumulate, st);
+  launch_slice(dp, d_acc, st, ev.data());
   CK(cudaStreamSynchronize(st));
   for (size_t i = 0; i < n; ++i) {
     op_ms[i] = 0.f;

@@ -28,26 +28,21 @@ struct DevicePlan {
   double* d_xeb_part = nullptr;         // fused-XEB block partials (device)
   void* d_blob = nullptr;               // one allocation behind the pointers above
   uint64_t blob_bytes = 0;
-  std::vector<uint64_t> op_slice_off;   // word offset of each op's strides
-  uint64_t leaf_root_slice_off = 0;
-  // Instantiated CUDA graphs of whole slice ranges, keyed by
-  // (s0, s1, accumulator, accumulate): a step is one graph launch.
-  struct GraphKey {
-    uint64_t s0, s1;
-    void* acc;
-    bool accumulate;
-    bool operator<(const GraphKey& o) const {
-      if (s0 != o.s0) return s0 < o.s0;
-      if (s1 != o.s1) return s1 < o.s1;
-      if (acc != o.acc) return acc < o.acc;
-      return accumulate < o.accumulate;
-    }
-  };
+  // slice parameters in device memory: per-bit projection strides of sliced
+  // leaf operands (-1: operand not sliced) and the current {slice, accumulate}
+  uint64_t* d_sstr = nullptr;
+  uint32_t* d_cur = nullptr;
+  std::vector<int64_t> a_str_off, b_str_off;  // per op, into d_sstr
+  int64_t lr_str_off = -1;                    // leaf root
+  int s_bits = 0;
+  // One instantiated CUDA graph of a whole slice's launches per accumulator
+  // (slice parameters are read from d_cur, so the graph serves every slice):
+  // a slice is one tiny set-slice kernel plus one graph launch.
   struct GraphEntry {
     void* exec = nullptr;   // cudaGraphExec_t
     uint64_t kernels = 0;   // device launches replayed per graph launch
   };
-  std::map<GraphKey, GraphEntry> graphs;
+  std::map<void*, GraphEntry> graphs;
   ~DevicePlan();
 };
 

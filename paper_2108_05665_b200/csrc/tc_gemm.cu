@@ -239,7 +239,8 @@ struct TcParams {
   const uint32_t* out_rows;  // root: item -> accumulator row
   uint64_t out_item;         // complex elements per output entry
   TcTable tom, ton;          // m / n -> output offset (complex elements)
-  int accumulate;
+  const uint32_t* cur;       // device {slice, accumulate}: the root adds when set
+  int root;
   int n_contig;              // ton(n) = ton(n0) + (n - n0) within every tile
   int m_contig;              // tom(m + 1) = tom(m) + 1: lanes (rows) store coalesced
   int transpose;             // epilogue transposes 32-row chunks through smem
@@ -323,6 +324,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   float* stage_out = reinterpret_cast<float*>(coff_s + kEpiGroups * (kMaxBn / 2));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // the root accumulates into the accumulator on every slice but the first
+  const int accumulate = p.root ? static_cast<int>(__ldg(p.cur + 1)) : 0;
   const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
   const uint32_t tiles_m = (p.M + kBM - 1) / kBM;
   const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             if (m0 + quarter * 32 + row >= p.M || co < 0) continue;
             float2 val = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
             float2* dst = p.out + co + row_om;
-            if (p.accumulate) {
+            if (accumulate) {
               const float2 old = *dst;
               val.x += old.x;
               val.y += old.y;
@@ -602,7 +605,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             co[2 * j] = t2.x;
             co[2 * j + 1] = t2.y;
           }
-          if (p.n_contig && !p.accumulate) {
+          if (p.n_contig && !accumulate) {
             // column pairs are consecutive in the output (and in one item)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 *reinterpret_cast<float4*>(p.out + co[2 * j] + om) =
                     make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-          } else if (!p.accumulate) {
+          } else if (!accumulate) {
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               if (co[j] >= 0)
@@ -644,10 +647,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
 // + slot], zero blocks past the group's size), so a unit's B̂ is one
 // (slots * 2N) x 2K matrix.
 __global__ void build_bhat_kernel(const float2* b, uint64_t b_item, const uint32_t* ib,
-                                  uint64_t b_slice, TcTable tbn, TcTable tbk, int fb, int kc,
+                                  const uint64_t* b_sstr, int s_bits, const uint32_t* cur,
+                                  TcTable tbn, TcTable tbk, int fb, int kc,
                                   uint32_t units, uint32_t slots, const uint32_t* grp_items,
                                   const uint32_t* grp_start, float* bhi, float* blo) {
   const uint64_t N = uint64_t{1} << fb, K = uint64_t{1} << kc;
+  uint64_t b_slice = 0;
+  if (b_sstr) {
+    const uint32_t s = __ldg(cur);
+    for (int i = 0; i < s_bits; ++i)
+      if (s >> i & 1) b_slice += __ldg(b_sstr + i);
+  }
   const uint64_t per_unit = uint64_t{slots ? slots : 1u};
   const uint64_t total = uint64_t{units} * per_unit * N * K;
   for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
@@ -721,7 +731,8 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   // 1) B̂ hi / lo (small: per unit 2N_eff x 2K floats); A is split in the kernel
   const int blocks = static_cast<int>(std::min<uint64_t>(148 * 8, (uint64_t{units} * Nr / 2 * K + 255) / 256));
   TcTable tbn{op.tbn_lo, op.tbn_hi, op.tbn_bits}, tbk{op.tbk_lo, op.tbk_hi, op.tbk_bits};
-  build_bhat_kernel<<<blocks, 256, 0, st>>>(op.b, op.b_item, op.ib, op.b_slice, tbn, tbk, op.fb,
+  build_bhat_kernel<<<blocks, 256, 0, st>>>(op.b, op.b_item, op.ib, op.b_sstr, op.s_bits, op.cur,
+                                            tbn, tbk, op.fb,
                                             op.kc, units, op.slots, op.grp_items, op.grp_start,
                                             op.bhat_hi, op.bhat_lo);
   // 2) GEMM: persistent, one CTA per SM; smem = ring + ton cache + transpose
@@ -762,7 +773,8 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   p.out_item = op.out_item;
   p.tom = TcTable{op.tom_lo, op.tom_hi, op.tom_bits};
   p.ton = TcTable{op.ton_lo, op.ton_hi, op.ton_bits};
-  p.accumulate = op.accumulate;
+  p.cur = op.cur;
+  p.root = op.root;
   p.n_contig = op.n_contig && (op.slots == 0 || op.fb >= 1);
   p.m_contig = op.m_contig;
   p.transpose = transpose ? 1 : 0;

@@ -19,7 +19,11 @@ struct TcOp {
   const float* a;                 // A table (floats, interleaved complex)
   const uint32_t* ia;
   const float2* b;                // B operand table base
-  uint64_t b_item, b_slice;
+  uint64_t b_item;
+  const uint64_t* b_sstr;         // B slice projection: per-bit strides (null: none)
+  int s_bits;
+  const uint32_t* cur;            // device {slice index, root accumulates}
+  int root;
   const uint32_t* ib;
   const uint32_t *tbn_lo, *tbn_hi, *tbk_lo, *tbk_hi;
   int tbn_bits, tbk_bits;
@@ -30,7 +34,6 @@ struct TcOp {
   uint64_t out_item;
   const uint32_t *tom_lo, *tom_hi, *ton_lo, *ton_hi;
   int tom_bits, ton_bits;
-  int accumulate;
   int n_contig;                   // output n index contiguous (vector epilogue stores)
   int m_contig;                   // output m index contiguous (row-per-lane stores coalesce)
   // Grouped mode (slots > 0): items sharing an A entry are one GEMM whose N
