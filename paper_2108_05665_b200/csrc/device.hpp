@@ -43,6 +43,12 @@ struct DevicePlan {
     uint64_t kernels = 0;   // device launches replayed per graph launch
   };
   std::map<void*, GraphEntry> graphs;
+  // Concurrent capture: independent ops (disjoint subtrees) are issued on
+  // several streams joined by per-op events, so the captured slice graph is
+  // a DAG and small ops run side by side.
+  std::vector<void*> aux_streams;  // cudaStream_t
+  std::vector<void*> op_events;    // cudaEvent_t per op
+  std::vector<void*> join_events;  // cudaEvent_t per aux stream, + fork
   ~DevicePlan();
 };
 

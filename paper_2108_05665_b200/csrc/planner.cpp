@@ -752,6 +752,41 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     c.ops.push_back(std::move(op));
   }
   c.arena_elems = arena_top;
+  // --- dependencies between ops (arena read/write ranges) ---------------------
+  {
+    struct Access {
+      uint64_t lo, hi;
+      int op;
+      bool write;
+    };
+    std::vector<Access> seen;
+    std::vector<int> op_of_node(n, -1);
+    for (size_t i = 0; i < c.ops.size(); ++i) op_of_node[c.ops[i].node] = static_cast<int>(i);
+    for (size_t i = 0; i < c.ops.size(); ++i) {
+      Op& op = c.ops[i];
+      std::vector<std::pair<uint64_t, uint64_t>> reads, writes;
+      if (!op.a_leaf && table_elems[op.child_a]) reads.push_back({op.a_base, op.a_base + table_elems[op.child_a]});
+      if (!op.b_leaf && table_elems[op.child_b]) reads.push_back({op.b_base, op.b_base + table_elems[op.child_b]});
+      if (!op.root && table_elems[op.node]) writes.push_back({op.out_base, op.out_base + table_elems[op.node]});
+      if (op.scratch_elems) writes.push_back({op.scratch_off, op.scratch_off + op.scratch_elems});
+      std::vector<int> deps;
+      for (const Access& a : seen) {
+        bool hit = false;
+        for (const auto& r : reads) hit |= a.write && a.lo < r.second && r.first < a.hi;
+        for (const auto& w : writes) hit |= a.lo < w.second && w.first < a.hi;
+        if (hit && c.ops[a.op].nb > 0) deps.push_back(a.op);
+      }
+      // operand producers (also covered by their write records; explicit for
+      // zero-size tables)
+      for (int ch : {op.child_a, op.child_b})
+        if (op_of_node[ch] >= 0 && c.ops[op_of_node[ch]].nb > 0) deps.push_back(op_of_node[ch]);
+      std::sort(deps.begin(), deps.end());
+      deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+      op.deps = std::move(deps);
+      for (const auto& r : reads) seen.push_back({r.first, r.second, static_cast<int>(i), false});
+      for (const auto& w : writes) seen.push_back({w.first, w.second, static_cast<int>(i), true});
+    }
+  }
 
   if (p.node_slot[p.root] >= 0) {
     // single-slot network: the root leaf itself is every request's value
@@ -813,6 +848,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
                    " slots %u kcontig %d ncontig %d mcontig %d%s\n",
                    op.node, op.fa, op.fb, op.kc, op.nb, (long)da, (long)db, op.config, op.grp_max,
                    op.a_kcontig, op.o_ncontig, op.o_mcontig, op.root ? " root" : "");
+      std::fprintf(stderr, "[mtcg]   deps");
+      for (int d : op.deps) std::fprintf(stderr, " %d", c.ops[d].node);
+      std::fprintf(stderr, "\n");
     }
   }
   return c;

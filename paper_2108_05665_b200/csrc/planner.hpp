@@ -75,6 +75,10 @@ struct Op {
   bool a_kcontig = false;          // A rows are K-contiguous (tak(k) == k)
   bool o_ncontig = false;          // output n index is contiguous (ton(n) == n)
   bool o_mcontig = false;          // output m bit 0 has stride 1
+  // ops this op must wait for when independent ops run concurrently: the
+  // producers of its operands and every earlier op that used the arena
+  // ranges it writes (the first-fit arena reuses memory in schedule order)
+  std::vector<int> deps;
   // exact algorithmic counts per slice (tensor.cpp:132-148)
   uint64_t mults = 0, adds = 0, rw = 0;
 };
