@@ -987,7 +987,7 @@ void launch_slice(DevicePlan& dp, void* d_acc, cudaStream_t st, cudaEvent_t* op_
 // event nodes until the allocator keeps independent subtrees apart.
 void ensure_dag_resources(DevicePlan& dp) {
   if (!dp.join_events.empty()) return;
-  static const int k_env = std::getenv("MTCG_STREAMS") ? std::atoi(std::getenv("MTCG_STREAMS")) : 1;
+  const int k_env = std::getenv("MTCG_STREAMS") ? std::atoi(std::getenv("MTCG_STREAMS")) : 1;
   const int k = std::max(1, std::min(16, k_env));
   for (int i = 1; i < k; ++i) {
     cudaStream_t s;
