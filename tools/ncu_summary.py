@@ -1,6 +1,7 @@
 """Summarise ncu reports (``ncu -i <rep> --page raw --csv``) into the metrics
 the roofline needs: duration, DRAM bytes, DRAM / tensor / SM utilisation,
-registers, occupancy. Usage: python tools/ncu_summary.py rep1.ncu-rep [...]"""
+registers, occupancy. Usage: python tools/ncu_summary.py rep1.ncu-rep [...]
+       python tools/ncu_summary.py --launches launches.csv [header text]"""
 import csv
 import io
 import subprocess
@@ -40,7 +41,38 @@ def summarise(path):
     return res
 
 
+def launch_list(path, header=""):
+    """Per-kernel share of an ncu launch list (``--metrics
+    gpu__time_duration.sum --csv --log-file``): cold-cache, serialised
+    per-launch times, so compare shares, not absolutes."""
+    lines = [l for l in open(path) if l.startswith('"')]
+    rows = list(csv.reader(io.StringIO("".join(lines))))
+    hdr = rows[0]
+    ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = {}
+    total = 0.0
+    n = 0
+    for r in rows[1:]:
+        v = float(r[iv].replace(",", ""))
+        v = v / 1e6 if r[iu] == "ns" else (v / 1e3 if r[iu] in ("us", "usecond") else v)
+        name = r[ik].split("(")[0].replace("void ", "").replace("mtcg::<unnamed>::", "")
+        if "<" in r[ik]:
+            name = r[ik].replace("void ", "").replace("mtcg::<unnamed>::", "").split(">(")[0] + ">"
+        c, t = agg.get(name, (0, 0.0))
+        agg[name] = (c + 1, t + v)
+        total += v
+        n += 1
+    out = [header, "(cold-cache, serialised per-launch times: compare shares, not absolutes)",
+           f"launches {n}, total {total:.3f} ms"]
+    for name, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append(f"{100 * t / total:5.1f}% {c:6d} {t:10.3f} ms  {name[:100]}")
+    return "\n".join(out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--launches":
+        print(launch_list(sys.argv[2], " ".join(sys.argv[3:])))
+        sys.exit(0)
     for p in sys.argv[1:]:
         print(f"== {p}")
         for d in summarise(p):
