@@ -502,6 +502,20 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
                              std::to_string(cap_bytes) + " bytes)",
                          p.root);
 
+  // Small tables (and small tensor-core scratch) get private, never-reused
+  // space above the first-fit region: ops on independent subtrees then share
+  // no memory, so the slice graph's dependencies are the data dependencies
+  // (the first-fit region alone chains nearly every op through reuse). Not
+  // used under a memory cap, where the reference's accounting (live tables,
+  // multieval.cpp:38-47) is the whole budget. MTCG_PRIVATE_MB sets the size
+  // limit per table; default 0 (off): on cfg2 it shortens the dependency
+  // critical path from 9.7 to 8.6 of 10.2 ms, but the multi-stream graph
+  // measured no faster (the small ops compete with the large ones for SMs).
+  const uint64_t private_mb = std::getenv("MTCG_PRIVATE_MB") ? std::strtoull(std::getenv("MTCG_PRIVATE_MB"), nullptr, 10) : 0;
+  const uint64_t private_elems = cap_bytes ? 0 : (private_mb << 20) / c.elem_bytes;
+  uint64_t private_top = 0;
+  std::vector<char> node_private(n, 0);
+  std::vector<size_t> scratch_private;
   timer.mark("shapes+sched");
   // --- ops ------------------------------------------------------------------------
   // smallest log2 N sent to the tensor cores (MTCG_TC_MIN_FB overrides; tuning)
@@ -733,7 +747,13 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       const auto& rk = ti.rank[node];
       for (uint64_t row = 0; row < ti.rows; ++row) op.out_rows[rk[row]] = row;
     } else if (op.nb > 0) {
-      arena_off[node] = alloc(table_elems[node], node);
+      if (table_elems[node] <= private_elems) {
+        node_private[node] = 1;
+        arena_off[node] = private_top;
+        private_top += (table_elems[node] + align - 1) / align * align;
+      } else {
+        arena_off[node] = alloc(table_elems[node], node);
+      }
       op.out_base = arena_off[node];
     }
     if (op.config == kTcConfig && op.nb > 0) {
@@ -742,16 +762,30 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       const uint64_t units = op.grp_max ? uint64_t{op.grp_start.size() - 1} * op.grp_max : op.nb;
       const uint64_t bhat = units << (op.fb + op.kc + 1);
       op.scratch_elems = 2 * bhat;  // B̂ hi / lo (A is split in shared memory)
-      op.scratch_off = alloc(op.scratch_elems, node);
-      release(op.scratch_off, op.scratch_elems);  // free again once the op is done
+      if (op.scratch_elems <= private_elems) {
+        scratch_private.push_back(c.ops.size());
+        op.scratch_off = private_top;
+        private_top += (op.scratch_elems + align - 1) / align * align;
+      } else {
+        op.scratch_off = alloc(op.scratch_elems, node);
+        release(op.scratch_off, op.scratch_elems);  // free again once the op is done
+      }
     }
     // children are dead once consumed
     for (int ch : {l, r})
-      if (p.node_slot[ch] < 0 && ti.distinct[ch] > 0)
+      if (p.node_slot[ch] < 0 && ti.distinct[ch] > 0 && !node_private[ch])
         release(arena_off[ch], table_elems[ch]);
     c.ops.push_back(std::move(op));
   }
-  c.arena_elems = arena_top;
+  // private tables sit above the first-fit region
+  for (Op& op : c.ops) {
+    if (!op.a_leaf && node_private[op.child_a]) op.a_base += arena_top;
+    if (!op.b_leaf && node_private[op.child_b]) op.b_base += arena_top;
+    if (!op.root && node_private[op.node]) op.out_base += arena_top;
+  }
+  for (size_t i : scratch_private) c.ops[i].scratch_off += arena_top;
+  c.arena_elems = arena_top + private_top;
+  c.private_elems = private_top;
   // --- dependencies between ops (arena read/write ranges) ---------------------
   {
     struct Access {

@@ -123,6 +123,7 @@ struct Compiled {
   uint64_t mults = 0, adds = 0, rw = 0, contractions = 0;
   int n_slice_slots = 0;               // ops/leaf root needing slice offsets
 
+  uint64_t private_elems = 0;          // of arena_elems: never-reused small tables
   uint64_t arena_bytes() const { return arena_elems * elem_bytes; }
   uint64_t resident_bytes() const {
     return leaf_elems * elem_bytes + 4 * (table_blob.size() + index_blob.size());
