@@ -37,6 +37,11 @@ constexpr int kTcConfig = 12;
 // Row-streaming kernel over groups of items that share their A entry: each
 // A row is read once and multiplied by every item's B of the group.
 constexpr int kRowsGroupedConfig = 13;
+// One warp per output element (lanes split K, shuffle reduction) for items
+// with few outputs and a long K; complex64 only (the warp reduction changes
+// the summation order, so complex128's reference order keeps the generic
+// kernel).
+constexpr int kDotConfig = 15;
 // shared-memory budget for one group's B blocks (bytes)
 constexpr int kGroupSmemBytes = 48 * 1024;
 

@@ -172,6 +172,7 @@ struct DevOp {
   const uint32_t* grp_items;  // grouped rows kernel: items ordered by A entry
   const uint32_t* grp_start;  // ... CSR offsets per group
   uint32_t n_groups, grp_max;
+  uint32_t grp_split;         // blocks sharing one group's items (few-group ops)
 };
 
 __device__ __forceinline__ uint64_t slice_offset_dev(const uint64_t* str, int bits, uint32_t s) {
@@ -440,10 +441,17 @@ __global__ void __launch_bounds__(256, 2)
   uint32_t* kao = reinterpret_cast<uint32_t*>(Bs + op.grp_max * K * N);
   uint32_t* ono = kao + K;
   uint32_t* items = ono + N;                               // [g]
-  const uint64_t group = blockIdx.y + uint64_t{gridDim.y} * blockIdx.z;
+  const uint64_t gid = blockIdx.y + uint64_t{gridDim.y} * blockIdx.z;
+  const uint64_t group = gid / op.grp_split;
   if (group >= op.n_groups) return;
-  const uint32_t g0 = __ldg(op.grp_start + group);
-  const int g = static_cast<int>(__ldg(op.grp_start + group + 1) - g0);
+  // this block's share of the group's items
+  const uint32_t gs = __ldg(op.grp_start + group);
+  const int gfull = static_cast<int>(__ldg(op.grp_start + group + 1) - gs);
+  const int per = (gfull + static_cast<int>(op.grp_split) - 1) / static_cast<int>(op.grp_split);
+  const int i0 = static_cast<int>(gid % op.grp_split) * per;
+  const int g = min(per, gfull - i0);
+  if (g <= 0) return;
+  const uint32_t g0 = gs + static_cast<uint32_t>(i0);
   for (int i = threadIdx.x; i < g; i += blockDim.x) items[i] = __ldg(op.grp_items + g0 + i);
   __syncthreads();
   const uint32_t item0 = items[0];
@@ -554,6 +562,38 @@ __global__ void __launch_bounds__(256)
     for (uint64_t c = 0; c < K; ++c) cmac(acc, A[op.tak(c)], B[op.tbk(c)], c == 0);
     T* dst = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + item)} : item) * op.out_item + o;
     *dst = op.accumulate ? cadd(*dst, acc) : acc;
+  }
+}
+
+// ---- one warp per output element (complex64, long K) ----------------------------
+
+__global__ void __launch_bounds__(256)
+    contract_dot(const DevOp<float2> op_in) {
+  DevOp<float2> op = op_in;
+  resolve_slice(op);
+  const int r_out = op.fa + op.fb;
+  const uint64_t total = uint64_t{op.nb} << r_out;
+  const uint64_t K = uint64_t{1} << op.kc;
+  const uint64_t omask = (uint64_t{1} << r_out) - 1;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = uint64_t{gridDim.x} * (blockDim.x / 32);
+  for (uint64_t e = (blockIdx.x * uint64_t{blockDim.x} + threadIdx.x) / 32; e < total; e += warps) {
+    const uint64_t item = e >> r_out, o = e & omask;
+    const float2* A = op.a + uint64_t{op.ia ? __ldg(op.ia + item) : (uint32_t)item} * op.a_item +
+                      op.a_slice + op.tam(o);
+    const float2* B = op.b + uint64_t{op.ib ? __ldg(op.ib + item) : (uint32_t)item} * op.b_item +
+                      op.b_slice + op.tbn(o);
+    float2 acc = make_float2(0.f, 0.f);
+    for (uint64_t c = lane; c < K; c += 32) cmac(acc, A[op.tak(c)], B[op.tbk(c)], false);
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, sh);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, sh);
+    }
+    if (lane == 0) {
+      float2* dst = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + item)} : item) * op.out_item + o;
+      *dst = op.accumulate ? cadd(*dst, acc) : acc;
+    }
   }
 }
 
@@ -741,11 +781,18 @@ void launch_rows_grouped_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st)
   }
   const uint64_t M = uint64_t{1} << op.fa;
   const uint64_t n_chunks = (M + 256 * RPT - 1) / (256 * RPT);
-  const uint64_t want = std::max<uint64_t>(1, (148 * 16 + op.n_groups - 1) / op.n_groups);
+  // few row chunks x groups: split each group's items over several blocks
+  DevOp<T> o = op;
+  o.grp_split = 1;
+  if (n_chunks * op.n_groups < 2 * 148)
+    o.grp_split = static_cast<uint32_t>(std::min<uint64_t>(
+        op.grp_max, (2 * 148 + n_chunks * op.n_groups - 1) / (n_chunks * op.n_groups)));
+  const uint64_t units = uint64_t{op.n_groups} * o.grp_split;
+  const uint64_t want = std::max<uint64_t>(1, (148 * 16 + units - 1) / units);
   const unsigned gx = static_cast<unsigned>(std::min<uint64_t>(n_chunks, want));
-  const unsigned gy = std::min<uint32_t>(op.n_groups, 65535u);
-  const unsigned gz = (op.n_groups + gy - 1) / gy;
-  kern<<<dim3(gx, gy, gz), 256, smem, st>>>(op);
+  const unsigned gy = static_cast<unsigned>(std::min<uint64_t>(units, 65535u));
+  const unsigned gz = static_cast<unsigned>((units + gy - 1) / gy);
+  kern<<<dim3(gx, gy, gz), 256, smem, st>>>(o);
 }
 
 template <class R, int K>
@@ -776,6 +823,20 @@ void launch_op(const DevOp<typename V2<R>::T>& op, int config, cudaStream_t st) 
   switch (config) {
     case kRowsConfig: return launch_rows<R>(op, st);
     case kRowsGroupedConfig: return launch_rows_grouped<R>(op, st);
+    case kDotConfig:
+      if constexpr (sizeof(R) == 4) {
+        const uint64_t warps = uint64_t{op.nb} << (op.fa + op.fb);
+        const uint64_t blocks = std::min<uint64_t>((warps + 7) / 8, kSmSlots * 8);
+        contract_dot<<<static_cast<unsigned>(blocks), 256, 0, st>>>(op);
+        return;
+      }
+      [[fallthrough]];  // (complex128 never selects it)
+    case kGenericConfig: {
+      const uint64_t total = uint64_t{op.nb} << (op.fa + op.fb);
+      const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, kSmSlots * 4);
+      contract_generic<R><<<static_cast<unsigned>(blocks), 256, 0, st>>>(op);
+      return;
+    }
     case 1: return launch_tile<R, 128, 64, 8, 4>(op, st);
     case 2: return launch_tile<R, 128, 32, 8, 2>(op, st);
     case 3: return launch_tile<R, 128, 16, 4, 2>(op, st);
@@ -786,11 +847,7 @@ void launch_op(const DevOp<typename V2<R>::T>& op, int config, cudaStream_t st) 
     case 8: return launch_tile<R, 64, 64, 4, 4>(op, st);
     case 9: return launch_tile<R, 32, 32, 2, 2>(op, st);
     case 10: return launch_tile<R, 16, 16, 1, 1>(op, st);
-    default: {
-      const uint64_t total = uint64_t{op.nb} << (op.fa + op.fb);
-      const uint64_t blocks = std::min<uint64_t>((total + 255) / 256, kSmSlots * 4);
-      contract_generic<R><<<static_cast<unsigned>(blocks), 256, 0, st>>>(op);
-    }
+    default: throw CudaError("unknown kernel configuration " + std::to_string(config));
   }
 }
 
@@ -901,6 +958,7 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
     d.grp_start = dp.d_index + op.grp_start_off;
     d.n_groups = op.grp_start.empty() ? 0 : static_cast<uint32_t>(op.grp_start.size() - 1);
     d.grp_max = op.grp_max;
+    d.grp_split = 1;
     d.accumulate = 0;
     if constexpr (sizeof(R) == 4) {
       if (op.config == kTcConfig) {

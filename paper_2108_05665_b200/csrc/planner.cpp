@@ -585,6 +585,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       return v;
     };
     op.config = select_config(op.fa, op.fb, op.kc);
+    if (op.config == kGenericConfig && c.precision == MTCG_C64 && op.kc >= 6) op.config = kDotConfig;
     // Tensor-core path (complex64 only): dense, K-contiguous intermediate A,
     // shapes the 128 x (2N) x (2K) real tiles cover exactly.
     // Ops with intensity MNK / (MK + NK + MN) >= 6 complex MACs per element
@@ -683,8 +684,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       for (uint32_t x : space) s.push_back(contains(lay, x) ? stride_in(lay, x) : 0);
       return s;
     };
-    if (op.config == kGenericConfig) {
-      // per-output-element kernel: index the stored output directly
+    if (op.config == kGenericConfig || op.config == kDotConfig) {
+      // per-output-element kernels: index the stored output directly
       std::vector<uint32_t> o_legs(out_layout.rbegin(), out_layout.rend());
       op.tam.build(strides_of(o_legs, a_layout));   // A offset per out index
       op.tbn.build(strides_of(o_legs, b_layout));   // B offset per out index
@@ -704,7 +705,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       op.a_kcontig = !op.a_leaf;
       for (size_t b = 0; b < ks.size(); ++b) op.a_kcontig &= ks[b] == (uint64_t{1} << b);
       const auto ns = strides_of(n_legs, out_layout);
-      op.o_ncontig = op.config != kGenericConfig;
+      op.o_ncontig = op.config != kGenericConfig && op.config != kDotConfig;
       for (size_t b = 0; b < ns.size(); ++b) op.o_ncontig &= ns[b] == (uint64_t{1} << b);
       const auto ms = strides_of(m_legs, out_layout);
       op.o_mcontig = !ms.empty() && ms[0] == 1;

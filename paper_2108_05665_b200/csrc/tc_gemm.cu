@@ -740,6 +740,14 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   // Short output rows (<= 32 complex per tile row) that are strided in memory
   // are transposed through smem in the epilogue; longer rows are written per
   // lane with vector stores.
+  static int n_sms = 0;
+  if (!n_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // (narrower n tiles for ops with fewer tiles than SMs were measured slower:
+  // every tile still walks the whole K, now with smem-bound small MMAs)
   const int bn = tc_tile_n(static_cast<int>(Nr));
   const bool transpose = !op.m_contig && bn <= 64;
   const int extra = 1024 + 768 + 4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) + 16 +
@@ -779,16 +787,10 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   p.m_contig = op.m_contig;
   p.transpose = transpose ? 1 : 0;
   static size_t smem_set[2] = {0, 0};
-  static int n_sms = 0;
   auto kern = bk == 32 ? tc_gemm_persistent<32> : tc_gemm_persistent<16>;
   if (smem > smem_set[bk == 32]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     smem_set[bk == 32] = smem;
-  }
-  if (!n_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * units;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));
