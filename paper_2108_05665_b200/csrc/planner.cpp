@@ -151,7 +151,10 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
   std::vector<uint32_t> mark;
   std::vector<uint64_t> touched;
   const uint64_t mark_limit = 16 * rows + 4096;
+  const bool tdbg = std::getenv("MTCG_TIMING") != nullptr;
+  double t_sort = 0, t_keys = 0, t_rank = 0;
   for (int node : ix.postorder) {
+    auto c0 = std::chrono::steady_clock::now();
     std::vector<uint32_t>& rk = ti.rank[node];
     rk.resize(rows);
     uint64_t span;  // keys lie in [0, span)
@@ -172,18 +175,30 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
       for (uint64_t r = 0; r < rows; ++r) keys[r] = rl[r] * dr + rr[r];
       span = ti.distinct[p.node_left[node]] * dr;
     }
+    auto c1 = std::chrono::steady_clock::now();
     // Dense ranks in key order. Keys order like the reference's
     // (rank_l << 32 | rank_r) since rank_r < distinct[right].
     touched.clear();
     if (span <= mark_limit) {
       if (mark.size() < span) mark.resize(span, 0);
-      for (uint64_t r = 0; r < rows; ++r)
-        if (!mark[keys[r]]) {
-          mark[keys[r]] = 1;
-          touched.push_back(keys[r]);
-        }
-      std::sort(touched.begin(), touched.end());
-      for (size_t i = 0; i < touched.size(); ++i) mark[touched[i]] = static_cast<uint32_t>(i + 1);
+      if (span <= 4 * rows + 1024) {
+        // counting pass: mark the present keys, then number them in key order
+        for (uint64_t r = 0; r < rows; ++r) mark[keys[r]] = 1;
+        uint32_t cnt = 0;
+        for (uint64_t key = 0; key < span; ++key)
+          if (mark[key]) {
+            mark[key] = ++cnt;
+            touched.push_back(key);
+          }
+      } else {
+        for (uint64_t r = 0; r < rows; ++r)
+          if (!mark[keys[r]]) {
+            mark[keys[r]] = 1;
+            touched.push_back(keys[r]);
+          }
+        std::sort(touched.begin(), touched.end());
+        for (size_t i = 0; i < touched.size(); ++i) mark[touched[i]] = static_cast<uint32_t>(i + 1);
+      }
       for (uint64_t r = 0; r < rows; ++r) rk[r] = mark[keys[r]] - 1;
       for (uint64_t key : touched) mark[key] = 0;
     } else {
@@ -194,6 +209,9 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
         rk[r] = static_cast<uint32_t>(
             std::lower_bound(touched.begin(), touched.end(), keys[r]) - touched.begin());
     }
+    auto c2 = std::chrono::steady_clock::now();
+    t_keys += std::chrono::duration<double, std::milli>(c1 - c0).count();
+    t_rank += std::chrono::duration<double, std::milli>(c2 - c1).count();
     ti.distinct[node] = static_cast<uint32_t>(touched.size());
     if (p.node_slot[node] >= 0) {
       ti.rank_value[node].assign(touched.begin(), touched.end());
@@ -210,6 +228,7 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
       }
     }
   }
+  if (tdbg) std::fprintf(stderr, "[mtcg]   keys %.3f ms, ranks %.3f ms\n", t_keys, t_rank);
   return ti;
 }
 
@@ -235,18 +254,11 @@ void SplitTable::build(const std::vector<uint64_t>& strides) {
   const int hi_bits = bits - lo_bits;
   lo.assign(size_t{1} << lo_bits, 0);
   hi.assign(size_t{1} << hi_bits, 0);
-  for (uint64_t x = 0; x < lo.size(); ++x) {
-    uint64_t o = 0;
-    for (int b = 0; b < lo_bits; ++b)
-      if (x >> b & 1) o += strides[b];
-    lo[x] = static_cast<uint32_t>(o);
-  }
-  for (uint64_t x = 0; x < hi.size(); ++x) {
-    uint64_t o = 0;
-    for (int b = 0; b < hi_bits; ++b)
-      if (x >> b & 1) o += strides[lo_bits + b];
-    hi[x] = static_cast<uint32_t>(o);
-  }
+  // off(x) = off(x without its lowest set bit) + stride of that bit: O(size)
+  for (uint64_t x = 1; x < lo.size(); ++x)
+    lo[x] = static_cast<uint32_t>(lo[x & (x - 1)] + strides[__builtin_ctzll(x)]);
+  for (uint64_t x = 1; x < hi.size(); ++x)
+    hi[x] = static_cast<uint32_t>(hi[x & (x - 1)] + strides[lo_bits + __builtin_ctzll(x)]);
 }
 
 namespace {
@@ -260,6 +272,26 @@ struct PhaseTimer {
     std::fprintf(stderr, "[mtcg] %-14s %8.3f ms\n", what,
                  std::chrono::duration<double, std::milli>(now - t).count());
     t = now;
+  }
+};
+
+// MTCG_TIMING=1: per-section totals accumulated over the ops loop.
+struct SectionTimer {
+  bool on = std::getenv("MTCG_TIMING") != nullptr;
+  double ms[8] = {};
+  std::chrono::steady_clock::time_point t;
+  void start() {
+    if (on) t = std::chrono::steady_clock::now();
+  }
+  void lap(int i) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    ms[i] += std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+  }
+  void print(const char* const* names, int n) const {
+    if (!on) return;
+    for (int i = 0; i < n; ++i) std::fprintf(stderr, "[mtcg]   %-14s %8.3f ms\n", names[i], ms[i]);
   }
 };
 }  // namespace
@@ -521,7 +553,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
   // smallest log2 N sent to the tensor cores (MTCG_TC_MIN_FB overrides; tuning)
   const int tc_min_fb = std::getenv("MTCG_TC_MIN_FB") ? std::atoi(std::getenv("MTCG_TC_MIN_FB")) : 4;
   c.node_contractions.assign(n, 0);
+  SectionTimer sec;
   for (int node : sched) {
+    sec.start();
     const int l = p.node_left[node], r = p.node_right[node];
     const auto& L = legs[l];
     const auto& R = legs[r];
@@ -575,6 +609,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         op.ib[b] = op.b_leaf ? vb[rb[b]] : rb[b];
       }
     }
+    sec.lap(0);
     const auto& a_layout = layout[op.child_a];
     const auto& b_layout = layout[op.child_b];
     // m / n bit orders: free legs by increasing address in the output layout
@@ -666,6 +701,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       op.grp_items = std::move(g_order);
       op.grp_start = std::move(g_start);
     }
+    sec.lap(1);
     // m / n bit orders: free legs by increasing address in the output layout;
     // the tensor-core path walks A rows in A's memory order instead (TMA rows)
     std::vector<uint32_t> m_legs = by_out_addr(fa_legs);
@@ -711,6 +747,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       op.o_mcontig = !ms.empty() && ms[0] == 1;
     }
 
+    sec.lap(2);
     // sliced legs carried by leaf operands: offsets per set bit of the slice
     auto slice_strides = [&](int child, std::vector<uint64_t>& v) {
       if (p.node_slot[child] < 0 || S == 0) return false;
@@ -741,6 +778,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     c.rw += op.rw * op.nb * c.n_slices;
     c.contractions += static_cast<uint64_t>(op.nb) * c.n_slices;
 
+    sec.lap(3);
     // output storage
     op.out_item = d_open;
     if (op.root) {
@@ -777,6 +815,12 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       if (p.node_slot[ch] < 0 && ti.distinct[ch] > 0 && !node_private[ch])
         release(arena_off[ch], table_elems[ch]);
     c.ops.push_back(std::move(op));
+    sec.lap(4);
+  }
+  {
+    static const char* const names[] = {"operands", "kernel choice", "tables", "slice+counts",
+                                        "storage"};
+    sec.print(names, 5);
   }
   // private tables sit above the first-fit region
   for (Op& op : c.ops) {

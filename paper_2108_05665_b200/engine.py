@@ -14,7 +14,7 @@ and the multi-GPU slice scheduler.
 from __future__ import annotations
 
 import ctypes as C
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
 import numpy as np
@@ -44,16 +44,32 @@ class OpCounters:
     rw: int = 0
 
 
-@dataclass
 class EvalResult:
     """EvalResult (multieval.hpp:36-41). `values[i]` is request i's tensor;
-    `amplitudes` is the same data as an (n_requests, 2^w) array."""
+    `amplitudes` is the same data as an (n_requests, 2^w) array. The per-
+    request Tensor objects are built on first access of `values` (10^4
+    Python objects per fetch otherwise dominate — and, through GC, spike —
+    the host side of an end-to-end evaluation)."""
 
-    values: List[Tensor]
-    counters: OpCounters
-    peak_bytes: int
-    node_contractions: np.ndarray
-    amplitudes: np.ndarray = field(repr=False, default=None)
+    def __init__(self, out_legs: List[int], counters: OpCounters, peak_bytes: int,
+                 node_contractions: np.ndarray, amplitudes: np.ndarray):
+        self.out_legs = list(out_legs)
+        self.counters = counters
+        self.peak_bytes = peak_bytes
+        self.node_contractions = node_contractions
+        self.amplitudes = amplitudes
+        self._values: Optional[List[Tensor]] = None
+
+    @property
+    def values(self) -> List[Tensor]:
+        if self._values is None:
+            self._values = [Tensor(list(self.out_legs), self.amplitudes[i])
+                            for i in range(self.amplitudes.shape[0])]
+        return self._values
+
+    def __repr__(self) -> str:
+        return (f"EvalResult(n={self.amplitudes.shape[0]}, counters={self.counters}, "
+                f"peak_bytes={self.peak_bytes})")
 
 
 @dataclass
@@ -165,8 +181,7 @@ def _result_from(res: A.mtcg_result, vals: np.ndarray, nc: np.ndarray, n_req: in
                  w: int) -> EvalResult:
     amps = vals.view(np.complex128).reshape(n_req, w)
     legs = [int(res.out_legs[i]) for i in range(res.n_out_legs)]
-    values = [Tensor(list(legs), amps[i]) for i in range(n_req)]
-    return EvalResult(values, OpCounters(int(res.mults), int(res.adds), int(res.rw)),
+    return EvalResult(legs, OpCounters(int(res.mults), int(res.adds), int(res.rw)),
                       int(res.hbm_peak_bytes), nc.copy(), amps)
 
 
