@@ -92,7 +92,8 @@ struct TupleIndex {
   uint64_t rows = 0;
   std::vector<uint32_t> row_tuple_first;  // request index representing row
   std::vector<uint64_t> row_of_request;
-  std::vector<std::vector<uint32_t>> rank;        // [node][row]
+  // rank of every row per node: views into one pooled buffer (see below)
+  std::vector<uint32_t*> rank;                    // [node] -> [row]
   std::vector<std::vector<uint32_t>> rank_value;  // leaves: rank -> value index
   std::vector<std::vector<uint32_t>> pair_l, pair_r;  // internal: rank -> child ranks
   std::vector<uint32_t> distinct;
@@ -114,19 +115,29 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
   for (int j = 0; j < m; ++j)
     if (p.slot_n_values[j] > 1) informative.push_back(j);
   const size_t w = informative.size();
-  std::vector<uint32_t> compact(k * w);
+  static thread_local std::vector<uint32_t> compact;  // scratch kept across compiles
+  compact.resize(k * w);
   for (uint64_t i = 0; i < k; ++i)
     for (size_t c = 0; c < w; ++c) compact[i * w + c] = T[i * m + informative[c]];
   const uint32_t* Cp = compact.data();
-  std::vector<uint64_t> order(k);
+  // Lexicographic order by an LSD radix sort (one stable counting pass per
+  // informative column, value ranges are the slots' value counts): O(k w)
+  // instead of a comparison sort. Sorted rows also keep the per-node key
+  // passes below cache-friendly.
+  std::vector<uint64_t> order(k), tmp(k);
   std::iota(order.begin(), order.end(), 0);
-  auto lex_less = [&](uint64_t a, uint64_t b) {
-    return std::lexicographical_compare(Cp + a * w, Cp + a * w + w, Cp + b * w, Cp + b * w + w);
-  };
+  std::vector<uint64_t> count;
+  for (size_t c = w; c-- > 0;) {
+    const uint64_t span = static_cast<uint64_t>(p.slot_n_values[informative[c]]);
+    count.assign(span + 1, 0);
+    for (uint64_t i = 0; i < k; ++i) ++count[Cp[order[i] * w + c] + 1];
+    for (uint64_t v = 0; v < span; ++v) count[v + 1] += count[v];
+    for (uint64_t i = 0; i < k; ++i) tmp[count[Cp[order[i] * w + c]]++] = order[i];
+    order.swap(tmp);
+  }
   auto lex_eq = [&](uint64_t a, uint64_t b) {
     return std::equal(Cp + a * w, Cp + a * w + w, Cp + b * w);
   };
-  std::stable_sort(order.begin(), order.end(), lex_less);
   ti.row_of_request.assign(k, 0);
   for (uint64_t i = 0; i < k; ++i) {
     if (i == 0 || !lex_eq(order[i - 1], order[i]))
@@ -135,7 +146,14 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
   }
   ti.rows = ti.row_tuple_first.size();
   const uint64_t rows = ti.rows;
-  ti.rank.assign(p.n_nodes, {});
+  // One buffer for all nodes' rank arrays, kept per thread across compiles:
+  // re-allocating ~n_nodes x rows words per compile page-faults fresh memory
+  // every time (ms of jitter on the one-shot path).
+  static thread_local std::vector<uint32_t> rank_pool;
+  if (rank_pool.size() < uint64_t{static_cast<uint64_t>(p.n_nodes)} * rows)
+    rank_pool.resize(uint64_t{static_cast<uint64_t>(p.n_nodes)} * rows);
+  ti.rank.assign(p.n_nodes, nullptr);
+  for (int node = 0; node < p.n_nodes; ++node) ti.rank[node] = rank_pool.data() + uint64_t{static_cast<uint64_t>(node)} * rows;
   ti.rank_value.assign(p.n_nodes, {});
   ti.distinct.assign(p.n_nodes, 0);
   ti.pair_l.assign(p.n_nodes, {});
@@ -143,25 +161,26 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
   // informative columns of the distinct rows, slot-major (sequential reads)
   std::vector<int> column_of(m, -1);
   for (size_t c = 0; c < w; ++c) column_of[informative[c]] = static_cast<int>(c);
-  std::vector<uint32_t> cols(w * rows);
+  static thread_local std::vector<uint32_t> cols;
+  cols.resize(w * rows);
   for (uint64_t r = 0; r < rows; ++r)
     for (size_t c = 0; c < w; ++c)
       cols[c * rows + r] = Cp[static_cast<uint64_t>(ti.row_tuple_first[r]) * w + c];
-  std::vector<uint64_t> keys(rows);
-  std::vector<uint32_t> mark;
+  static thread_local std::vector<uint64_t> keys;
+  keys.resize(rows);
+  static thread_local std::vector<uint32_t> mark;  // all-zero between nodes and compiles
   std::vector<uint64_t> touched;
   const uint64_t mark_limit = 16 * rows + 4096;
   const bool tdbg = std::getenv("MTCG_TIMING") != nullptr;
-  double t_sort = 0, t_keys = 0, t_rank = 0;
+  double t_keys = 0, t_rank = 0;
   for (int node : ix.postorder) {
     auto c0 = std::chrono::steady_clock::now();
-    std::vector<uint32_t>& rk = ti.rank[node];
-    rk.resize(rows);
+    uint32_t* rk = ti.rank[node];
     uint64_t span;  // keys lie in [0, span)
     if (p.node_slot[node] >= 0) {
       const int c = column_of[p.node_slot[node]];
       if (c < 0) {  // single-valued slot: every row has value 0
-        std::fill(rk.begin(), rk.end(), 0u);
+        std::fill(rk, rk + rows, 0u);
         ti.distinct[node] = rows ? 1 : 0;
         if (rows) ti.rank_value[node].assign(1, 0u);
         continue;
@@ -169,8 +188,8 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
       for (uint64_t r = 0; r < rows; ++r) keys[r] = cols[c * rows + r];
       span = static_cast<uint64_t>(p.slot_n_values[p.node_slot[node]]);
     } else {
-      const auto& rl = ti.rank[p.node_left[node]];
-      const auto& rr = ti.rank[p.node_right[node]];
+      const uint32_t* rl = ti.rank[p.node_left[node]];
+      const uint32_t* rr = ti.rank[p.node_right[node]];
       const uint64_t dr = ti.distinct[p.node_right[node]];
       for (uint64_t r = 0; r < rows; ++r) keys[r] = rl[r] * dr + rr[r];
       span = ti.distinct[p.node_left[node]] * dr;
@@ -783,7 +802,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     op.out_item = d_open;
     if (op.root) {
       op.out_rows.resize(op.nb);
-      const auto& rk = ti.rank[node];
+      const uint32_t* rk = ti.rank[node];
       for (uint64_t row = 0; row < ti.rows; ++row) op.out_rows[rk[row]] = row;
     } else if (op.nb > 0) {
       if (table_elems[node] <= private_elems) {
