@@ -992,6 +992,7 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
         const uint64_t bhat_elems = units << (op.fb + op.kc + 1);
         t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off);
         t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + bhat_elems);
+        t.partials = reinterpret_cast<uint32_t*>(arena + op.scratch_off + 2 * bhat_elems);
         t.out = reinterpret_cast<float2*>(d.out);
         t.out_rows = d.out_rows;
         t.out_item = op.out_item;
@@ -1003,8 +1004,7 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
         t.ton_bits = d.ton.lo_bits;
         t.n_contig = op.o_ncontig ? 1 : 0;
         t.m_contig = op.o_mcontig ? 1 : 0;
-        tc_contract(t, st);
-        dp.engine->launches += 2;  // B̂ build + GEMM
+        dp.engine->launches += tc_contract(t, st);  // [absmax +] B̂ build + GEMM
         if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
         if (dag) dag->end(oi);
         continue;

@@ -819,7 +819,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       op.a_entries = ti.distinct[op.child_a];
       const uint64_t units = op.grp_max ? uint64_t{op.grp_start.size() - 1} * op.grp_max : op.nb;
       const uint64_t bhat = units << (op.fb + op.kc + 1);
-      op.scratch_elems = 2 * bhat;  // B̂ hi / lo (A is split in shared memory)
+      // B̂ hi / lo (A is split in shared memory) + 4 KB of operand-max partials
+      op.scratch_elems = 2 * bhat + 4096 / c.elem_bytes;
       if (op.scratch_elems <= private_elems) {
         scratch_private.push_back(c.ops.size());
         op.scratch_off = private_top;

@@ -22,6 +22,7 @@
 // while the next tiles' main loop runs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -201,6 +202,43 @@ __device__ __forceinline__ void mma_stage_wide(uint32_t d, uint64_t ahi, uint64_
   }
 }
 
+// 3xFP16 (kind::f16, fp32 accumulate) stage: the split operands are fp16 in
+// 64-byte SWIZZLE_64B rows (32 halves = 2 k-steps of 16), so the descriptors
+// are those of the 16-float TF32 stage. Same term order as mma_stage2.
+__device__ __forceinline__ void mma_stage_f16(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi,
+                                              uint64_t blo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b64 ah1, al1, bh1, bl1;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "add.s64 ah1, %1, 2;\n\tadd.s64 al1, %2, 2;\n\t"
+      "add.s64 bh1, %3, 2;\n\tadd.s64 bl1, %4, 2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], al1, bh1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah1, bl1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah1, bh1, %5, 1;\n\t}" ::"r"(d),
+      "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc));
+}
+
+// Wide 3xFP16 stage (bn <= 128): Âhi [B̂hi; B̂lo] (N = 2 bn) + Âlo B̂hi.
+__device__ __forceinline__ void mma_stage_f16_wide(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi,
+                                                   uint32_t idesc2, uint32_t idesc1, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b64 ah1, al1, bh1;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "add.s64 ah1, %1, 2;\n\tadd.s64 al1, %2, 2;\n\tadd.s64 bh1, %3, 2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], ah1, bh1, %4, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], al1, bh1, %5, 1;\n\t}" ::"r"(d),
+      "l"(ahi), "l"(alo), "l"(bhi), "r"(idesc2), "r"(idesc1), "r"(acc));
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -245,6 +283,7 @@ struct TcParams {
   int m_contig;              // tom(m + 1) = tom(m) + 1: lanes (rows) store coalesced
   int transpose;             // epilogue transposes 32-row chunks through smem
   unsigned long long* dbg;   // MTCG_TC_TRACE: per-tile role timestamps of CTA 0
+  const uint32_t* partials;  // 3xFP16: absmax partials (A, then B)
   // grouped mode (slots > 0): unit = group of items sharing the A entry;
   // complex column c of a unit -> item grp_items[grp_start[u] + (c >> fb)],
   // item column c & (2^fb - 1)
@@ -272,6 +311,25 @@ __device__ __forceinline__ float tf32_rna_alu(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
+// ---- 3xFP16 operand scaling ----------------------------------------------------
+//
+// fp16 has the TF32 significand (11 bits) but a 5-bit exponent, so each
+// operand is scaled by an exact power of two 2^s chosen from its max |x| so
+// that max |x| 2^s < 2^14: hi = rn_f16(x 2^s), lo = rn_f16(x 2^s - hi) keep 22
+// significant bits for every |x| >= max 2^-29 (smaller elements carry an
+// absolute error <= max 2^-40), and the epilogue multiplies by 2^-(sA+sB).
+// The maxima come from absmax_kernel's per-block partials (kAbsBlocks per
+// operand; stateless, no reset), reduced by every consumer block.
+constexpr int kAbsBlocks = 148;
+
+__device__ __forceinline__ int f16_scale_exp(uint32_t max_bits) {
+  if (max_bits == 0) return 0;
+  const int e = static_cast<int>((max_bits >> 23) & 0xFFu) - 127;  // max < 2^(e+1)
+  return max(-125, min(125, 13 - e));
+}
+
+__device__ __forceinline__ float pow2f(int s) { return __int_as_float((s + 127) << 23); }
+
 // ---- persistent warp-specialised variant -------------------------------------
 //
 // One CTA per SM loops over output tiles (item, m-tile, n-tile; n fastest so
@@ -280,6 +338,7 @@ __device__ __forceinline__ float tf32_rna_alu(float x) {
 //   warp 1      MMA issuer: 3 x (BK/8) tcgen05.mma per stage into a ring of up
 //               to 8 TMEM accumulators
 //   warps 2-5   converters: split each landed A stage into TF32 hi / lo in smem
+//               (F16: into scaled fp16 hi / lo, in place over the raw stage)
 //   warps 6-13  epilogue, two warpgroups taking alternate tiles: tcgen05.ld a
 //               finished accumulator, scatter complex results, release it —
 //               overlapping later tiles' main loops (short-K tiles are
@@ -292,7 +351,9 @@ constexpr int kMaxAcc = 8;          // TMEM accumulator buffers
 constexpr int kMaxTonCache = 2048;  // output column offsets cached in smem
 constexpr int kMaxBn = 256;         // real columns per tile
 
-template <int BK>
+// F16 = 3xFP16 operands (kind::f16, BK = 32 raw floats per stage = 2 k-steps
+// of 16); otherwise 3xTF32 (kind::tf32, BK/8 k-steps per stage).
+template <int BK, bool F16>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_persistent(const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ CUtensorMap map_bhi,
@@ -304,9 +365,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // compiler, so smem accesses below compile to LDS/STS rather than generic
   // LD/ST through L1.
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  static_assert(!F16 || BK == 32, "3xFP16 stages hold 32 raw floats of K");
+  // TF32: [A hi | A lo | B̂hi | B̂lo], fp32. F16: [A raw -> (A hi | A lo) | B̂hi
+  // | B̂lo], the fp16 operands in 64-byte SWIZZLE_64B rows.
   const int a_bytes = kBM * BK * 4;
-  const int b_bytes = p.bn * BK * 4;
-  const int stage_bytes = 2 * a_bytes + 2 * b_bytes;
+  const int b_bytes = p.bn * BK * (F16 ? 2 : 4);
+  const int a_span = F16 ? a_bytes : 2 * a_bytes;
+  const int stage_bytes = a_span + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(base + n_stages * stage_bytes);
   uint64_t* conv = full + kMaxStages;
   uint64_t* empty = conv + kMaxStages;
@@ -343,6 +408,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const bool ton_cached = n_item_cols <= kMaxTonCache;
   if (ton_cached)
     for (int n = threadIdx.x; n < n_item_cols; n += blockDim.x) ton_s[n] = p.ton(n);
+  if constexpr (F16) {  // operand maxima -> tmem_slot[1] (A), tmem_slot[2] (B)
+    if (threadIdx.x < 2) tmem_slot[1 + threadIdx.x] = 0;
+    __syncthreads();
+    if (threadIdx.x < 2 * kAbsBlocks)
+      atomicMax(&tmem_slot[1 + threadIdx.x / kAbsBlocks], __ldg(p.partials + threadIdx.x));
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
@@ -419,8 +490,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
           uint8_t* sp = base + st * stage_bytes;
           mbar_expect_tx(&full[st], a_bytes + 2 * b_bytes);
           tma_load_2d(sp, &map_a, &full[st], s * BK, a_row0);
-          tma_load_2d(sp + 2 * a_bytes, &map_bhi, &full[st], s * BK, b_row0);
-          tma_load_2d(sp + 2 * a_bytes + b_bytes, &map_blo, &full[st], s * BK, b_row0);
+          tma_load_2d(sp + a_span, &map_bhi, &full[st], s * BK, b_row0);
+          tma_load_2d(sp + a_span + b_bytes, &map_blo, &full[st], s * BK, b_row0);
         }
         trace(p, pit, 1);
       }
@@ -429,10 +500,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // (a single-thread branch makes ptxas wrap every tcgen05.mma in an
     // elect/R2UR loop: ~147 cycles per MMA instead of the ~40-cycle shared-
     // memory operand-read floor of a 128 x N x 8 tf32 MMA; tools/mma_bench.cu)
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                           (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
-    const uint32_t idesc2 = (1u << 4) | (2u << 7) | (2u << 10) |
-                            (static_cast<uint32_t>((2 * p.bn) >> 3) << 17) | ((kBM >> 4) << 24);
+    // c_format F32; a/b format TF32 (2) or F16 (0); K-major; N >> 3; M >> 4
+    constexpr uint32_t fmt = F16 ? 0u : (2u << 7) | (2u << 10);
+    const uint32_t idesc = (1u << 4) | fmt | (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
+    const uint32_t idesc2 =
+        (1u << 4) | fmt | (static_cast<uint32_t>((2 * p.bn) >> 3) << 17) | ((kBM >> 4) << 24);
     uint64_t g = 0, it = 0;
     for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const uint32_t tb = static_cast<uint32_t>(it % n_acc);
@@ -445,7 +517,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_wait(&conv[st], static_cast<uint32_t>(g / n_stages) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sp = smem_u32(base + st * stage_bytes);
-        if (wide)
+        if constexpr (F16) {
+          if (wide)
+            mma_stage_f16_wide(dacc, sw_desc<16>(sp), sw_desc<16>(sp + a_bytes / 2),
+                               sw_desc<16>(sp + a_bytes), idesc2, idesc, s > 0 ? 1u : 0u);
+          else
+            mma_stage_f16(dacc, sw_desc<16>(sp), sw_desc<16>(sp + a_bytes / 2), sw_desc<16>(sp + a_bytes),
+                          sw_desc<16>(sp + a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
+        } else if (wide)
           mma_stage_wide<BK / 8>(dacc, sw_desc<BK>(sp), sw_desc<BK>(sp + a_bytes),
                                  sw_desc<BK>(sp + 2 * a_bytes), idesc2, idesc, s > 0 ? 1u : 0u);
         else if constexpr (BK == 32)
@@ -462,11 +541,50 @@ __global__ void __launch_bounds__(kPThreads, 1)
   } else if (warp < 6) {  // ---- converters ----
     const int ct = threadIdx.x - 64;
     uint64_t g = 0, cit = 0;
+    const float sa = F16 ? pow2f(f16_scale_exp(tmem_slot[1])) : 1.f;
     for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++cit) {
       for (int s = 0; s < k_stages; ++s, ++g) {
         const int st = static_cast<int>(g % n_stages);
         mbar_wait(&full[st], static_cast<uint32_t>(g / n_stages) & 1);
         if (ct == 0 && s == 0) trace(p, cit, 4);
+        if constexpr (F16) {
+          // Raw stage: 128 rows x 128 B (SWIZZLE_128B: 16-byte chunk c of row r
+          // at c ^ (r & 7)). Thread pair q = (row r, 16-half column group j)
+          // reads its 8 floats (chunks 2j, 2j + 1), then — after all converter
+          // threads have read (in place) — writes 8 fp16 hi at r * 64 +
+          // (j ^ ((r >> 1) & 3)) * 16 (SWIZZLE_64B) and 8 fp16 lo 8 KB above.
+          uint8_t* sp = base + st * stage_bytes;
+          float4 v[4][2];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int q = ct + 128 * i, r = q >> 2, j = q & 3;
+            const float4* row = reinterpret_cast<const float4*>(sp + r * 128);
+            v[i][0] = row[(2 * j) ^ (r & 7)];
+            v[i][1] = row[(2 * j + 1) ^ (r & 7)];
+          }
+          asm volatile("bar.sync 3, 128;" ::: "memory");
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int q = ct + 128 * i, r = q >> 2, j = q & 3;
+            const float x[8] = {v[i][0].x * sa, v[i][0].y * sa, v[i][0].z * sa, v[i][0].w * sa,
+                                v[i][1].x * sa, v[i][1].y * sa, v[i][1].z * sa, v[i][1].w * sa};
+            uint32_t h[4], l[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __half2 hh = __floats2half2_rn(x[2 * e], x[2 * e + 1]);
+              const float2 hf = __half22float2(hh);
+              const __half2 ll = __floats2half2_rn(x[2 * e] - hf.x, x[2 * e + 1] - hf.y);
+              h[e] = *reinterpret_cast<const uint32_t*>(&hh);
+              l[e] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+            const int off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+            *reinterpret_cast<uint4*>(sp + off) = make_uint4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<uint4*>(sp + a_bytes / 2 + off) = make_uint4(l[0], l[1], l[2], l[3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&conv[st]);
+          continue;
+        }
         float4* hi = reinterpret_cast<float4*>(base + st * stage_bytes);
         float4* lo = reinterpret_cast<float4*>(base + st * stage_bytes + a_bytes);
 #pragma unroll
@@ -484,6 +602,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
     }
   } else {  // ---- epilogue: kEpiGroups warpgroups take alternate tiles ----
     const int eg = (warp - 6) / 4;  // epilogue group
+    // 3xFP16: undo the operand scales (exact powers of two)
+    const float osa = F16 ? pow2f(-f16_scale_exp(tmem_slot[1])) : 1.f;
+    const float osb = F16 ? pow2f(-f16_scale_exp(tmem_slot[2])) : 1.f;
     const int quarter = warp % 4;   // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;
     int64_t* coff = coff_s + eg * (kMaxBn / 2);
@@ -559,6 +680,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
           }
+          if constexpr (F16) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * osa * osb);
+          }
           // Output rows are not adjacent in memory: transpose the warp's
           // 32 rows x 16 complex chunk through shared memory so that
           // consecutive lanes write consecutive columns of a row.
@@ -594,6 +719,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
             tmem_ld16(tacc + c0 + 16 * h + p.bn, w);
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+          }
+          if constexpr (F16) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * osa * osb);
           }
           if (m >= p.M) continue;
           // the 8 column offsets (uniform across lanes): 4 LDS.128 up front,
@@ -642,37 +771,58 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
-// B̂ (2N x 2K floats per item, K-major) from the B operand, split hi/lo. In
-// grouped mode unit u holds `slots` item blocks (items grp_items[grp_start[u]
-// + slot], zero blocks past the group's size), so a unit's B̂ is one
-// (slots * 2N) x 2K matrix.
-__global__ void build_bhat_kernel(const float2* b, uint64_t b_item, const uint32_t* ib,
-                                  const uint64_t* b_sstr, int s_bits, const uint32_t* cur,
-                                  TcTable tbn, TcTable tbk, int fb, int kc,
-                                  uint32_t units, uint32_t slots, const uint32_t* grp_items,
-                                  const uint32_t* grp_start, float* bhi, float* blo) {
-  const uint64_t N = uint64_t{1} << fb, K = uint64_t{1} << kc;
-  uint64_t b_slice = 0;
-  if (b_sstr) {
-    const uint32_t s = __ldg(cur);
-    for (int i = 0; i < s_bits; ++i)
-      if (s >> i & 1) b_slice += __ldg(b_sstr + i);
+// B operand element e of the B̂ build (e = (blk * N + n) * K + k, blk = unit *
+// slots + slot in grouped mode; zero for the padding blocks of a group).
+struct BhatSrc {
+  const float2* b;
+  uint64_t b_item;
+  const uint32_t* ib;
+  const uint64_t* b_sstr;
+  int s_bits;
+  const uint32_t* cur;
+  TcTable tbn, tbk;
+  int fb, kc;
+  uint32_t slots;
+  const uint32_t* grp_items;
+  const uint32_t* grp_start;
+
+  __device__ __forceinline__ uint64_t slice_offset() const {
+    uint64_t off = 0;
+    if (b_sstr) {
+      const uint32_t s = __ldg(cur);
+      for (int i = 0; i < s_bits; ++i)
+        if (s >> i & 1) off += __ldg(b_sstr + i);
+    }
+    return off;
   }
-  const uint64_t per_unit = uint64_t{slots ? slots : 1u};
-  const uint64_t total = uint64_t{units} * per_unit * N * K;
-  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
-       e += uint64_t{gridDim.x} * blockDim.x) {
-    const uint64_t k = e % K, n = (e / K) % N, blk = e / (K * N);  // blk = unit * slots + slot
-    float2 v = make_float2(0.f, 0.f);
+  __device__ __forceinline__ float2 value(uint64_t e, uint64_t b_slice, uint64_t& k, uint64_t& n,
+                                          uint64_t& blk) const {
+    const uint64_t K = uint64_t{1} << kc, N = uint64_t{1} << fb;
+    k = e & (K - 1);
+    n = (e >> kc) & (N - 1);
+    blk = e >> (kc + fb);
     uint32_t item = static_cast<uint32_t>(blk);
-    bool live = true;
     if (slots) {
       const uint32_t u = static_cast<uint32_t>(blk / slots), slot = static_cast<uint32_t>(blk % slots);
       const uint32_t g0 = grp_start[u];
-      live = g0 + slot < grp_start[u + 1];
-      if (live) item = grp_items[g0 + slot];
+      if (g0 + slot >= grp_start[u + 1]) return make_float2(0.f, 0.f);
+      item = grp_items[g0 + slot];
     }
-    if (live) v = b[uint64_t{ib ? ib[item] : item} * b_item + b_slice + tbn(n) + tbk(k)];
+    return b[uint64_t{ib ? ib[item] : item} * b_item + b_slice + tbn(n) + tbk(k)];
+  }
+};
+
+// B̂ (2N x 2K floats per item, K-major) from the B operand, split TF32 hi/lo.
+// In grouped mode unit u holds `slots` item blocks (items grp_items[grp_start[u]
+// + slot], zero blocks past the group's size), so a unit's B̂ is one
+// (slots * 2N) x 2K matrix.
+__global__ void build_bhat_kernel(const BhatSrc src, uint64_t total, float* bhi, float* blo) {
+  const uint64_t K = uint64_t{1} << src.kc, N = uint64_t{1} << src.fb;
+  const uint64_t b_slice = src.slice_offset();
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    uint64_t k, n, blk;
+    const float2 v = src.value(e, b_slice, k, n, blk);
     const float q[4] = {v.x, -v.y, v.y, v.x};  // row 2n: [br, -bi]; row 2n+1: [bi, br]
     const uint64_t r0 = (blk * 2 * N + 2 * n) * (2 * K) + 2 * k;
     const uint64_t r1 = r0 + 2 * K;
@@ -684,6 +834,72 @@ __global__ void build_bhat_kernel(const float2* b, uint64_t b_item, const uint32
       bhi[idx[t]] = __uint_as_float(h);
       blo[idx[t]] = q[t] - __uint_as_float(h);
     }
+  }
+}
+
+__device__ __forceinline__ float block_max(float m, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  }
+  __syncthreads();
+  return m;
+}
+
+// partials[blk] = max |A| over a grid-stride share of the A table,
+// partials[kAbsBlocks + blk] = max |B| over the B elements the op reads.
+__global__ void __launch_bounds__(512) absmax_kernel(const float4* a, uint64_t a_n4, const BhatSrc src,
+                                                     uint64_t b_total, uint32_t* partials) {
+  __shared__ float red[32];
+  float m = 0.f;
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < a_n4;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    const float4 v = __ldg(a + i);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  m = block_max(m, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = __float_as_uint(m);
+  const uint64_t b_slice = src.slice_offset();
+  float mb = 0.f;
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < b_total;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    uint64_t k, n, blk;
+    const float2 v = src.value(e, b_slice, k, n, blk);
+    mb = fmaxf(mb, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+  mb = block_max(mb, red);
+  if (threadIdx.x == 0) partials[kAbsBlocks + blockIdx.x] = __float_as_uint(mb);
+}
+
+// B̂ as scaled fp16 hi / lo (same layout as build_bhat_kernel, 2-byte elements).
+__global__ void build_bhat_f16_kernel(const BhatSrc src, uint64_t total, const uint32_t* partials,
+                                      __half* bhi, __half* blo) {
+  __shared__ uint32_t mb;
+  if (threadIdx.x == 0) mb = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < kAbsBlocks; i += blockDim.x) atomicMax(&mb, partials[kAbsBlocks + i]);
+  __syncthreads();
+  const float sb = pow2f(f16_scale_exp(mb));
+  const uint64_t K = uint64_t{1} << src.kc, N = uint64_t{1} << src.fb;
+  const uint64_t b_slice = src.slice_offset();
+  for (uint64_t e = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; e < total;
+       e += uint64_t{gridDim.x} * blockDim.x) {
+    uint64_t k, n, blk;
+    const float2 v = src.value(e, b_slice, k, n, blk);
+    const float xr = v.x * sb, xi = v.y * sb;
+    const uint64_t r0 = (blk * 2 * N + 2 * n) * (2 * K) + 2 * k;
+    const uint64_t r1 = r0 + 2 * K;
+    const __half2 h0 = __floats2half2_rn(xr, -xi), h1 = __floats2half2_rn(xi, xr);
+    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+    *reinterpret_cast<__half2*>(bhi + r0) = h0;
+    *reinterpret_cast<__half2*>(bhi + r1) = h1;
+    *reinterpret_cast<__half2*>(blo + r0) = __floats2half2_rn(xr - f0.x, -xi - f0.y);
+    *reinterpret_cast<__half2*>(blo + r1) = __floats2half2_rn(xi - f1.x, xr - f1.y);
   }
 }
 
@@ -701,15 +917,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-CUtensorMap make_map(const float* base, uint64_t cols, uint64_t rows, uint32_t box_rows, int bk) {
+// 2D K-major map, box = bk elements x box_rows; 128-byte rows swizzle 128B,
+// 64-byte rows 64B (fp32 bk = 32 / 16, fp16 bk = 32).
+CUtensorMap make_map(const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows, int bk,
+                     bool f16 = false) {
   CUtensorMap m;
+  const uint64_t esize = f16 ? 2 : 4;
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * sizeof(float)};
+  cuuint64_t strides[1] = {cols * esize};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(bk), box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           bk == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+  CUresult r = encode_fn()(&m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                           2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           bk * esize == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
@@ -718,23 +939,64 @@ CUtensorMap make_map(const float* base, uint64_t cols, uint64_t rows, uint32_t b
 
 }  // namespace
 
+bool tc_f16() {
+  // 3xFP16 (default) or 3xTF32 (MTCG_TC_KIND=tf32) split operands
+  static const bool f16 = !(std::getenv("MTCG_TC_KIND") && std::string(std::getenv("MTCG_TC_KIND")) == "tf32");
+  return f16;
+}
+
+// 3xFP16 halves the MMA time but needs max |A| first (one extra pass over
+// the A table, until the producers emit it). Take it when the op reuses each
+// A entry across enough output columns that the tensor-core time dominates:
+// units * N_eff >= 192 * a_entries (cfg2: nodes 279, 227; not the low-K,
+// HBM-bound ops such as 337 or 285).
+bool tc_use_f16(const TcOp& op) {
+  if (!tc_f16()) return false;
+  static const bool always = std::getenv("MTCG_TC_F16_ALL") != nullptr;
+  if (always) return true;
+  const uint64_t units = op.slots ? op.n_groups : op.nb;
+  const uint64_t n_eff = (uint64_t{1} << op.fb) * (op.slots ? op.slots : 1u);
+  return units * n_eff >= 192 * op.a_entries;
+}
+
 int tc_tile_n(int Nr) {
   static const int cap = std::getenv("MTCG_TC_BN") ? std::atoi(std::getenv("MTCG_TC_BN")) : 256;
   return Nr >= cap ? cap : Nr;
 }
 
-void tc_contract(const TcOp& op, cudaStream_t st) {
+int tc_contract(const TcOp& op, cudaStream_t st) {
   const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb, K = uint64_t{1} << op.kc;
   // units: items, or groups of items sharing the A entry (N_eff = slots x N)
   const uint32_t units = op.slots ? op.n_groups : op.nb;
   const uint64_t Nr = 2 * N * (op.slots ? op.slots : 1u), Kr = 2 * K;
-  // 1) B̂ hi / lo (small: per unit 2N_eff x 2K floats); A is split in the kernel
-  const int blocks = static_cast<int>(std::min<uint64_t>(148 * 8, (uint64_t{units} * Nr / 2 * K + 255) / 256));
-  TcTable tbn{op.tbn_lo, op.tbn_hi, op.tbn_bits}, tbk{op.tbk_lo, op.tbk_hi, op.tbk_bits};
-  build_bhat_kernel<<<blocks, 256, 0, st>>>(op.b, op.b_item, op.ib, op.b_sstr, op.s_bits, op.cur,
-                                            tbn, tbk, op.fb,
-                                            op.kc, units, op.slots, op.grp_items, op.grp_start,
-                                            op.bhat_hi, op.bhat_lo);
+  const bool f16 = tc_use_f16(op);
+  // 1) B̂ hi / lo (small: per unit 2N_eff x 2K); A is split in the kernel. The
+  // 3xFP16 path first reduces max |A| and max |B| into per-block partials.
+  const uint64_t b_total = uint64_t{units} * Nr / 2 * K;
+  const int blocks = static_cast<int>(std::min<uint64_t>(148 * 8, (b_total + 255) / 256));
+  BhatSrc src;
+  src.b = op.b;
+  src.b_item = op.b_item;
+  src.ib = op.ib;
+  src.b_sstr = op.b_sstr;
+  src.s_bits = op.s_bits;
+  src.cur = op.cur;
+  src.tbn = TcTable{op.tbn_lo, op.tbn_hi, op.tbn_bits};
+  src.tbk = TcTable{op.tbk_lo, op.tbk_hi, op.tbk_bits};
+  src.fb = op.fb;
+  src.kc = op.kc;
+  src.slots = op.slots;
+  src.grp_items = op.grp_items;
+  src.grp_start = op.grp_start;
+  if (f16) {
+    absmax_kernel<<<kAbsBlocks, 512, 0, st>>>(reinterpret_cast<const float4*>(op.a),
+                                              op.a_entries * M * Kr / 4, src, b_total, op.partials);
+    build_bhat_f16_kernel<<<blocks, 256, 0, st>>>(src, b_total, op.partials,
+                                                  reinterpret_cast<__half*>(op.bhat_hi),
+                                                  reinterpret_cast<__half*>(op.bhat_lo));
+  } else {
+    build_bhat_kernel<<<blocks, 256, 0, st>>>(src, b_total, op.bhat_hi, op.bhat_lo);
+  }
   // 2) GEMM: persistent, one CTA per SM; smem = ring + ton cache + transpose
   // buffers; keep >= 2 stages (halve the n tile if needed)
   // Short output rows (<= 32 complex per tile row) that are strided in memory
@@ -754,17 +1016,21 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
                     8 * kEpiGroups * (kMaxBn / 2) +
                     (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
   constexpr int kSmemMax = 227 * 1024;
-  auto stage_of = [&](int bk) { return 2 * kBM * bk * 4 + 2 * bn * bk * 4; };
-  // 32-float stages unless only 2 of them fit (MTCG_TC_BK overrides)
+  auto stage_of = [&](int bk) {
+    return f16 ? kBM * bk * 4 + 2 * bn * bk * 2 : 2 * kBM * bk * 4 + 2 * bn * bk * 4;
+  };
+  // TF32: 32-float stages unless only 2 of them fit (MTCG_TC_BK overrides);
+  // 3xFP16: 32 raw floats (in-place split: 16 KB A + 2 x bn x 64 B B̂)
   static const int bk_env = std::getenv("MTCG_TC_BK") ? std::atoi(std::getenv("MTCG_TC_BK")) : 0;
-  const int bk = bk_env == 16 || bk_env == 32 ? bk_env
+  const int bk = f16 ? 32
+                 : bk_env == 16 || bk_env == 32 ? bk_env
                  : (kSmemMax - extra) / stage_of(32) >= 3 ? 32 : 16;
   const int stage_bytes = stage_of(bk);
   const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
   const size_t smem = extra + static_cast<size_t>(n_stages) * stage_bytes;
   const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM, bk);
-  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn, bk);
-  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn, bk);
+  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn, bk, f16);
+  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn, bk, f16);
   TcParams p;
   p.M = static_cast<int>(M);
   p.Nr = static_cast<int>(Nr);
@@ -786,11 +1052,14 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
   p.n_contig = op.n_contig && (op.slots == 0 || op.fb >= 1);
   p.m_contig = op.m_contig;
   p.transpose = transpose ? 1 : 0;
-  static size_t smem_set[2] = {0, 0};
-  auto kern = bk == 32 ? tc_gemm_persistent<32> : tc_gemm_persistent<16>;
-  if (smem > smem_set[bk == 32]) {
+  p.partials = op.partials;
+  static size_t smem_set[3] = {0, 0, 0};
+  const int kv = f16 ? 2 : bk == 32 ? 1 : 0;
+  auto kern = f16 ? tc_gemm_persistent<32, true>
+                  : bk == 32 ? tc_gemm_persistent<32, false> : tc_gemm_persistent<16, false>;
+  if (smem > smem_set[kv]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    smem_set[bk == 32] = smem;
+    smem_set[kv] = smem;
   }
   const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * units;
   const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));
@@ -808,8 +1077,8 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
     cudaStreamSynchronize(st);
     cudaFree(p.dbg);
     const unsigned long long t0 = h[0];
-    std::fprintf(stderr, "[tc trace node %d] bk=%d stages=%d bn=%d tiles=%llu grid=%u n_acc<=%d\n",
-                 op.node, bk, n_stages, bn, static_cast<unsigned long long>(tiles), grid, kMaxAcc);
+    std::fprintf(stderr, "[tc trace node %d] f16=%d bk=%d stages=%d bn=%d tiles=%llu grid=%u n_acc<=%d\n",
+                 op.node, f16 ? 1 : 0, bk, n_stages, bn, static_cast<unsigned long long>(tiles), grid, kMaxAcc);
     std::fprintf(stderr, " tile  prod0  prod1  conv(full) mma0  mma1  epi0  epi1   (cycles from tile0 prod0)\n");
     for (int i = 0; i < kTraceTiles; ++i) {
       if (!h[i * 8]) break;
@@ -821,6 +1090,7 @@ void tc_contract(const TcOp& op, cudaStream_t st) {
                      (long long)(h[i * 8 + 6] - t0));
     }
   }
+  return f16 ? 3 : 2;
 }
 
 }  // namespace mtcg

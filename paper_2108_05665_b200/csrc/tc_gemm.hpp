@@ -1,4 +1,4 @@
-// tcgen05 3xTF32 complex GEMM path (see tc_gemm.cu).
+// tcgen05 split-precision (3xFP16 / 3xTF32) complex GEMM path (see tc_gemm.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -27,8 +27,9 @@ struct TcOp {
   const uint32_t* ib;
   const uint32_t *tbn_lo, *tbn_hi, *tbk_lo, *tbk_hi;
   int tbn_bits, tbk_bits;
-  float* bhat_hi;                 // scratch: units * 2N_eff * 2K floats
+  float* bhat_hi;                 // scratch: units * 2N_eff * 2K floats (3xFP16: halves)
   float* bhat_lo;
+  uint32_t* partials;             // scratch: 2 x 148 words of operand maxima (3xFP16)
   float2* out;
   const uint32_t* out_rows;
   uint64_t out_item;
@@ -44,7 +45,10 @@ struct TcOp {
   uint32_t slots;
 };
 
-void tc_contract(const TcOp& op, cudaStream_t st);
+// Launches the op's kernels on `st`; returns how many.
+int tc_contract(const TcOp& op, cudaStream_t st);
+bool tc_f16();                   // 3xFP16 split operands allowed (default) vs 3xTF32 only
+bool tc_use_f16(const TcOp& op);  // this op takes the 3xFP16 path
 int tc_tile_n(int n_real);
 
 }  // namespace mtcg
