@@ -306,7 +306,17 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
             traffic = json.load(open(prof)).get(f"node{top.node}")
         except Exception:  # noqa: BLE001
             traffic = None
+    scheme = {}
+    if bound == "tensor" and top.kernel == 12:
+        # split-precision complex GEMM: every real MAC costs 3 tensor-core MMAs
+        # (hi*hi + hi*lo + lo*hi) at the fp16 rate (3xFP16, default) or at half
+        # of it (3xTF32, MTCG_TC_KIND=tf32)
+        tf32 = os.environ.get("MTCG_TC_KIND") == "tf32"
+        ceiling = peak / (6.0 if tf32 else 3.0)
+        scheme = {"scheme": "3xTF32" if tf32 else "3xFP16 (power-of-2 scaled fp16 hi/lo)",
+                  "scheme_ceiling": ceiling, "frac_of_scheme_ceiling": achieved / ceiling}
     return {
+        **scheme,
         "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
         "frac": achieved / peak, "traffic": traffic,
         "kernel": (f"node {top.node}: M=2^{top.fa} N=2^{top.fb} K=2^{top.kc} x{top.batch} "

@@ -284,6 +284,8 @@ struct TcParams {
   int transpose;             // epilogue transposes 32-row chunks through smem
   unsigned long long* dbg;   // MTCG_TC_TRACE: per-tile role timestamps of CTA 0
   const uint32_t* partials;  // 3xFP16: absmax partials (A, then B)
+  int n_conv;                // converter warps (4 or 8); the other 12 - n_conv warps
+                             // form (12 - n_conv) / 4 epilogue groups
   // grouped mode (slots > 0): unit = group of items sharing the A entry;
   // complex column c of a unit -> item grp_items[grp_start[u] + (c >> fb)],
   // item column c & (2^fb - 1)
@@ -344,16 +346,123 @@ __device__ __forceinline__ float pow2f(int s) { return __int_as_float((s + 127) 
 //               overlapping later tiles' main loops (short-K tiles are
 //               epilogue-bound; MTCG_TC_TRACE=<node> prints role timestamps).
 // The ring depth S is chosen so the stages fill ~220 KB of shared memory.
-constexpr int kEpiGroups = 2;       // epilogue warpgroups (alternate tiles)
+// Long-K ops (>= 32 stages per tile) run 8 converter warps (warps 2-9) and one
+// epilogue group (warps 10-13): the split is the per-stage critical path
+// there, the epilogue has a whole main loop to drain each tile.
+constexpr int kEpiGroups = 2;       // max epilogue warpgroups (alternate tiles)
 constexpr int kPThreads = 192 + 128 * kEpiGroups;
 constexpr int kMaxStages = 12;
 constexpr int kMaxAcc = 8;          // TMEM accumulator buffers
 constexpr int kMaxTonCache = 2048;  // output column offsets cached in smem
 constexpr int kMaxBn = 256;         // real columns per tile
 
+// ---- CTA-pair (cta_group::2) helpers ----
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// Shared::cluster address of the same smem object in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+
+// Arrive on a barrier of another CTA of the cluster. The default-semantics
+// form (as CUTLASS's ClusterBarrier::arrive): `.release.cluster` compiles to
+// MEMBAR.ALL.GPU + ERRBAR per arrive, which stalled the pair kernel's
+// converters (tools/mma_f16_bench.cu, profiles/r01).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Waits on barriers the peer CTA arrives on. The default (.acquire.cta)
+// try_wait is what CUTLASS's 2-SM pipelines use for peer-signalled barriers;
+// MTCG_TC_ACQ_CLUSTER=1 builds use the cluster-scope form instead.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+#ifdef MTCG_TC_ACQ_CLUSTER
+  while (!mbar_try_wait_cluster(bar, parity)) {
+  }
+#else
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#endif
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// 3xFP16 stage on the CTA pair (M = 256: A rows 0-127 in the leader's smem,
+// 128-255 in the peer's; B̂ rows split likewise; D rows in each CTA's TMEM).
+__device__ __forceinline__ void mma_stage_f16_pair(uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi,
+                                                   uint64_t blo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b64 ah1, al1, bh1, bl1;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "add.s64 ah1, %1, 2;\n\tadd.s64 al1, %2, 2;\n\t"
+      "add.s64 bh1, %3, 2;\n\tadd.s64 bl1, %4, 2;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %4, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], al1, bh1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ah1, bl1, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], ah1, bh1, %5, 1;\n\t}" ::"r"(d),
+      "l"(ahi), "l"(alo), "l"(bhi), "l"(blo), "r"(idesc), "r"(acc));
+}
+
+// Commit the pair's issued MMAs to the same barrier in both CTAs.
+__device__ __forceinline__ void mma_commit_pair_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+// Position in the smem / TMEM rings: slot and wrap count (no 64-bit
+// divisions per stage — they cost ~50 instructions on every role's loop).
+struct Ring {
+  int slot = 0;
+  uint32_t round = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      ++round;
+    }
+  }
+};
+
 // F16 = 3xFP16 operands (kind::f16, BK = 32 raw floats per stage = 2 k-steps
 // of 16); otherwise 3xTF32 (kind::tf32, BK/8 k-steps per stage).
-template <int BK, bool F16>
+// PAIR (F16, bn = 256 only): a 2-CTA cluster computes 256 x bn tiles with
+// cta_group::2 MMAs. Each CTA loads its own 128 A rows and HALF of the B̂ tile
+// (bn / 2 rows of hi and lo): 32 KB per stage instead of 48 KB for the same
+// tensor work, so 6 stages are in flight instead of 4. Both CTAs produce and
+// convert; their converters arrive on the leader's conv barrier (remote
+// arrive), the leader issues the MMAs and multicasts the stage / accumulator
+// commits to both CTAs, and both CTAs' epilogues drain their own TMEM rows and
+// arrive on the leader's acc_empty.
+template <int BK, bool F16, bool PAIR = false>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_gemm_persistent(const __grid_constant__ CUtensorMap map_a,
                        const __grid_constant__ CUtensorMap map_bhi,
@@ -366,10 +475,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // LD/ST through L1.
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   static_assert(!F16 || BK == 32, "3xFP16 stages hold 32 raw floats of K");
+  static_assert(!PAIR || F16, "CTA pairs run the 3xFP16 kernel");
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const uint32_t cta0 = PAIR ? blockIdx.x / 2 : blockIdx.x;  // tile walker start / step
+  const uint32_t ncta = PAIR ? gridDim.x / 2 : gridDim.x;
+  constexpr int kTM = PAIR ? 2 * kBM : kBM;                     // tile rows
+  const int m_off = static_cast<int>(rank) * kBM;               // this CTA's rows in the tile
+  const int bn_cta = PAIR ? p.bn / 2 : p.bn;                    // B̂ rows this CTA loads
   // TF32: [A hi | A lo | B̂hi | B̂lo], fp32. F16: [A raw -> (A hi | A lo) | B̂hi
   // | B̂lo], the fp16 operands in 64-byte SWIZZLE_64B rows.
   const int a_bytes = kBM * BK * 4;
-  const int b_bytes = p.bn * BK * (F16 ? 2 : 4);
+  const int b_bytes = bn_cta * BK * (F16 ? 2 : 4);
   const int a_span = F16 ? a_bytes : 2 * a_bytes;
   const int stage_bytes = a_span + 2 * b_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(base + n_stages * stage_bytes);
@@ -392,11 +508,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // the root accumulates into the accumulator on every slice but the first
   const int accumulate = p.root ? static_cast<int>(__ldg(p.cur + 1)) : 0;
   const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
-  const uint32_t tiles_m = (p.M + kBM - 1) / kBM;
+  const uint32_t tiles_m = (p.M + kTM - 1) / kTM;
   const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
   const int k_stages = p.Kr / BK;
   // wide mode (bn <= 128): each accumulator holds [hi-B half | lo-B half]
-  const bool wide = p.bn <= 128;
+  const bool wide = !PAIR && p.bn <= 128;
   const uint32_t acc_cols = wide ? 2 * p.bn : p.bn;
   uint32_t buf_cols = 32;
   while (buf_cols < acc_cols) buf_cols <<= 1;
@@ -418,23 +534,33 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
+      mbar_init(&conv[s], PAIR ? 2 : 32 * p.n_conv);  // PAIR: one arrive per CTA
       mbar_init(&empty[s], 1);
     }
     for (uint32_t b = 0; b < n_acc; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 128);
+      mbar_init(&acc_empty[b], PAIR ? 8 : 128);  // PAIR: one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_slot)),
-                 "r"(tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive
+  else
+    __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -467,14 +593,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
-      uint64_t g = 0;
+      Ring rg;
       uint32_t cached_item = ~0u, a_entry = 0;
       uint64_t pit = 0;
       TileWalk w;
-      w.init(blockIdx.x, gridDim.x, tiles_n, tiles_m);
-      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++pit, w.advance()) {
+      w.init(cta0, ncta, tiles_n, tiles_m);
+      for (uint64_t t = cta0; t < tiles; t += ncta, ++pit, w.advance()) {
         const uint32_t item = w.u;
-        const int m0 = static_cast<int>(w.m) * kBM, n0 = static_cast<int>(w.n) * p.bn;
+        const int m0 = static_cast<int>(w.m) * kTM + m_off;
+        const int n0 = static_cast<int>(w.n) * p.bn + static_cast<int>(rank) * bn_cta;
         trace(p, pit, 0);
         if (item != cached_item) {  // units change every tiles_m * tiles_n tiles
           cached_item = item;
@@ -483,10 +610,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         const int a_row0 = static_cast<int>(a_entry * static_cast<uint64_t>(p.M)) + m0;
         const int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
-        for (int s = 0; s < k_stages; ++s, ++g) {
-          const int st = static_cast<int>(g % n_stages);
-          if (g >= static_cast<uint64_t>(n_stages))
-            mbar_wait(&empty[st], static_cast<uint32_t>((g / n_stages) - 1) & 1);
+        for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
+          const int st = rg.slot;
+          if (rg.round > 0) {
+            if constexpr (PAIR)
+              mbar_wait_cluster(&empty[st], (rg.round - 1) & 1);
+            else
+              mbar_wait(&empty[st], (rg.round - 1) & 1);
+          }
           uint8_t* sp = base + st * stage_bytes;
           mbar_expect_tx(&full[st], a_bytes + 2 * b_bytes);
           tma_load_2d(sp, &map_a, &full[st], s * BK, a_row0);
@@ -502,22 +633,36 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // memory operand-read floor of a 128 x N x 8 tf32 MMA; tools/mma_bench.cu)
     // c_format F32; a/b format TF32 (2) or F16 (0); K-major; N >> 3; M >> 4
     constexpr uint32_t fmt = F16 ? 0u : (2u << 7) | (2u << 10);
-    const uint32_t idesc = (1u << 4) | fmt | (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kBM >> 4) << 24);
+    const uint32_t idesc = (1u << 4) | fmt | (static_cast<uint32_t>(p.bn >> 3) << 17) | ((kTM >> 4) << 24);
     const uint32_t idesc2 =
         (1u << 4) | fmt | (static_cast<uint32_t>((2 * p.bn) >> 3) << 17) | ((kBM >> 4) << 24);
-    uint64_t g = 0, it = 0;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-      const uint32_t tb = static_cast<uint32_t>(it % n_acc);
-      if (it >= n_acc) mbar_wait(&acc_empty[tb], static_cast<uint32_t>((it / n_acc) - 1) & 1);
+    Ring rg, ra;
+    uint64_t it = 0;
+    // (PAIR: the peer CTA's MMA warp has nothing to issue)
+    for (uint64_t t = cta0; t < tiles && (!PAIR || rank == 0); t += ncta, ++it,
+                  ra.next(static_cast<int>(n_acc))) {
+      const uint32_t tb = static_cast<uint32_t>(ra.slot);
+      if (ra.round > 0) {
+        if constexpr (PAIR)
+          mbar_wait_cluster(&acc_empty[tb], (ra.round - 1) & 1);
+        else
+          mbar_wait(&acc_empty[tb], (ra.round - 1) & 1);
+      }
       if (lane == 0) trace(p, it, 2);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t dacc = tmem + tb * buf_cols;
-      for (int s = 0; s < k_stages; ++s, ++g) {
-        const int st = static_cast<int>(g % n_stages);
-        mbar_wait(&conv[st], static_cast<uint32_t>(g / n_stages) & 1);
+      for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
+        const int st = rg.slot;
+        if constexpr (PAIR)
+          mbar_wait_cluster(&conv[st], rg.round & 1);
+        else
+          mbar_wait(&conv[st], rg.round & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sp = smem_u32(base + st * stage_bytes);
-        if constexpr (F16) {
+        if constexpr (PAIR) {
+          mma_stage_f16_pair(dacc, sw_desc<16>(sp), sw_desc<16>(sp + a_bytes / 2), sw_desc<16>(sp + a_bytes),
+                             sw_desc<16>(sp + a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
+        } else if constexpr (F16) {
           if (wide)
             mma_stage_f16_wide(dacc, sw_desc<16>(sp), sw_desc<16>(sp + a_bytes / 2),
                                sw_desc<16>(sp + a_bytes), idesc2, idesc, s > 0 ? 1u : 0u);
@@ -533,19 +678,28 @@ __global__ void __launch_bounds__(kPThreads, 1)
         else
           mma_stage2(dacc, sw_desc<BK>(sp), sw_desc<BK>(sp + a_bytes), sw_desc<BK>(sp + 2 * a_bytes),
                      sw_desc<BK>(sp + 2 * a_bytes + b_bytes), idesc, s > 0 ? 1u : 0u);
-        mma_commit_elect(&empty[st]);
+        if constexpr (PAIR)
+          mma_commit_pair_elect(&empty[st]);
+        else
+          mma_commit_elect(&empty[st]);
       }
-      mma_commit_elect(&acc_full[tb]);
+      if constexpr (PAIR)
+        mma_commit_pair_elect(&acc_full[tb]);
+      else
+        mma_commit_elect(&acc_full[tb]);
       if (lane == 0) trace(p, it, 3);
     }
-  } else if (warp < 6) {  // ---- converters ----
-    const int ct = threadIdx.x - 64;
-    uint64_t g = 0, cit = 0;
+  } else if (warp < 2 + p.n_conv) {  // ---- converters ----
+    const int ct = threadIdx.x - 64, nct = 32 * p.n_conv;
+    const int per = nct == 256 ? 2 : 4;  // F16: (row, column group) pairs per thread
+    Ring rg;
+    uint64_t cit = 0;
     const float sa = F16 ? pow2f(f16_scale_exp(tmem_slot[1])) : 1.f;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++cit) {
-      for (int s = 0; s < k_stages; ++s, ++g) {
-        const int st = static_cast<int>(g % n_stages);
-        mbar_wait(&full[st], static_cast<uint32_t>(g / n_stages) & 1);
+    const uint32_t conv_leader = PAIR ? mapa(conv, 0) : 0u;  // the leader's conv[0]
+    for (uint64_t t = cta0; t < tiles; t += ncta, ++cit) {
+      for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
+        const int st = rg.slot;
+        mbar_wait(&full[st], rg.round & 1);
         if (ct == 0 && s == 0) trace(p, cit, 4);
         if constexpr (F16) {
           // Raw stage: 128 rows x 128 B (SWIZZLE_128B: 16-byte chunk c of row r
@@ -557,15 +711,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
           float4 v[4][2];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int q = ct + 128 * i, r = q >> 2, j = q & 3;
+            if (i >= per) break;
+            const int q = ct + nct * i, r = q >> 2, j = q & 3;
             const float4* row = reinterpret_cast<const float4*>(sp + r * 128);
             v[i][0] = row[(2 * j) ^ (r & 7)];
             v[i][1] = row[(2 * j + 1) ^ (r & 7)];
           }
-          asm volatile("bar.sync 3, 128;" ::: "memory");
+          asm volatile("bar.sync 3, %0;" ::"r"(nct) : "memory");
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int q = ct + 128 * i, r = q >> 2, j = q & 3;
+            if (i >= per) break;
+            const int q = ct + nct * i, r = q >> 2, j = q & 3;
             const float x[8] = {v[i][0].x * sa, v[i][0].y * sa, v[i][0].z * sa, v[i][0].w * sa,
                                 v[i][1].x * sa, v[i][1].y * sa, v[i][1].z * sa, v[i][1].w * sa};
             uint32_t h[4], l[4];
@@ -582,14 +738,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
             *reinterpret_cast<uint4*>(sp + a_bytes / 2 + off) = make_uint4(l[0], l[1], l[2], l[3]);
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&conv[st]);
+          if constexpr (PAIR) {
+            // one cluster-scope release per CTA (after all converters' writes)
+            asm volatile("bar.sync 3, %0;" ::"r"(nct) : "memory");
+            if (ct == 0) mbar_arrive_cluster(conv_leader + 8u * static_cast<uint32_t>(st));
+          } else {
+            mbar_arrive(&conv[st]);
+          }
           continue;
         }
         float4* hi = reinterpret_cast<float4*>(base + st * stage_bytes);
         float4* lo = reinterpret_cast<float4*>(base + st * stage_bytes + a_bytes);
-#pragma unroll
-        for (int i = 0; i < (kBM * BK * 4) / 16 / 128; ++i) {
-          const int e = ct + i * 128;
+#pragma unroll 4
+        for (int e = ct; e < (kBM * BK * 4) / 16; e += nct) {
           const float4 v = hi[e];
           const float4 h = make_float4(tf32_rna_alu(v.x), tf32_rna_alu(v.y), tf32_rna_alu(v.z),
                                        tf32_rna_alu(v.w));
@@ -600,8 +761,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_arrive(&conv[st]);
       }
     }
-  } else {  // ---- epilogue: kEpiGroups warpgroups take alternate tiles ----
-    const int eg = (warp - 6) / 4;  // epilogue group
+  } else {  // ---- epilogue: n_epi warpgroups take alternate tiles ----
+    const int e0 = 2 + p.n_conv;    // first epilogue warp
+    const int n_epi = (12 - p.n_conv) / 4;
+    const int eg = (warp - e0) / 4;  // epilogue group
     // 3xFP16: undo the operand scales (exact powers of two)
     const float osa = F16 ? pow2f(-f16_scale_exp(tmem_slot[1])) : 1.f;
     const float osb = F16 ? pow2f(-f16_scale_exp(tmem_slot[2])) : 1.f;
@@ -628,7 +791,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     };
     // the group's first tile; the next tile's row offset (and column offsets
     // when its key changes) is fetched while the current one drains
-    uint64_t t = blockIdx.x + uint64_t{static_cast<uint32_t>(eg)} * gridDim.x;
+    uint64_t t = cta0 + uint64_t{static_cast<uint32_t>(eg)} * ncta;
     uint64_t it = eg;
     uint32_t nxt_unit = 0;
     int m0 = 0, nxt_m0 = 0, nxt_n0 = 0;
@@ -636,10 +799,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t key = ~uint64_t{0}, nxt_key = ~uint64_t{0}, table_key = ~uint64_t{0};
     int64_t my_coff = -1, nxt_coff = -1;
     TileWalk w;  // walks the group's tiles one fetch ahead
-    w.init(t, kEpiGroups * uint64_t{gridDim.x}, tiles_n, tiles_m);
+    w.init(t, n_epi * uint64_t{ncta}, tiles_n, tiles_m);
     auto fetch = [&]() {
       nxt_unit = w.u;
-      nxt_m0 = static_cast<int>(w.m) * kBM;
+      nxt_m0 = static_cast<int>(w.m) * kTM + m_off;
       nxt_n0 = static_cast<int>(w.n) * p.bn;
       w.advance();
       nxt_om = nxt_m0 + r < p.M ? p.tom(nxt_m0 + r) : 0u;
@@ -650,12 +813,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
     };
     if (t < tiles) fetch();
-    for (; t < tiles; t += kEpiGroups * uint64_t{gridDim.x}, it += kEpiGroups) {
+    const uint32_t acc_empty_leader = PAIR ? mapa(acc_empty, 0) : 0u;
+    for (; t < tiles; t += n_epi * uint64_t{ncta}, it += n_epi) {
       m0 = nxt_m0;
       om = nxt_om;
       key = nxt_key;
       my_coff = nxt_coff;
-      if (t + kEpiGroups * uint64_t{gridDim.x} < tiles) fetch();
+      if (t + n_epi * uint64_t{ncta} < tiles) fetch();
       if (key != table_key) {  // uniform across the group
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));  // readers of the old table done
         if (r < kMaxBn / 2) coff[r] = my_coff;
@@ -663,8 +827,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
         table_key = key;
       }
       const uint32_t tb = static_cast<uint32_t>(it % n_acc);
-      mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
-      if (warp == 6 && lane == 0) trace(p, it, 5);
+      if constexpr (PAIR)
+        mbar_wait_cluster(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
+      else
+        mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
+      if (warp == e0 && lane == 0) trace(p, it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + r;
       const uint32_t tacc = tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16);
@@ -687,7 +854,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           // Output rows are not adjacent in memory: transpose the warp's
           // 32 rows x 16 complex chunk through shared memory so that
           // consecutive lanes write consecutive columns of a row.
-          float* buf = stage_out + (warp - 6) * 32 * 33;
+          float* buf = stage_out + (warp - e0) * 32 * 33;
 #pragma unroll
           for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
           __syncwarp();
@@ -759,15 +926,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&acc_empty[tb]);
-      if (warp == 6 && lane == 0) trace(p, it, 6);
+      if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * tb);
+      } else {
+        mbar_arrive(&acc_empty[tb]);
+      }
+      if (warp == e0 && lane == 0) trace(p, it, 6);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(tmem_cols));
+  if constexpr (PAIR) {
+    cluster_sync_all();  // no remote arrive / MMA into this CTA is still in flight
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+  } else {
+    __syncthreads();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
   }
 }
 
@@ -1016,8 +1192,13 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
                     8 * kEpiGroups * (kMaxBn / 2) +
                     (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
   constexpr int kSmemMax = 227 * 1024;
+  // CTA pairs for 3xFP16 ops with full-width (256-column) tiles and at least
+  // one 256-row tile (MTCG_TC_PAIR=0 disables)
+  static const bool pair_env = !(std::getenv("MTCG_TC_PAIR") && std::atoi(std::getenv("MTCG_TC_PAIR")) == 0);
+  const bool pair = f16 && pair_env && bn == 256 && M >= 256 && n_sms >= 2;
+  const int bn_cta = pair ? bn / 2 : bn;
   auto stage_of = [&](int bk) {
-    return f16 ? kBM * bk * 4 + 2 * bn * bk * 2 : 2 * kBM * bk * 4 + 2 * bn * bk * 4;
+    return f16 ? kBM * bk * 4 + 2 * bn_cta * bk * 2 : 2 * kBM * bk * 4 + 2 * bn * bk * 4;
   };
   // TF32: 32-float stages unless only 2 of them fit (MTCG_TC_BK overrides);
   // 3xFP16: 32 raw floats (in-place split: 16 KB A + 2 x bn x 64 B B̂)
@@ -1029,8 +1210,8 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
   const size_t smem = extra + static_cast<size_t>(n_stages) * stage_bytes;
   const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM, bk);
-  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn, bk, f16);
-  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn, bk, f16);
+  const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn_cta, bk, f16);
+  const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn_cta, bk, f16);
   TcParams p;
   p.M = static_cast<int>(M);
   p.Nr = static_cast<int>(Nr);
@@ -1053,16 +1234,25 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   p.m_contig = op.m_contig;
   p.transpose = transpose ? 1 : 0;
   p.partials = op.partials;
-  static size_t smem_set[3] = {0, 0, 0};
-  const int kv = f16 ? 2 : bk == 32 ? 1 : 0;
-  auto kern = f16 ? tc_gemm_persistent<32, true>
-                  : bk == 32 ? tc_gemm_persistent<32, false> : tc_gemm_persistent<16, false>;
+  // 8 converter warps + 1 epilogue group once the main loop per tile (>= 32
+  // stages) outlasts a tile's epilogue (MTCG_TC_CONV=4|8 overrides)
+  static const int conv_env = std::getenv("MTCG_TC_CONV") ? std::atoi(std::getenv("MTCG_TC_CONV")) : 0;
+  p.n_conv = conv_env == 4 || conv_env == 8 ? conv_env : (Kr / bk >= 32 ? 8 : 4);
+  static size_t smem_set[4] = {0, 0, 0, 0};
+  const int kv = pair ? 3 : f16 ? 2 : bk == 32 ? 1 : 0;
+  auto kern = pair  ? tc_gemm_persistent<32, true, true>
+              : f16 ? tc_gemm_persistent<32, true>
+              : bk == 32 ? tc_gemm_persistent<32, false> : tc_gemm_persistent<16, false>;
   if (smem > smem_set[kv]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (pair) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     smem_set[kv] = smem;
   }
-  const uint64_t tiles = ((M + kBM - 1) / kBM) * ((Nr + bn - 1) / bn) * units;
-  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));
+  const uint64_t tile_m = pair ? 2 * kBM : kBM;
+  const uint64_t tiles = ((M + tile_m - 1) / tile_m) * ((Nr + bn - 1) / bn) * units;
+  // pairs: two CTAs per tile, an even grid of whole clusters
+  const unsigned grid = pair ? static_cast<unsigned>(std::min<uint64_t>(2 * tiles, n_sms & ~1))
+                             : static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));
   p.dbg = nullptr;
   const char* tr = std::getenv("MTCG_TC_TRACE");
   const bool tracing = tr && std::atoi(tr) == op.node;
@@ -1070,15 +1260,31 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
     cudaMalloc(&p.dbg, sizeof(unsigned long long) * kTraceTiles * 8);
     cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * kTraceTiles * 8, st);
   }
-  kern<<<grid, kPThreads, smem, st>>>(ma, mbhi, mblo, p, n_stages);
+  if (pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kPThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, ma, mbhi, mblo, p, n_stages);
+  } else {
+    kern<<<grid, kPThreads, smem, st>>>(ma, mbhi, mblo, p, n_stages);
+  }
   if (tracing) {
     std::vector<unsigned long long> h(kTraceTiles * 8);
     cudaMemcpyAsync(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     cudaFree(p.dbg);
     const unsigned long long t0 = h[0];
-    std::fprintf(stderr, "[tc trace node %d] f16=%d bk=%d stages=%d bn=%d tiles=%llu grid=%u n_acc<=%d\n",
-                 op.node, f16 ? 1 : 0, bk, n_stages, bn, static_cast<unsigned long long>(tiles), grid, kMaxAcc);
+    std::fprintf(stderr, "[tc trace node %d] pair=%d conv=%d f16=%d bk=%d stages=%d bn=%d tiles=%llu grid=%u n_acc<=%d\n",
+                 op.node, pair ? 1 : 0, p.n_conv, f16 ? 1 : 0, bk, n_stages, bn, static_cast<unsigned long long>(tiles), grid, kMaxAcc);
     std::fprintf(stderr, " tile  prod0  prod1  conv(full) mma0  mma1  epi0  epi1   (cycles from tile0 prod0)\n");
     for (int i = 0; i < kTraceTiles; ++i) {
       if (!h[i * 8]) break;
