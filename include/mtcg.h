@@ -123,6 +123,12 @@ typedef struct mtcg_options {
 
 /* mtcg_options.flags */
 #define MTCG_FLAG_NO_TENSOR_CORES 1 /* dense ops on the CUDA-core kernels */
+#define MTCG_FLAG_SLICE_REUSE 2     /* evaluate slice-invariant subtrees (no
+                                       sliced leg among their leaves) once per
+                                       run instead of once per slice; values
+                                       are unchanged, counters stay the
+                                       reference's (per-slice) counts. Ignored
+                                       under a memory cap. */
 
 /* eval outputs. `values` is a caller buffer of values_capacity complex
  * elements receiving, request-major, each request's tensor (order-0, or
@@ -156,6 +162,10 @@ typedef struct mtcg_plan_info {
   uint64_t hbm_resident_bytes;  /* leaves + index arrays kept on device */
   int32_t precision;
   int32_t n_kernels_per_slice;  /* device launches per slice */
+  uint64_t prologue_ops;        /* MTCG_FLAG_SLICE_REUSE: slice-invariant ops
+                                   run once per run range (0 without) */
+  uint64_t executed_contractions; /* contractions one run over all slices
+                                     executes (= contractions without reuse) */
 } mtcg_plan_info;
 
 int mtcg_version(void);

@@ -94,6 +94,8 @@ class mtcg_plan_info(C.Structure):
         ("hbm_resident_bytes", C.c_uint64),
         ("precision", C.c_int32),
         ("n_kernels_per_slice", C.c_int32),
+        ("prologue_ops", C.c_uint64),
+        ("executed_contractions", C.c_uint64),
     ]
 
 

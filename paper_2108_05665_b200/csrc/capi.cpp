@@ -73,6 +73,14 @@ void check_problem_pointers(const mtcg_problem* p) {
     throw DataError("null array in problem");
 }
 
+// Slice reuse keeps invariant tables resident across slices, outside the
+// reference's per-slice accounting: it is dropped under an explicit cap
+// (options or handle), where MemoryCapError must follow the reference.
+mtcg_options effective_options(const mtcg_handle* h, mtcg_options o) {
+  if (o.memory_cap_bytes || h->cap) o.flags &= ~MTCG_FLAG_SLICE_REUSE;
+  return o;
+}
+
 uint64_t device_cap(const mtcg_handle* h, const mtcg_options& o) {
   if (o.memory_cap_bytes) return o.memory_cap_bytes;
   if (h->cap) return h->cap;
@@ -95,6 +103,8 @@ void fill_info(const Compiled& c, mtcg_plan_info* info) {
   info->hbm_arena_bytes = c.arena_bytes();
   info->hbm_resident_bytes = c.resident_bytes();
   info->precision = c.precision;
+  info->prologue_ops = c.n_prologue_ops;
+  info->executed_contractions = c.executed_contractions;
   int k = 0;
   for (const Op& op : c.ops)
     if (op.nb) ++k;
@@ -178,7 +188,7 @@ mtcg_status mtcg_compile(mtcg_handle* h, const mtcg_problem* p, const mtcg_optio
   return guarded(err, errlen, cap_node, [&] {
     if (!h || !out) throw DataError("null handle");
     check_problem_pointers(p);
-    const mtcg_options o = opt ? *opt : default_options();
+    const mtcg_options o = effective_options(h, opt ? *opt : default_options());
     Compiled c = compile_problem(*p, o, device_cap(h, o));
     auto plan = std::make_unique<mtcg_plan>();
     plan->dp = upload_plan(h->engine, std::move(c));
@@ -231,7 +241,7 @@ mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p, const mtcg_options*
   mtcg_status st = guarded(err, errlen, &cap_node, [&] {
     if (!h || !res) throw DataError("null argument");
     check_problem_pointers(p);
-    const mtcg_options o = opt ? *opt : default_options();
+    const mtcg_options o = effective_options(h, opt ? *opt : default_options());
     Compiled c = compile_problem(*p, o, device_cap(h, o));
     mtcg_plan plan;
     plan.dp = upload_plan(h->engine, std::move(c));

@@ -911,16 +911,18 @@ struct DagIssue {
 // Launches one slice's ops; the slice index and the root's accumulate flag
 // are read by the kernels from dp.d_cur (set by set_slice_kernel), so this
 // launch sequence is the same for every slice and is captured once.
+// Ops [op0, op1) only (default: all): the slice-reuse prologue and the
+// per-slice ops are launched (and captured) separately.
 template <class R>
 void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEvent_t* op_events = nullptr,
-                      DagIssue* dag = nullptr) {
+                      DagIssue* dag = nullptr, size_t op0 = 0, size_t op1 = ~size_t{0}) {
   using T = typename V2<R>::T;
   Compiled& c = dp.c;
   T* arena = static_cast<T*>(dp.d_arena);
   const T* leaves = static_cast<const T*>(dp.d_leaves);
   T* acc = static_cast<T*>(d_acc);
   auto sstr = [&](int64_t off) -> const uint64_t* { return off < 0 ? nullptr : dp.d_sstr + off; };
-  for (size_t oi = 0; oi < c.ops.size(); ++oi) {
+  for (size_t oi = op0; oi < std::min(op1, c.ops.size()); ++oi) {
     const Op& op = c.ops[oi];
     if (op.nb == 0) continue;
     const cudaStream_t st = dag ? dag->begin(oi) : st_main;
@@ -1031,11 +1033,11 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
 }
 
 void launch_slice(DevicePlan& dp, void* d_acc, cudaStream_t st, cudaEvent_t* op_events = nullptr,
-                  DagIssue* dag = nullptr) {
+                  DagIssue* dag = nullptr, size_t op0 = 0, size_t op1 = ~size_t{0}) {
   if (dp.c.precision == MTCG_C64)
-    launch_slice_ops<float>(dp, d_acc, st, op_events, dag);
+    launch_slice_ops<float>(dp, d_acc, st, op_events, dag, op0, op1);
   else
-    launch_slice_ops<double>(dp, d_acc, st, op_events, dag);
+    launch_slice_ops<double>(dp, d_acc, st, op_events, dag, op0, op1);
 }
 
 // Streams and events for concurrent capture (created once per plan).
@@ -1101,8 +1103,10 @@ void* engine_stream(Engine* e) { return e->stream; }
 
 DevicePlan::~DevicePlan() {
   if (engine) cudaSetDevice(engine->device);
-  for (auto& [k, g] : graphs)
+  for (auto& [k, g] : graphs) {
     if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
+    if (g.exec_pro) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec_pro));
+  }
   for (void* e : op_events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : join_events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* s : aux_streams) cudaStreamDestroy(static_cast<cudaStream_t>(s));
@@ -1135,6 +1139,8 @@ void* engine_pinned(Engine* e, uint64_t bytes) {
   }
   return e->pinned;
 }
+
+void ensure_arena(DevicePlan& dp);
 
 std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
   CK(cudaSetDevice(e->device));
@@ -1203,21 +1209,35 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c) {
   dp->d_sstr = reinterpret_cast<uint64_t*>(d + o_sstr);
   dp->d_cur = reinterpret_cast<uint32_t*>(d + o_cur);
   dp->d_xeb_part = reinterpret_cast<double*>(d + o_xeb);
-  if (cc.arena_elems) {
-    const uint64_t need = cc.arena_elems * eb;
-    if (e->arena_bytes < need) {
-      if (e->arena) {
-        CK(cudaStreamSynchronize(e->stream));
-        CK(cudaFree(e->arena));
-        e->arena = nullptr;
-        e->arena_bytes = 0;
-      }
-      CK(cudaMalloc(&e->arena, need));
-      e->arena_bytes = need;
-    }
-    dp->d_arena = e->arena;
-  }
+  ensure_arena(*dp);
   return dp;
+}
+
+// The intermediate arena is the handle's, shared by its plans and grown to
+// the largest one on demand: a plan resolves it before every run (a later,
+// larger plan may have moved it) and drops graphs captured on the old one.
+void ensure_arena(DevicePlan& dp) {
+  Engine* e = dp.engine;
+  const uint64_t need = dp.c.arena_elems * static_cast<uint64_t>(dp.c.elem_bytes);
+  if (!need) return;
+  if (e->arena_bytes < need) {
+    if (e->arena) {
+      CK(cudaDeviceSynchronize());  // no plan's work may still use it
+      CK(cudaFree(e->arena));
+      e->arena = nullptr;
+      e->arena_bytes = 0;
+    }
+    CK(cudaMalloc(&e->arena, need));
+    e->arena_bytes = need;
+  }
+  if (dp.d_arena != e->arena) {
+    dp.d_arena = e->arena;
+    for (auto& [k, g] : dp.graphs) {
+      if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
+      if (g.exec_pro) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec_pro));
+    }
+    dp.graphs.clear();
+  }
 }
 
 void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
@@ -1225,38 +1245,56 @@ void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accu
   CK(cudaSetDevice(dp.engine->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
   if (s0 >= s1) return;
+  ensure_arena(dp);
   // One slice's launches are captured as a CUDA graph on first use (per
   // accumulator) and replayed for every slice after a set-slice kernel: the
   // host issues 2 launches per slice. MTCG_NO_GRAPHS=1 launches directly.
+  // With slice reuse the invariant ops (ops [0, n_pro)) form a second graph
+  // run once per call, before the first slice: the arena is shared by the
+  // handle's plans, so their resident tables are rebuilt on every run.
   const bool graphs = !std::getenv("MTCG_NO_GRAPHS");
+  const size_t n_pro = dp.c.n_prologue_ops;
   DevicePlan::GraphEntry* ge = nullptr;
+  auto capture = [&](size_t op0, size_t op1, void*& exec_out, uint64_t& kernels_out) {
+    const uint64_t before = dp.engine->launches;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      DagIssue dag(dp, st);
+      launch_slice(dp, d_acc, st, nullptr, &dag, op0, op1);
+    } catch (...) {
+      cudaStreamEndCapture(st, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &graph));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ierr = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CK(ierr);
+    exec_out = exec;
+    kernels_out = dp.engine->launches - before;
+    dp.engine->launches = before;  // counted when replayed
+  };
   if (graphs) {
     auto it = dp.graphs.find(d_acc);
     if (it == dp.graphs.end()) {
-      const uint64_t before = dp.engine->launches;
-      cudaGraph_t graph = nullptr;
       ensure_dag_resources(dp);
-      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      try {
-        DagIssue dag(dp, st);
-        launch_slice(dp, d_acc, st, nullptr, &dag);
-      } catch (...) {
-        cudaStreamEndCapture(st, &graph);
-        if (graph) cudaGraphDestroy(graph);
-        throw;
-      }
-      CK(cudaStreamEndCapture(st, &graph));
-      cudaGraphExec_t exec = nullptr;
-      const cudaError_t ierr = cudaGraphInstantiate(&exec, graph, 0);
-      cudaGraphDestroy(graph);
-      CK(ierr);
       DevicePlan::GraphEntry e;
-      e.exec = exec;
-      e.kernels = dp.engine->launches - before;
-      dp.engine->launches = before;  // counted when replayed
+      capture(n_pro, ~size_t{0}, e.exec, e.kernels);
+      if (n_pro) capture(0, n_pro, e.exec_pro, e.kernels_pro);
       it = dp.graphs.emplace(d_acc, e).first;
     }
     ge = &it->second;
+  }
+  if (n_pro) {
+    set_slice(dp, s0, accumulate, st);
+    if (ge) {
+      CK(cudaGraphLaunch(static_cast<cudaGraphExec_t>(ge->exec_pro), st));
+      dp.engine->launches += ge->kernels_pro;
+    } else {
+      launch_slice(dp, d_acc, st, nullptr, nullptr, 0, n_pro);
+    }
   }
   for (uint64_t s = s0; s < s1; ++s) {
     set_slice(dp, s, accumulate || s > s0, st);
@@ -1264,7 +1302,7 @@ void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accu
       CK(cudaGraphLaunch(static_cast<cudaGraphExec_t>(ge->exec), st));
       dp.engine->launches += ge->kernels;
     } else {
-      launch_slice(dp, d_acc, st);
+      launch_slice(dp, d_acc, st, nullptr, nullptr, n_pro);
     }
   }
 }
@@ -1273,6 +1311,7 @@ void time_ops(DevicePlan& dp, uint64_t slice, void* d_acc, bool accumulate, void
               float* op_ms) {
   CK(cudaSetDevice(dp.engine->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
+  ensure_arena(dp);
   const size_t n = dp.c.ops.size();
   std::vector<cudaEvent_t> ev(2 * n);
   for (auto& e : ev) CK(cudaEventCreate(&e));

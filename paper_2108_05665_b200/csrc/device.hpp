@@ -41,6 +41,8 @@ struct DevicePlan {
   struct GraphEntry {
     void* exec = nullptr;   // cudaGraphExec_t
     uint64_t kernels = 0;   // device launches replayed per graph launch
+    void* exec_pro = nullptr;  // slice-reuse prologue (invariant ops), once per run
+    uint64_t kernels_pro = 0;
   };
   std::map<void*, GraphEntry> graphs;
   // Concurrent capture: independent ops (disjoint subtrees) are issued on

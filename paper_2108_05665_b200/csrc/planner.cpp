@@ -496,6 +496,29 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     }
   }
 
+  // --- cross-slice reuse (MTCG_FLAG_SLICE_REUSE) ----------------------------------
+  // A node is slice-invariant when no leaf of its subtree carries a sliced
+  // leg: its tables are the same in every slice (the reference recomputes
+  // them per slice, multieval.cpp:465-476). Invariant nodes are scheduled
+  // first (a prologue run once per run range) and the invariant tables read
+  // by slice-dependent parents are never released. The C ABI drops the flag
+  // under an explicit memory cap (the reference's per-slice accounting is the
+  // budget there).
+  std::vector<char> invariant(n, 0);
+  if ((opt.flags & MTCG_FLAG_SLICE_REUSE) && S > 0) {
+    for (int node : ix.postorder) {
+      if (p.node_slot[node] >= 0) {
+        bool any = false;
+        for (uint32_t x : slot_layout[p.node_slot[node]]) any |= contains(c.sliced, x);
+        invariant[node] = !any;
+      } else {
+        invariant[node] = invariant[p.node_left[node]] && invariant[p.node_right[node]];
+      }
+    }
+    std::stable_partition(sched.begin(), sched.end(), [&](int node) { return invariant[node] != 0; });
+    for (int node : sched) c.n_prologue_ops += invariant[node] ? 1 : 0;
+  }
+
   // --- static arena: first-fit over the schedule ---------------------------
   const uint64_t align = 256 / c.elem_bytes;
   std::map<uint64_t, uint64_t> free_blocks;  // offset -> length
@@ -796,6 +819,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     c.adds += op.adds * op.nb * c.n_slices;
     c.rw += op.rw * op.nb * c.n_slices;
     c.contractions += static_cast<uint64_t>(op.nb) * c.n_slices;
+    c.executed_contractions += static_cast<uint64_t>(op.nb) * (invariant[node] ? 1 : c.n_slices);
 
     sec.lap(3);
     // output storage
@@ -831,8 +855,10 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       }
     }
     // children are dead once consumed
+    // (invariant tables read by a slice-dependent parent live across slices)
     for (int ch : {l, r})
-      if (p.node_slot[ch] < 0 && ti.distinct[ch] > 0 && !node_private[ch])
+      if (p.node_slot[ch] < 0 && ti.distinct[ch] > 0 && !node_private[ch] &&
+          !(invariant[ch] && !invariant[node]))
         release(arena_off[ch], table_elems[ch]);
     c.ops.push_back(std::move(op));
     sec.lap(4);

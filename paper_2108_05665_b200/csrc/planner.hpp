@@ -124,6 +124,11 @@ struct Compiled {
   int n_slice_slots = 0;               // ops/leaf root needing slice offsets
 
   uint64_t private_elems = 0;          // of arena_elems: never-reused small tables
+  // MTCG_FLAG_SLICE_REUSE: ops[0, n_prologue_ops) are the slice-invariant
+  // nodes, run once per run range; their tables feeding slice-dependent
+  // parents stay resident in the arena across slices
+  size_t n_prologue_ops = 0;
+  uint64_t executed_contractions = 0;  // per run range of S slices: see slice_contractions()
   uint64_t arena_bytes() const { return arena_elems * elem_bytes; }
   uint64_t resident_bytes() const {
     return leaf_elems * elem_bytes + 4 * (table_blob.size() + index_blob.size());

@@ -100,3 +100,60 @@ def test_device_slice_offsets_every_slice(engine, seed):
     torch.cuda.synchronize()
     ov, _, _, _ = O.eval_problem(p)
     assert bits_equal(cp.fetch(acc.data_ptr()).amplitudes, ov)
+
+
+@pytest.mark.parametrize("name,precision", [("cfg2", "c64"), ("cfg2", "c128")])
+def test_slice_reuse_bit_identical(engine, name, precision):
+    """Cross-slice reuse (MTCG_FLAG_SLICE_REUSE): the
+    slice-invariant subtrees evaluated once per run give bit-identical
+    amplitudes (every op is deterministic; only the schedule changes), also
+    for staged slice ranges (the prologue reruns on every run call)."""
+    p, c, bits = workload(name)
+    base = run(engine, p, EvalOptions(precision=precision))
+    reuse = run(engine, p, EvalOptions(precision=precision, slice_reuse=True))
+    assert bits_equal(base, reuse)
+    cp = engine.compile(p, A.MTCG_EVAL_AUTO, EvalOptions(precision=precision, slice_reuse=True))
+    assert cp.info.prologue_ops > 0
+    assert cp.info.executed_contractions < cp.info.contractions
+    capped = engine.compile(p, A.MTCG_EVAL_AUTO, EvalOptions(precision=precision, slice_reuse=True,
+                                                               memory_cap_bytes=64 << 30))
+    assert capped.info.prologue_ops == 0  # reference cap accounting: no resident tables
+    del capped
+    acc = cp.new_accumulator()
+    S = cp.n_slices
+    cp.run(0, S // 2, acc.data_ptr())
+    cp.run(S // 2, S, acc.data_ptr(), accumulate=True)
+    staged = cp.fetch(acc.data_ptr()).amplitudes
+    # two partial folds: the same per-slice values, summed (c128 summation
+    # order matches the single fold: slices accumulate in index order)
+    if precision == "c128":
+        assert bits_equal(staged, base)
+    else:
+        assert rel_err(staged, base, c.n_qubits) <= TOL
+
+
+@pytest.mark.parametrize("seed", [0, 3, 6, 9, 12, 15])
+def test_slice_reuse_random_instances(engine, seed):
+    p, c, bits = random_instance(seed)
+    cp = engine.compile(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", slice_reuse=True))
+    acc = cp.new_accumulator()
+    cp.run(0, cp.n_slices, acc.data_ptr())
+    ov, _, _, _ = O.eval_problem(p)
+    assert bits_equal(cp.fetch(acc.data_ptr()).amplitudes, ov)
+
+
+def test_plan_survives_arena_growth(engine):
+    """Plans share the handle's arena; compiling a larger plan moves it. An
+    earlier plan must follow (re-resolve the arena, re-capture its graph)."""
+    p1, c1, _ = workload("cfg1")
+    opts = EvalOptions(precision="c128")
+    cp1 = engine.compile(p1, A.MTCG_EVAL_AUTO, opts)
+    acc1 = cp1.new_accumulator()
+    cp1.run(0, cp1.n_slices, acc1.data_ptr())  # graph captured on the current arena
+    first = cp1.fetch(acc1.data_ptr()).amplitudes
+    p2, _, _ = workload("cfg2")
+    cp2 = engine.compile(p2, A.MTCG_EVAL_AUTO, EvalOptions(precision="c64", slice_reuse=True))
+    acc2 = cp2.new_accumulator()
+    cp2.run(0, 1, acc2.data_ptr())
+    cp1.run(0, cp1.n_slices, acc1.data_ptr())
+    assert bits_equal(cp1.fetch(acc1.data_ptr()).amplitudes, first)
