@@ -202,6 +202,11 @@ def test_cfg2_full_size_against_reference_golden(engine, tensor_cores):
     assert np.linalg.norm(r.amplitudes - want) / np.linalg.norm(want) <= TOL
     f_ref = O.linear_xeb(c.n_qubits, (np.abs(want) ** 2).ravel())
     f_dev = cp.xeb(acc.data_ptr(), c.n_qubits)
+    scale = np.vdot(want, r.amplitudes).real / np.vdot(want, want).real - 1.0
+    print(f"cfg2 full size, tensor_cores={tensor_cores}: max rel "
+          f"{rel_err(r.amplitudes, want, c.n_qubits):.2e}, L2 "
+          f"{np.linalg.norm(r.amplitudes - want) / np.linalg.norm(want):.2e}, scale bias {scale:.2e}, "
+          f"F {f_dev:.6f} vs {f_ref:.6f} (dF {f_dev - f_ref:.2e})")
     if tensor_cores:
         assert abs(f_dev - f_ref) <= 2 * TOL * (1 + abs(f_ref))
     else:
