@@ -8,6 +8,7 @@
 #include <memory>
 
 #include "device.hpp"
+#include "configs.hpp"
 #include "planner.hpp"
 
 using namespace mtcg;
@@ -107,7 +108,7 @@ void fill_info(const Compiled& c, mtcg_plan_info* info) {
   info->executed_contractions = c.executed_contractions;
   int k = 0;
   for (const Op& op : c.ops)
-    if (op.nb) ++k;
+    if (op.nb && (op.chain < 0 || op.chain_tail)) ++k;
   if (c.has_leaf_root && c.n_rows) ++k;
   info->n_kernels_per_slice = k;
 }
@@ -290,7 +291,7 @@ mtcg_status mtcg_plan_op_info(const mtcg_plan* plan, int32_t i, mtcg_op_info* in
   const Compiled& c = plan->dp->c;
   const Op& op = c.ops[i];
   info->node = op.node;
-  info->kernel = op.config;
+  info->kernel = op.chain >= 0 ? kChainConfig : op.config;
   info->fa = op.fa;
   info->fb = op.fb;
   info->kc = op.kc;

@@ -42,6 +42,9 @@ constexpr int kRowsGroupedConfig = 13;
 // the summation order, so complex128's reference order keeps the generic
 // kernel).
 constexpr int kDotConfig = 15;
+// Member of a fused operand chain (planner.hpp Chain; reported by op_info —
+// the chain's last op launches the chain kernel, the others nothing).
+constexpr int kChainConfig = 16;
 // shared-memory budget for one group's B blocks (bytes)
 constexpr int kGroupSmemBytes = 48 * 1024;
 

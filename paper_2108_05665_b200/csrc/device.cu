@@ -565,6 +565,189 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- fused operand chains (planner.hpp Chain) --------------------------------------
+//
+// One block = one final item x nu consecutive untouched-leg combinations u.
+// The head's A block (nu x 2^|Q_in| elements) is loaded into shared memory,
+// every step contracts the active touched legs with its small B in the
+// reference's order (out = sum_c x[in_base(o) + in_c(c)] * b[b_base(o) + b_c(c)],
+// the first product seeding the sum, as contract_pair) into the other
+// buffer, and the tail's block is stored: the intermediate tables of the run
+// never touch HBM.
+template <class T>
+struct ChainDev {
+  const T* a;              // head's A table
+  uint64_t a_item;
+  T* out;                  // tail's output table
+  uint64_t out_item;
+  const uint32_t* entries; // [(steps + 1) x nb]
+  uint32_t nb;
+  int n_steps, q, inner_bits, outer_bits, n_ld, n_st;
+  DTable tu_in, tu_out;    // outer combination -> block base offset
+  // block maps, per index bit: shared-memory position and element offset
+  uint32_t ld_p[12], ld_o[12], st_p[12], st_o[12];
+  int ld_bits, st_bits;
+  const uint32_t* cur;     // slice parameters (B operands that are sliced leaves)
+  int s_bits;
+  struct Step {
+    const T* b;
+    uint64_t b_item;
+    const uint64_t* b_sstr;
+    const uint32_t* tbl;
+    int out_bits, kc, g_bits, f_bits;
+    int tbl_rel;           // word offset of the step's tables from step 0's
+  } steps[kMaxChainSteps];
+  int tbl_words;           // all steps' tables
+  int cpb_bits;            // log2 outer chunks per block
+};
+
+// One step over the block: work item (inner combination uu, kept-leg
+// combination f) loads its K inputs once and writes its G outputs; K, G are
+// compile-time so inputs (and small B tiles) live in registers.
+template <class T, int KC, int GB>
+__device__ __forceinline__ void chain_step(const T* X, T* Y, const T* Bs, const uint32_t* tb, int pitch,
+                                           int inner_bits, int f_bits) {
+  constexpr int K = 1 << KC, G = 1 << GB;
+  constexpr bool b_regs = K * G * sizeof(T) <= 64;  // small B tiles in registers
+  const int F = 1 << f_bits;
+  const uint32_t* in_base = tb;
+  const uint32_t* out_f = tb + F;
+  const uint32_t* out_g = out_f + F;
+  const uint32_t* in_c = out_g + G;
+  uint32_t ic[K], og[G];
+#pragma unroll
+  for (int c = 0; c < K; ++c) ic[c] = in_c[c];
+#pragma unroll
+  for (int g = 0; g < G; ++g) og[g] = out_g[g];
+  T br[b_regs ? K * G : 1];
+  if constexpr (b_regs) {
+#pragma unroll
+    for (int i = 0; i < K * G; ++i) br[i] = Bs[i];
+  }
+  const int n = F << inner_bits;
+  const int umask = (1 << inner_bits) - 1;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const int uu = e & umask, f = e >> inner_bits;
+    const T* x = X + uu * pitch + in_base[f];
+    T xv[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) xv[c] = x[ic[c]];
+    T* y = Y + uu * pitch + out_f[f];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      T acc = czero<T>();
+#pragma unroll
+      for (int c = 0; c < K; ++c) cmac(acc, xv[c], b_regs ? br[c * G + g] : Bs[c * G + g], c == 0);
+      y[og[g]] = acc;
+    }
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void chain_step_any(int kc, int gb, const T* X, T* Y, const T* Bs,
+                                               const uint32_t* tb, int pitch, int inner_bits, int f_bits) {
+#define MTCG_CHAIN_CASE(KC_, GB_) \
+  case KC_ * 4 + GB_:             \
+    chain_step<T, KC_, GB_>(X, Y, Bs, tb, pitch, inner_bits, f_bits); \
+    break;
+  switch (kc * 4 + gb) {
+    MTCG_CHAIN_CASE(0, 0) MTCG_CHAIN_CASE(0, 1) MTCG_CHAIN_CASE(0, 2) MTCG_CHAIN_CASE(0, 3)
+    MTCG_CHAIN_CASE(1, 0) MTCG_CHAIN_CASE(1, 1) MTCG_CHAIN_CASE(1, 2) MTCG_CHAIN_CASE(1, 3)
+    MTCG_CHAIN_CASE(2, 0) MTCG_CHAIN_CASE(2, 1) MTCG_CHAIN_CASE(2, 2) MTCG_CHAIN_CASE(2, 3)
+    MTCG_CHAIN_CASE(3, 0) MTCG_CHAIN_CASE(3, 1) MTCG_CHAIN_CASE(3, 2) MTCG_CHAIN_CASE(3, 3)
+    default: break;
+  }
+#undef MTCG_CHAIN_CASE
+}
+
+// Each block walks `cpb` consecutive outer chunks of one item: the next
+// chunk's elements are loaded into registers while the current one is
+// contracted and stored (the load latency is the kernel's critical path; a
+// block per chunk left most blocks outside their load phase).
+template <class R>
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2)
+    chain_kernel(const __grid_constant__ ChainDev<typename V2<R>::T> d) {
+  using T = typename V2<R>::T;
+  extern __shared__ __align__(16) uint8_t chain_smem[];
+  const int pitch = (1 << d.q) + 1;  // odd row pitch: rows start in different banks
+  const int blk = pitch << d.inner_bits;
+  T* const X0 = reinterpret_cast<T*>(chain_smem);
+  T* const Y0 = X0 + blk;
+  T* Bs = Y0 + blk;                                                    // B tiles, 64 per step
+  uint32_t* tb = reinterpret_cast<uint32_t*>(Bs + 64 * d.n_steps);    // all steps' tables
+  const int chunk_bits = d.outer_bits - d.cpb_bits;
+  const uint32_t item = blockIdx.x >> chunk_bits;
+  const uint64_t outer0 = (blockIdx.x & ((uint64_t{1} << chunk_bits) - 1)) << d.cpb_bits;
+  // every step's tables (contiguous in the index blob) and B tile, once
+  for (int i = threadIdx.x; i < d.tbl_words; i += blockDim.x) tb[i] = __ldg(d.steps[0].tbl + i);
+  const uint32_t slice = d.cur ? __ldg(d.cur) : 0u;
+  for (int l = 0; l < d.n_steps; ++l) {
+    const auto& st = d.steps[l];
+    const int KG = 1 << (st.kc + st.g_bits);
+    if (threadIdx.x < KG) {
+      const uint32_t* boff = st.tbl + (2 << st.f_bits) + (1 << st.g_bits) + (1 << st.kc);
+      const uint64_t b_slice = st.b_sstr ? slice_offset_dev(st.b_sstr, d.s_bits, slice) : 0;
+      const T* B = st.b + uint64_t{__ldg(d.entries + uint64_t{d.nb} * (l + 1) + item)} * st.b_item + b_slice;
+      Bs[64 * l + threadIdx.x] = B[__ldg(boff + threadIdx.x)];
+    }
+  }
+  const T* Aitem = d.a + uint64_t{__ldg(d.entries + item)} * d.a_item;
+  T* Oitem = d.out + uint64_t{item} * d.out_item;
+  constexpr int kU = 8;  // elements per thread per chunk (2^(inner + |Q_in|) <= 2048)
+  // element e = threadIdx.x + 256 u of a map: bits 0-7 from the thread,
+  // bits 8-10 from u
+  uint32_t lp = 0, lo = 0, sp = 0, so = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < d.ld_bits && (threadIdx.x >> i & 1)) {
+      lp += d.ld_p[i];
+      lo += d.ld_o[i];
+    }
+    if (i < d.st_bits && (threadIdx.x >> i & 1)) {
+      sp += d.st_p[i];
+      so += d.st_o[i];
+    }
+  }
+  auto hi = [&](const uint32_t* tab, int bits, int u) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (8 + i < bits && (u >> i & 1)) x += tab[8 + i];
+    return x;
+  };
+  T v[kU];
+  auto fetch = [&](uint64_t outer) {
+    const T* A = Aitem + d.tu_in(outer) + lo;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (threadIdx.x + 256 * u < d.n_ld) v[u] = A[hi(d.ld_o, d.ld_bits, u)];
+  };
+  fetch(outer0);
+  const int n_chunks = 1 << d.cpb_bits;
+  for (int k = 0; k < n_chunks; ++k) {
+    __syncthreads();  // the previous chunk's results are stored
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (threadIdx.x + 256 * u < d.n_ld) X0[lp + hi(d.ld_p, d.ld_bits, u)] = v[u];
+    if (k + 1 < n_chunks) fetch(outer0 + k + 1);  // in flight during the steps
+    T* X = X0;
+    T* Y = Y0;
+    for (int l = 0; l < d.n_steps; ++l) {
+      const auto& st = d.steps[l];
+      __syncthreads();
+      chain_step_any<T>(st.kc, st.g_bits, X, Y, Bs + 64 * l, tb + st.tbl_rel, pitch, d.inner_bits, st.f_bits);
+      T* t = X;
+      X = Y;
+      Y = t;
+    }
+    __syncthreads();
+    T* O = Oitem + d.tu_out(outer0 + k) + so;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (threadIdx.x + 256 * u < d.n_st) O[hi(d.st_o, d.st_bits, u)] = X[sp + hi(d.st_p, d.st_bits, u)];
+  }
+}
+
 // ---- one warp per output element (complex64, long K) ----------------------------
 
 __global__ void __launch_bounds__(256)
@@ -913,6 +1096,74 @@ struct DagIssue {
 // launch sequence is the same for every slice and is captured once.
 // Ops [op0, op1) only (default: all): the slice-reuse prologue and the
 // per-slice ops are launched (and captured) separately.
+// Shared memory of a chain block: 2 buffers x 2^(inner + q) elements.
+template <class R>
+void launch_chain(DevicePlan& dp, const Chain& ch, cudaStream_t st) {
+  using T = typename V2<R>::T;
+  const Compiled& c = dp.c;
+  T* arena = static_cast<T*>(dp.d_arena);
+  const T* leaves = static_cast<const T*>(dp.d_leaves);
+  const Op& head = c.ops[ch.head];
+  const Op& tail = c.ops[ch.tail];
+  ChainDev<T> d;
+  d.a = arena + head.a_base;
+  d.a_item = head.a_item;
+  d.out = arena + ch.out_base;
+  d.out_item = tail.out_item;
+  d.entries = dp.d_index + ch.entries_off;
+  d.nb = tail.nb;
+  d.n_steps = static_cast<int>(ch.steps.size());
+  d.q = ch.q;
+  d.inner_bits = ch.u_inner_bits;
+  d.outer_bits = ch.u_bits - ch.u_inner_bits;
+  d.ld_bits = static_cast<int>(ch.qin.size() / 2);
+  d.st_bits = static_cast<int>(ch.qout.size() / 2);
+  d.n_ld = 1 << d.ld_bits;
+  d.n_st = 1 << d.st_bits;
+  if (d.ld_bits > 11 || d.st_bits > 11) throw InternalError("chain block larger than 2048 elements");
+  for (int i = 0; i < d.ld_bits; ++i) {
+    d.ld_p[i] = ch.qin[2 * i];
+    d.ld_o[i] = ch.qin[2 * i + 1];
+  }
+  for (int i = 0; i < d.st_bits; ++i) {
+    d.st_p[i] = ch.qout[2 * i];
+    d.st_o[i] = ch.qout[2 * i + 1];
+  }
+  d.tu_in = dtable(dp.d_tables, ch.tu_in);
+  d.tu_out = dtable(dp.d_tables, ch.tu_out);
+  d.cur = dp.d_cur;
+  d.s_bits = dp.s_bits;
+  for (size_t l = 0; l < ch.steps.size(); ++l) {
+    const ChainStep& cs = ch.steps[l];
+    const Op& op = c.ops[cs.op];
+    auto& s = d.steps[l];
+    s.b = op.b_leaf ? leaves + op.b_base : arena + op.b_base;
+    s.b_item = op.b_item;
+    s.b_sstr = dp.b_str_off[cs.op] < 0 ? nullptr : dp.d_sstr + dp.b_str_off[cs.op];
+    s.tbl = dp.d_index + cs.tbl_off;
+    s.out_bits = __builtin_ctz(cs.n_out);
+    s.kc = cs.kc;
+    s.g_bits = cs.g_bits;
+    s.f_bits = cs.f_bits;
+    s.tbl_rel = static_cast<int>(cs.tbl_off - ch.steps[0].tbl_off);
+  }
+  d.tbl_words = static_cast<int>(ch.steps.back().tbl_off + ch.steps.back().tbl.size() - ch.steps[0].tbl_off);
+  const size_t smem = (2 * ((size_t{1} << d.q) + 1 << d.inner_bits) + 64 * ch.steps.size()) * sizeof(T) +
+                      4 * static_cast<size_t>(d.tbl_words);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    CK(cudaFuncSetAttribute(chain_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    smem_set = smem;
+  }
+  // chunks per block: up to 8, keeping >= 4 blocks per SM's worth of work
+  d.cpb_bits = 0;
+  while (d.cpb_bits < 3 && d.outer_bits - d.cpb_bits > 0 &&
+         (uint64_t{tail.nb} << (d.outer_bits - d.cpb_bits - 1)) >= 148 * 8)
+    ++d.cpb_bits;
+  const uint64_t blocks = uint64_t{tail.nb} << (d.outer_bits - d.cpb_bits);
+  chain_kernel<R><<<static_cast<unsigned>(blocks), 256, smem, st>>>(d);
+}
+
 template <class R>
 void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEvent_t* op_events = nullptr,
                       DagIssue* dag = nullptr, size_t op0 = 0, size_t op1 = ~size_t{0}) {
@@ -925,8 +1176,16 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
   for (size_t oi = op0; oi < std::min(op1, c.ops.size()); ++oi) {
     const Op& op = c.ops[oi];
     if (op.nb == 0) continue;
+    if (op.chain >= 0 && !op.chain_tail) continue;  // evaluated by its chain's tail
     const cudaStream_t st = dag ? dag->begin(oi) : st_main;
     if (op_events) CK(cudaEventRecord(op_events[2 * oi], st));
+    if (op.chain >= 0) {
+      launch_chain<R>(dp, c.chains[op.chain], st);
+      dp.engine->launches++;
+      if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
+      if (dag) dag->end(oi);
+      continue;
+    }
     DevOp<T> d;
     d.a = op.a_leaf ? leaves + op.a_base : arena + op.a_base;
     d.b = op.b_leaf ? leaves + op.b_base : arena + op.b_base;
@@ -1320,7 +1579,8 @@ void time_ops(DevicePlan& dp, uint64_t slice, void* d_acc, bool accumulate, void
   CK(cudaStreamSynchronize(st));
   for (size_t i = 0; i < n; ++i) {
     op_ms[i] = 0.f;
-    if (dp.c.ops[i].nb) CK(cudaEventElapsedTime(&op_ms[i], ev[2 * i], ev[2 * i + 1]));
+    const Op& op = dp.c.ops[i];
+    if (op.nb && (op.chain < 0 || op.chain_tail)) CK(cudaEventElapsedTime(&op_ms[i], ev[2 * i], ev[2 * i + 1]));
   }
   for (auto& e : ev) cudaEventDestroy(e);
 }

@@ -877,6 +877,312 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
   for (size_t i : scratch_private) c.ops[i].scratch_off += arena_top;
   c.arena_elems = arena_top + private_top;
   c.private_elems = private_top;
+  // --- fused operand chains ---------------------------------------------------------
+  // Runs of consecutive skinny ops (CUDA-core configs, K <= 8, N <= 8) where
+  // each op's A is the previous op's table and the items map one-to-one: one
+  // kernel keeps the running tensor block in shared memory (Chain). Members
+  // are consecutive in the schedule, so the tables they read (the head's A,
+  // every step's B) are still intact when the tail launches. Within one
+  // slice-reuse segment only.
+  if (!std::getenv("MTCG_NO_CHAIN")) {
+    std::vector<int> op_of(n, -1);
+    for (size_t i = 0; i < c.ops.size(); ++i) op_of[c.ops[i].node] = static_cast<int>(i);
+    auto eligible = [&](const Op& op) {
+      return !op.root && op.nb > 0 && op.kc <= 3 && op.fb <= 3 && op.config != kTcConfig &&
+             op.config != kDotConfig && op.config != kRowsGroupedConfig;
+    };
+    auto bijective = [&](const Op& op) {
+      std::vector<char> seen(op.nb, 0);
+      for (uint32_t v : op.ia) {
+        if (v >= op.nb || seen[v]) return false;
+        seen[v] = 1;
+      }
+      return true;
+    };
+    auto linked = [&](size_t i) {  // op i+1 continues op i
+      const Op& a = c.ops[i];
+      const Op& b = c.ops[i + 1];
+      const bool seg = (i < c.n_prologue_ops) == (i + 1 < c.n_prologue_ops);
+      return seg && eligible(a) && eligible(b) && !b.a_leaf && op_of[b.child_a] == static_cast<int>(i) &&
+             a.nb == b.nb && bijective(b);
+    };
+    const int q_max = 8;
+    size_t i = 0;
+    while (i + 1 < c.ops.size()) {
+      if (!linked(i) || c.ops[i].a_leaf) {
+        ++i;
+        continue;
+      }
+      // extend while the touched legs fit q_max positions: all T0 legs the
+      // run closes are loaded up front, each step then closes some touched
+      // legs and opens its B's new legs
+      const int t0 = c.ops[i].child_a;
+      const std::vector<uint32_t>& T = legs[t0];
+      auto chain_q = [&](size_t k) {
+        std::vector<uint32_t> cur(T), qin;
+        for (size_t s = i; s <= k; ++s) {
+          const auto& bl = legs[c.ops[s].child_b];
+          std::vector<uint32_t> next;
+          for (uint32_t x : cur)
+            if (!contains(bl, x)) next.push_back(x);
+            else if (contains(T, x)) qin.push_back(x);
+          for (uint32_t x : bl)
+            if (!contains(cur, x)) next.push_back(x);
+          cur = next;
+        }
+        std::vector<uint32_t> active(qin);
+        size_t qm = active.size();
+        cur = T;
+        for (size_t s = i; s <= k; ++s) {
+          const auto& bl = legs[c.ops[s].child_b];
+          std::vector<uint32_t> next, na;
+          for (uint32_t x : cur)
+            if (!contains(bl, x)) next.push_back(x);
+          for (uint32_t x : active)
+            if (!contains(bl, x)) na.push_back(x);
+          for (uint32_t x : bl)
+            if (!contains(cur, x)) {
+              next.push_back(x);
+              na.push_back(x);
+            }
+          cur = next;
+          active = na;
+          qm = std::max(qm, active.size());
+        }
+        return static_cast<int>(qm);
+      };
+      int best_end = -1;
+      for (size_t k = i + 1; k < c.ops.size() && linked(k - 1) && k - i < kMaxChainSteps; ++k) {
+        if (chain_q(k) > q_max) break;
+        best_end = static_cast<int>(k);
+      }
+      if (best_end < 0) {
+        ++i;
+        continue;
+      }
+      const size_t j = static_cast<size_t>(best_end);
+      // ---- build the chain over ops [i, j] ----
+      Chain ch;
+      ch.head = static_cast<int>(i);
+      ch.tail = static_cast<int>(j);
+      const auto& l0 = layout[t0];
+      // Q_in: T0 legs some step closes, by T0 stride ascending
+      std::vector<uint32_t> cur(T);
+      std::vector<uint32_t> qin;
+      {
+        std::vector<uint32_t> tmp(T);
+        for (size_t s = i; s <= j; ++s) {
+          const auto& bl = legs[c.ops[s].child_b];
+          std::vector<uint32_t> next;
+          for (uint32_t x : tmp)
+            if (!contains(bl, x)) next.push_back(x);
+            else if (contains(T, x) && !contains(qin, x)) qin.push_back(x);
+          for (uint32_t x : bl)
+            if (!contains(tmp, x)) next.push_back(x);
+          tmp = next;
+        }
+      }
+      std::sort(qin.begin(), qin.end(),
+                [&](uint32_t x, uint32_t y) { return stride_in(l0, x) < stride_in(l0, y); });
+      std::map<uint32_t, int> pos;  // touched leg -> position
+      for (size_t b = 0; b < qin.size(); ++b) pos[qin[b]] = static_cast<int>(b);
+      const std::map<uint32_t, int> pos0 = pos;
+      int q = static_cast<int>(qin.size());
+      std::vector<uint32_t> active(qin);
+      for (size_t s = i; s <= j; ++s) {
+        const Op& op = c.ops[s];
+        const auto& bl = legs[op.child_b];
+        const auto& blay = layout[op.child_b];
+        std::vector<uint32_t> closed, opened, kept;
+        for (uint32_t x : bl) (contains(cur, x) ? closed : opened).push_back(x);
+        std::sort(closed.begin(), closed.end());
+        std::sort(opened.begin(), opened.end());
+        for (uint32_t x : active)
+          if (!contains(closed, x)) kept.push_back(x);
+        // positions after the step: kept legs stay, opened legs take the
+        // lowest free positions (closed ones included — a separate buffer)
+        std::map<uint32_t, int> npos;
+        std::vector<char> used(64, 0);
+        for (uint32_t x : kept) {
+          npos[x] = pos[x];
+          used[pos[x]] = 1;
+        }
+        for (uint32_t x : opened) {
+          int p_ = 0;
+          while (used[p_]) ++p_;
+          used[p_] = 1;
+          npos[x] = p_;
+          q = std::max(q, p_ + 1);
+        }
+        // output combination o = f + (g << |kept|): f over the kept touched
+        // legs (lowest positions first), g over the opened legs
+        std::sort(kept.begin(), kept.end(), [&](uint32_t x, uint32_t y) { return pos[x] < pos[y]; });
+        std::vector<uint32_t> out_legs(kept);
+        out_legs.insert(out_legs.end(), opened.begin(), opened.end());
+        ChainStep st;
+        st.op = static_cast<int>(s);
+        st.kc = static_cast<int>(closed.size());
+        st.n_out = 1u << out_legs.size();
+        // B tile: (closed combo c, opened combo g) at c * G + g, loaded from
+        // the entry at boff[c * G + g]
+        const uint32_t G = 1u << opened.size(), F = 1u << kept.size();
+        std::vector<uint32_t> in_base(F), out_f(F), out_g(G);
+        for (uint32_t f = 0; f < F; ++f)
+          for (size_t x = 0; x < kept.size(); ++x)
+            if (f >> x & 1) {
+              in_base[f] += 1u << pos[kept[x]];
+              out_f[f] += 1u << npos[kept[x]];
+            }
+        for (uint32_t g = 0; g < G; ++g)
+          for (size_t x = 0; x < opened.size(); ++x)
+            if (g >> x & 1) out_g[g] += 1u << npos[opened[x]];
+        // reduction order: ascending closed ids, row-major (bit 0 = highest id)
+        std::vector<uint32_t> k_legs(closed.rbegin(), closed.rend());
+        const uint32_t K = 1u << k_legs.size();
+        std::vector<uint32_t> in_c(K), boff(K * G);
+        for (uint32_t cc = 0; cc < K; ++cc) {
+          uint32_t coff = 0;
+          for (size_t x = 0; x < k_legs.size(); ++x)
+            if (cc >> x & 1) {
+              in_c[cc] += 1u << pos[k_legs[x]];
+              coff += static_cast<uint32_t>(stride_in(blay, k_legs[x]));
+            }
+          for (uint32_t g = 0; g < G; ++g) {
+            uint32_t goff = 0;
+            for (size_t x = 0; x < opened.size(); ++x)
+              if (g >> x & 1) goff += static_cast<uint32_t>(stride_in(blay, opened[x]));
+            boff[cc * G + g] = coff + goff;
+          }
+        }
+        st.g_bits = static_cast<int>(opened.size());
+        st.f_bits = static_cast<int>(kept.size());
+        for (auto* v : {&in_base, &out_f, &out_g, &in_c, &boff})
+          st.tbl.insert(st.tbl.end(), v->begin(), v->end());
+        ch.steps.push_back(std::move(st));
+        std::vector<uint32_t> next;
+        for (uint32_t x : cur)
+          if (!contains(closed, x)) next.push_back(x);
+        for (uint32_t x : opened) next.push_back(x);
+        cur = next;
+        active = out_legs;
+        pos = npos;
+      }
+      ch.q = q;
+      // untouched legs: T0's legs outside Q_in == the tail's legs outside active
+      const int tl = c.ops[j].node;
+      const auto& lt = layout[tl];
+      std::vector<uint32_t> U;
+      for (uint32_t x : T)
+        if (!contains(qin, x)) U.push_back(x);
+      bool consistent = U.size() + active.size() == lt.size();
+      for (uint32_t x : U) consistent &= contains(lt, x);
+      if (!consistent) throw InternalError("operand chain: leg bookkeeping mismatch");
+      // A block takes 2^cb combinations of the "inner" untouched legs: the
+      // lowest-stride ones of the input AND of the output layout, alternating,
+      // so both its loads and its stores run over contiguous memory (the
+      // touched legs fill 2^q positions per combination; 2^(cb+q) <= 4096
+      // elements per buffer in complex64, 2048 in complex128).
+      auto by = [&](const std::vector<uint32_t>& lay) {
+        std::vector<uint32_t> v(U);
+        std::sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) { return stride_in(lay, x) < stride_in(lay, y); });
+        return v;
+      };
+      const std::vector<uint32_t> u_in = by(l0), u_out = by(lt);
+      const int cb_max = std::max(0, (c.elem_bytes == 8 ? 11 : 10) - q);
+      std::vector<uint32_t> inner;
+      for (size_t r = 0; static_cast<int>(inner.size()) < std::min<int>(cb_max, static_cast<int>(U.size())); ++r) {
+        if (r < u_out.size() && !contains(inner, u_out[r])) inner.push_back(u_out[r]);
+        if (static_cast<int>(inner.size()) < cb_max && r < u_in.size() && !contains(inner, u_in[r]))
+          inner.push_back(u_in[r]);
+      }
+      std::vector<uint32_t> outer;
+      for (uint32_t x : u_out)
+        if (!contains(inner, x)) outer.push_back(x);
+      ch.u_bits = static_cast<int>(U.size());
+      ch.u_inner_bits = static_cast<int>(inner.size());
+      {
+        std::vector<uint64_t> si, so;
+        for (uint32_t x : outer) {
+          si.push_back(stride_in(l0, x));
+          so.push_back(stride_in(lt, x));
+        }
+        ch.tu_in.build(si);
+        ch.tu_out.build(so);
+      }
+      // load / store maps over (inner untouched legs x touched legs), in
+      // address order: (shared-memory position, element offset in the block)
+      auto block_map = [&](const std::vector<uint32_t>& touched, const std::vector<uint32_t>& lay,
+                           const std::map<uint32_t, int>& tpos, std::vector<uint32_t>& out) {
+        std::vector<uint32_t> all(inner);
+        all.insert(all.end(), touched.begin(), touched.end());
+        std::sort(all.begin(), all.end(), [&](uint32_t x, uint32_t y) { return stride_in(lay, x) < stride_in(lay, y); });
+        // per bit of the block index: its shared-memory position and its
+        // element offset (rows of 2^q + 1 elements: an odd pitch spreads rows
+        // over the banks)
+        for (uint32_t leg : all) {
+          auto it = std::find(inner.begin(), inner.end(), leg);
+          out.push_back(it != inner.end() ? ((1u << q) + 1) << static_cast<int>(it - inner.begin())
+                                          : 1u << tpos.at(leg));
+          out.push_back(static_cast<uint32_t>(stride_in(lay, leg)));
+        }
+      };
+      block_map(qin, l0, pos0, ch.qin);
+      block_map(active, lt, pos, ch.qout);
+      // entries per final item: back through the one-to-one item maps
+      const uint32_t nb = c.ops[j].nb;
+      const size_t L = j - i + 1;
+      ch.entries.assign((L + 1) * nb, 0);
+      for (uint32_t b = 0; b < nb; ++b) {
+        uint32_t it = b;
+        for (size_t s = j + 1; s-- > i;) {
+          ch.entries[(s - i + 1) * nb + b] = c.ops[s].ib[it];
+          if (s > i) it = c.ops[s].ia[it];
+          else ch.entries[b] = c.ops[s].ia[it];
+        }
+      }
+      const int ci = static_cast<int>(c.chains.size());
+      for (size_t s = i; s <= j; ++s) c.ops[s].chain = ci;
+      c.ops[j].chain_tail = true;
+      if (std::getenv("MTCG_DUMP_OPS")) {
+        std::fprintf(stderr, "[mtcg] chain:");
+        for (size_t s2 = i; s2 <= j; ++s2) std::fprintf(stderr, " %d", c.ops[s2].node);
+        std::fprintf(stderr, "  q %d u_bits %d inner %d items %u\n", ch.q, ch.u_bits, ch.u_inner_bits, nb);
+        std::fprintf(stderr, "[mtcg]   ld bit strides:");
+        for (size_t e = 0; e < ch.qin.size() / 2; ++e) std::fprintf(stderr, " %u", ch.qin[2 * e + 1]);
+        std::fprintf(stderr, "\n[mtcg]   st bit strides:");
+        for (size_t e = 0; e < ch.qout.size() / 2; ++e) std::fprintf(stderr, " %u", ch.qout[2 * e + 1]);
+        std::fprintf(stderr, "\n");
+      }
+      c.chains.push_back(std::move(ch));
+      i = j + 1;
+    }
+    // Each tail writes its table into its own region above the arena: in the
+    // first-fit arena it could overlap the head's A or a step's B, which the
+    // chain kernel still reads while it writes (members write nothing, so
+    // nothing else changes). Chains are dropped if that does not fit the cap.
+    uint64_t top = c.arena_elems;
+    for (const Chain& ch : c.chains) top += (table_elems[c.ops[ch.tail].node] + align - 1) / align * align;
+    if (cap_bytes && top * c.elem_bytes + fixed_bytes > cap_bytes) {
+      for (Op& op : c.ops) {
+        op.chain = -1;
+        op.chain_tail = false;
+      }
+      c.chains.clear();
+    }
+    top = c.arena_elems;
+    for (Chain& ch : c.chains) {
+      const int tn = c.ops[ch.tail].node;
+      ch.out_base = top;
+      c.ops[ch.tail].out_base = top;
+      for (Op& o : c.ops) {
+        if (!o.a_leaf && o.child_a == tn) o.a_base = top;
+        if (!o.b_leaf && o.child_b == tn) o.b_base = top;
+      }
+      top += (table_elems[tn] + align - 1) / align * align;
+    }
+    c.arena_elems = top;
+  }
+
   // --- dependencies between ops (arena read/write ranges) ---------------------
   {
     struct Access {
@@ -889,9 +1195,16 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     for (size_t i = 0; i < c.ops.size(); ++i) op_of_node[c.ops[i].node] = static_cast<int>(i);
     for (size_t i = 0; i < c.ops.size(); ++i) {
       Op& op = c.ops[i];
+      // fused chains: members launch nothing; the tail performs every
+      // member's operand reads
+      if (op.chain >= 0 && !op.chain_tail) continue;
       std::vector<std::pair<uint64_t, uint64_t>> reads, writes;
-      if (!op.a_leaf && table_elems[op.child_a]) reads.push_back({op.a_base, op.a_base + table_elems[op.child_a]});
-      if (!op.b_leaf && table_elems[op.child_b]) reads.push_back({op.b_base, op.b_base + table_elems[op.child_b]});
+      const size_t first = op.chain >= 0 ? static_cast<size_t>(c.chains[op.chain].head) : i;
+      for (size_t m = first; m <= i; ++m) {
+        const Op& mo = c.ops[m];
+        if (!mo.a_leaf && table_elems[mo.child_a]) reads.push_back({mo.a_base, mo.a_base + table_elems[mo.child_a]});
+        if (!mo.b_leaf && table_elems[mo.child_b]) reads.push_back({mo.b_base, mo.b_base + table_elems[mo.child_b]});
+      }
       if (!op.root && table_elems[op.node]) writes.push_back({op.out_base, op.out_base + table_elems[op.node]});
       if (op.scratch_elems) writes.push_back({op.scratch_off, op.scratch_off + op.scratch_elems});
       std::vector<int> deps;
@@ -903,8 +1216,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       }
       // operand producers (also covered by their write records; explicit for
       // zero-size tables)
-      for (int ch : {op.child_a, op.child_b})
-        if (op_of_node[ch] >= 0 && c.ops[op_of_node[ch]].nb > 0) deps.push_back(op_of_node[ch]);
+      for (size_t m = first; m <= i; ++m)
+        for (int ch : {c.ops[m].child_a, c.ops[m].child_b})
+          if (op_of_node[ch] >= 0 && c.ops[op_of_node[ch]].nb > 0) deps.push_back(op_of_node[ch]);
       std::sort(deps.begin(), deps.end());
       deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
       op.deps = std::move(deps);
@@ -955,6 +1269,14 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     op.grp_items_off = put_index(op.grp_items);
     op.grp_start_off = put_index(op.grp_start);
     op.out_rows_off = put_index(op.out_rows);
+  }
+  for (Chain& ch : c.chains) {
+    put_table(ch.tu_in);
+    put_table(ch.tu_out);
+    ch.qin_off = put_index(ch.qin);
+    ch.qout_off = put_index(ch.qout);
+    ch.entries_off = put_index(ch.entries);
+    for (ChainStep& st : ch.steps) st.tbl_off = put_index(st.tbl);
   }
   if (c.has_leaf_root) {
     put_table(c.leaf_root.tout);

@@ -81,6 +81,51 @@ struct Op {
   std::vector<int> deps;
   // exact algorithmic counts per slice (tensor.cpp:132-148)
   uint64_t mults = 0, adds = 0, rw = 0;
+  // fused operand chain (Compiled::chains) this op belongs to, -1: none. The
+  // chain's last op launches the fused kernel; the others launch nothing.
+  int chain = -1;
+  bool chain_tail = false;
+};
+
+// A run of consecutive skinny ops along one operand chain (each op's A is the
+// previous op's output, items map one-to-one) evaluated by one kernel: a block
+// of the first op's A is loaded into shared memory once, every step contracts
+// it in place with its small B in the reference's order, and only the last
+// op's table is written. Intermediate tables never reach HBM.
+//   The legs the chain touches (A legs some step closes, legs a B opens) live
+//   in shared-memory positions [0, 2^q) per untouched-leg combination u;
+//   closed legs free their positions for the legs opened after them.
+constexpr int kMaxChainSteps = 8;
+constexpr int kMaxChainTable = 2 * 256 + 8 + 8 + 64;  // words of one step's tables (q <= 8, K, G <= 8)
+struct ChainStep {
+  int op = -1;                 // op index (B operand, ib, slice strides)
+  int kc = 0;
+  int g_bits = 0;              // legs the step's B opens
+  int f_bits = 0;              // touched legs the step keeps
+  uint32_t n_out = 0;          // combos of the active touched legs after the step
+  // in_base[2^f] | out_f[2^f] | out_g[2^g] | in_c[2^kc] | boff[2^(kc + g)]:
+  // row positions of the kept-leg combination f in the input and output
+  // rows, of the opened-leg combination g, of the closed combination c, and
+  // the B tile's element offsets (c * 2^g + g) in the B entry
+  std::vector<uint32_t> tbl;
+  uint64_t tbl_off = 0;        // word offset in the index blob
+};
+struct Chain {
+  int head = -1, tail = -1;    // op indices, consecutive
+  int q = 0;                   // log2 positions per inner combination
+  int u_bits = 0;              // untouched legs
+  int u_inner_bits = 0;        // of which inside one block (the rest index blocks)
+  SplitTable tu_in, tu_out;    // outer combination -> element offset in the head's A / tail's output
+  // block load / store maps: the block's elements are indexed by bits over
+  // (inner untouched legs + touched legs) in address order; per bit, the
+  // (shared-memory position, element offset) it adds
+  std::vector<uint32_t> qin, qout;
+  uint64_t qin_off = 0, qout_off = 0;
+  uint64_t out_base = 0;       // tail output: its own arena region (never reused)
+  std::vector<ChainStep> steps;
+  // per final item: the head's A entry, then each step's B entry ([steps+1][nb])
+  std::vector<uint32_t> entries;
+  uint64_t entries_off = 0;
 };
 
 // A plan whose root is a leaf (single-slot network): copy/accumulate the
@@ -112,6 +157,7 @@ struct Compiled {
   std::vector<double> leaf_values;     // complex128 interleaved (host copy)
   // schedule
   std::vector<Op> ops;
+  std::vector<Chain> chains;           // fused operand chains (MTCG_NO_CHAIN=1: none)
   bool has_leaf_root = false;
   LeafRoot leaf_root;
   std::vector<uint32_t> table_blob;    // all SplitTables

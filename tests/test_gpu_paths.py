@@ -157,3 +157,58 @@ def test_plan_survives_arena_growth(engine):
     cp2.run(0, 1, acc2.data_ptr())
     cp1.run(0, cp1.n_slices, acc1.data_ptr())
     assert bits_equal(cp1.fetch(acc1.data_ptr()).amplitudes, first)
+
+
+def _op_kernels(cp):
+    import ctypes as C
+
+    from paper_2108_05665_b200._lib import lib
+
+    class OpInfo(C.Structure):
+        _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
+                    ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
+                    ("mults", C.c_uint64), ("bytes", C.c_uint64)]
+
+    L = lib()
+    L.mtcg_plan_op_count.restype = C.c_int32
+    L.mtcg_plan_op_count.argtypes = [C.c_void_p]
+    L.mtcg_plan_op_info.argtypes = [C.c_void_p, C.c_int32, C.POINTER(OpInfo)]
+    out = []
+    for i in range(L.mtcg_plan_op_count(cp.h)):
+        oi = OpInfo()
+        L.mtcg_plan_op_info(cp.h, i, C.byref(oi))
+        out.append((oi.node, oi.kernel))
+    return out
+
+
+@pytest.mark.parametrize("name,precision", [("cfg1", "c128"), ("cfg2", "c128"), ("cfg2", "c64")])
+def test_fused_chains_match_unfused(engine, monkeypatch, name, precision):
+    """Fused operand chains (consecutive skinny ops evaluated in shared memory,
+    planner.hpp Chain) keep every step's reduction order: bit-identical to
+    the op-by-op path in both precisions; and they are in use (cfg2: nodes
+    301 -> 302 -> 304 -> 305)."""
+    p, c, bits = workload(name)
+    opts = EvalOptions(precision=precision)
+    cp = engine.compile(p, A.MTCG_EVAL_AUTO, opts)
+    fused_nodes = [n for n, k in _op_kernels(cp) if k == 16]
+    assert fused_nodes, "no fused chains"
+    if name == "cfg2":
+        assert {301, 302, 304, 305} <= set(fused_nodes)
+    del cp
+    fused = run(engine, p, opts)
+    monkeypatch.setenv("MTCG_NO_CHAIN", "1")
+    plain = run(engine, p, opts)
+    assert bits_equal(fused, plain)
+    if precision == "c128" and name == "cfg1":
+        ov, _, _, _ = O.eval_problem(p)
+        assert bits_equal(fused, ov)
+
+
+@pytest.mark.parametrize("seed", list(range(0, 40, 3)))
+def test_fused_chains_random_instances(engine, seed):
+    p, c, bits = random_instance(seed)
+    cp = engine.compile(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128"))
+    acc = cp.new_accumulator()
+    cp.run(0, cp.n_slices, acc.data_ptr())
+    ov, _, _, _ = O.eval_problem(p)
+    assert bits_equal(cp.fetch(acc.data_ptr()).amplitudes, ov)
