@@ -190,7 +190,26 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
     } else {
       const uint32_t* rl = ti.rank[p.node_left[node]];
       const uint32_t* rr = ti.rank[p.node_right[node]];
+      const uint64_t dl = ti.distinct[p.node_left[node]];
       const uint64_t dr = ti.distinct[p.node_right[node]];
+      if (rows && (dl == 1 || dr == 1)) {
+        // one child is the same for every row: key = the other child's rank,
+        // already dense — share its rank array (read-only from here on)
+        const bool left_varies = dr == 1;
+        ti.rank[node] = const_cast<uint32_t*>(left_varies ? rl : rr);
+        const uint64_t d = left_varies ? dl : dr;
+        ti.distinct[node] = static_cast<uint32_t>(d);
+        auto& pl = ti.pair_l[node];
+        auto& pr = ti.pair_r[node];
+        pl.resize(d);
+        pr.resize(d);
+        for (uint64_t i = 0; i < d; ++i) {
+          pl[i] = left_varies ? static_cast<uint32_t>(i) : 0u;
+          pr[i] = left_varies ? 0u : static_cast<uint32_t>(i);
+        }
+        t_keys += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c0).count();
+        continue;
+      }
       for (uint64_t r = 0; r < rows; ++r) keys[r] = rl[r] * dr + rr[r];
       span = ti.distinct[p.node_left[node]] * dr;
     }
