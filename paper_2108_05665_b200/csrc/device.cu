@@ -268,10 +268,12 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
     }
     __syncthreads();
     // A tile: k fastest across lanes (K-contiguous rows)
+#pragma unroll 8
     for (int e = tid; e < TM * tk; e += NT) {
       const int row = e / tk, kk = e - row * tk;
       As[kk * (TM + 1) + row] = row < m_valid ? A[aoff[row] + kao[kk]] : czero<T>();
     }
+#pragma unroll 8
     for (int e = tid; e < TN * tk; e += NT) {
       const int col = e / tk, kk = e - col * tk;
       Bs[kk * (TN + 1) + col] = col < n_valid ? B[boff[col] + kbo[kk]] : czero<T>();
@@ -1028,7 +1030,11 @@ void launch_op(const DevOp<typename V2<R>::T>& op, int config, cudaStream_t st) 
     case 6: return launch_tile<R, 256, 2, 2, 1>(op, st);
     case 7: return launch_tile<R, 256, 1, 1, 1>(op, st);
     case 8: return launch_tile<R, 64, 64, 4, 4>(op, st);
-    case 9: return launch_tile<R, 32, 32, 2, 2>(op, st);
+    case 9:
+      // long K: 4 x 4 register tiles (8 shared loads per 16 complex MACs
+      // instead of 4 per 4; 64 threads per 32 x 32 tile)
+      if (op.kc >= 5) return launch_tile<R, 32, 32, 4, 4>(op, st);
+      return launch_tile<R, 32, 32, 2, 2>(op, st);
     case 10: return launch_tile<R, 16, 16, 1, 1>(op, st);
     default: throw CudaError("unknown kernel configuration " + std::to_string(config));
   }
