@@ -166,6 +166,8 @@ typedef struct mtcg_plan_info {
                                    run once per run range (0 without) */
   uint64_t executed_contractions; /* contractions one run over all slices
                                      executes (= contractions without reuse) */
+  uint64_t fused_chains;        /* runs of skinny ops evaluated by one kernel */
+  uint64_t fused_ops;           /* ops inside those runs */
 } mtcg_plan_info;
 
 int mtcg_version(void);

@@ -96,6 +96,8 @@ class mtcg_plan_info(C.Structure):
         ("n_kernels_per_slice", C.c_int32),
         ("prologue_ops", C.c_uint64),
         ("executed_contractions", C.c_uint64),
+        ("fused_chains", C.c_uint64),
+        ("fused_ops", C.c_uint64),
     ]
 
 

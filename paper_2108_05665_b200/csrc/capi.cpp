@@ -106,6 +106,9 @@ void fill_info(const Compiled& c, mtcg_plan_info* info) {
   info->precision = c.precision;
   info->prologue_ops = c.n_prologue_ops;
   info->executed_contractions = c.executed_contractions;
+  info->fused_chains = c.chains.size();
+  info->fused_ops = 0;
+  for (const Chain& ch : c.chains) info->fused_ops += static_cast<uint64_t>(ch.tail - ch.head + 1);
   int k = 0;
   for (const Op& op : c.ops)
     if (op.nb && (op.chain < 0 || op.chain_tail)) ++k;

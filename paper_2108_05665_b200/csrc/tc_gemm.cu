@@ -378,30 +378,11 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
-__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.b32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-
-// Waits on barriers the peer CTA arrives on. The default (.acquire.cta)
-// try_wait is what CUTLASS's 2-SM pipelines use for peer-signalled barriers;
-// MTCG_TC_ACQ_CLUSTER=1 builds use the cluster-scope form instead.
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-#ifdef MTCG_TC_ACQ_CLUSTER
-  while (!mbar_try_wait_cluster(bar, parity)) {
-  }
-#else
-  while (!mbar_try_wait(bar, parity)) {
-  }
-#endif
-}
+// Waits on barriers the peer CTA arrives on (remote arrives, multicast
+// commits). The default-semantics (.acquire.cta) try_wait, as CUTLASS's 2-SM
+// pipelines use for peer-signalled barriers; the .acquire.cluster form
+// measured no different.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::

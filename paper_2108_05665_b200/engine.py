@@ -81,6 +81,7 @@ class EmulateResult:
     peak_bytes: int
     node_contractions: np.ndarray
     contractions: int = 0
+    plan_info: Optional[A.mtcg_plan_info] = None  # schedule facts (prologue, fused chains)
 
 
 def _raise(status: int, err: C.Array, cap_node: int = -1):
@@ -294,9 +295,11 @@ def emulate_arrays(problem: A.ProblemArrays, opts: Optional[EvalOptions] = None,
                             err, 1024)
     if st:
         _raise(st, err, cap_node.value)
-    return EmulateResult(OpCounters(int(info.mults), int(info.adds), int(info.rw)),
-                         int(info.hbm_arena_bytes + info.hbm_resident_bytes),
-                         nc[:problem.n_nodes].copy(), int(info.contractions))
+    r = EmulateResult(OpCounters(int(info.mults), int(info.adds), int(info.rw)),
+                      int(info.hbm_arena_bytes + info.hbm_resident_bytes),
+                      nc[:problem.n_nodes].copy(), int(info.contractions))
+    r.plan_info = info  # the device schedule the same options would build
+    return r
 
 
 def emulate(plan: Plan, d: NetworkDiagram, assignments: AssignmentSet,

@@ -109,3 +109,47 @@ def test_device_entry_points_fail_loudly_without_gpu():
 
     with pytest.raises(EngineError):
         Engine(0)
+
+
+# ---- device schedule built on the host (no GPU): slice reuse, fused chains ----
+
+
+def test_slice_reuse_schedule_keeps_reference_counts():
+    """MTCG_FLAG_SLICE_REUSE reorders the schedule (slice-invariant prologue)
+    but every reference count is unchanged; cfg2 executes fewer contractions."""
+    p, c, bits = workload("cfg2")
+    base = emulate_arrays(p, EvalOptions())
+    reuse = emulate_arrays(p, EvalOptions(slice_reuse=True))
+    assert np.array_equal(base.node_contractions, reuse.node_contractions)
+    assert base.counters == reuse.counters and base.contractions == reuse.contractions
+    assert base.plan_info.prologue_ops == 0
+    assert base.plan_info.executed_contractions == base.contractions
+    assert reuse.plan_info.prologue_ops > 0
+    assert reuse.plan_info.executed_contractions < reuse.contractions
+
+
+def test_fused_chains_planned_and_switchable(monkeypatch):
+    """cfg2's spine runs (e.g. nodes 301-305) become fused chains; counts are
+    unaffected; MTCG_NO_CHAIN=1 turns them off; unsliced cfg1 has runs too."""
+    p, c, bits = workload("cfg2")
+    r = emulate_arrays(p, EvalOptions())
+    assert r.plan_info.fused_chains >= 5
+    assert r.plan_info.fused_ops >= 2 * r.plan_info.fused_chains
+    monkeypatch.setenv("MTCG_NO_CHAIN", "1")
+    off = emulate_arrays(p, EvalOptions())
+    assert off.plan_info.fused_chains == 0 and off.plan_info.fused_ops == 0
+    assert np.array_equal(off.node_contractions, r.node_contractions)
+    assert off.counters == r.counters
+    monkeypatch.delenv("MTCG_NO_CHAIN")
+    p1, _, _ = workload("cfg1")
+    assert emulate_arrays(p1, EvalOptions()).plan_info.fused_chains >= 1
+
+
+@pytest.mark.parametrize("seed", range(0, 60, 7))
+def test_schedule_flags_never_change_counts_on_random_instances(seed):
+    p, c, bits = random_instance(seed)
+    a = emulate_arrays(p, EvalOptions())
+    b = emulate_arrays(p, EvalOptions(slice_reuse=True))
+    assert np.array_equal(a.node_contractions, b.node_contractions)
+    assert a.counters == b.counters
+    assert b.plan_info.executed_contractions <= b.contractions
