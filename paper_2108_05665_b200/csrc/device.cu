@@ -1255,7 +1255,13 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
         t.grp_start = op.grp_max ? d.grp_start : nullptr;
         t.n_groups = op.grp_max ? d.n_groups : 0;
         t.slots = op.grp_max;
-        const uint64_t units = op.grp_max ? uint64_t{d.n_groups} * op.grp_max : op.nb;
+        const uint32_t ga_per = op.ga_tiles.empty() ? 0u : 1u + (128u >> op.fa);
+        t.ga_tiles = op.ga_tiles.empty() ? nullptr : dp.d_index + op.ga_tiles_off;
+        t.n_ga_tiles = ga_per ? static_cast<uint32_t>(op.ga_tiles.size() / ga_per) : 0u;
+        t.ga_groups = op.ga_groups.empty() ? nullptr : dp.d_index + op.ga_groups_off;
+        t.n_ga_groups = static_cast<uint32_t>(op.ga_groups.size());
+        const uint64_t units = t.n_ga_groups ? uint64_t{t.n_ga_groups}
+                               : op.grp_max ? uint64_t{d.n_groups} * op.grp_max : op.nb;
         const uint64_t bhat_elems = units << (op.fb + op.kc + 1);
         t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off);
         t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + bhat_elems);

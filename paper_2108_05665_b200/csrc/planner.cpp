@@ -629,6 +629,24 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     Op op;
     op.node = node;
     op.a_is_left = fl.size() >= fr.size();
+    // Tensor-core gather mode (see below): the gathered A side has M = 32 / 64
+    // rows per item and the B side is shared (>= 8 items per B entry); pick
+    // the orientation that satisfies it, else keep A = the side with more
+    // free legs (the CUDA-core kernels assume fa >= fb).
+    bool ga_mode = false;
+    if (c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) && !std::getenv("MTCG_NO_GATHER") &&
+        closed.size() >= 4 && ti.distinct[node] >= 1024 && !std::getenv("MTCG_TC_ONLY")) {
+      auto fits = [&](int ca, const std::vector<uint32_t>& fa_, int cb, const std::vector<uint32_t>& fb_) {
+        return p.node_slot[ca] < 0 && (fa_.size() == 5 || fa_.size() == 6) && fb_.size() >= 4 && fb_.size() <= 7 &&
+               uint64_t{ti.distinct[cb]} * 8 <= ti.distinct[node];
+      };
+      if (fits(op.a_is_left ? l : r, op.a_is_left ? fl : fr, op.a_is_left ? r : l, op.a_is_left ? fr : fl)) {
+        ga_mode = true;
+      } else if (fits(op.a_is_left ? r : l, op.a_is_left ? fr : fl, op.a_is_left ? l : r, op.a_is_left ? fl : fr)) {
+        ga_mode = true;
+        op.a_is_left = !op.a_is_left;
+      }
+    }
     op.child_a = op.a_is_left ? l : r;
     op.child_b = op.a_is_left ? r : l;
     const auto& fa_legs = op.a_is_left ? fl : fr;
@@ -750,9 +768,32 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         s = *end ? end + 1 : end;
       }
     }
-    if (tc_ok && tc_listed) {
+    // Gather mode: M = 32 / 64 rows per item is too short for a 128-row
+    // tensor tile, but when many items share few B entries (cfg2 node 349:
+    // 9,992 items of 32 x 32 x 128 over 128 B entries) the items of one B
+    // entry stack into 128-row tiles against one B̂ (MTCG_NO_GATHER=1 off).
+    const bool ga_ok = ga_mode && !(tc_ok && tc_listed);
+    if (tc_ok && tc_listed && !ga_mode) {
       op.config = kTcConfig;
       if (grouped) op.grp_max = tc_slots;
+    } else if (ga_ok) {
+      op.config = kTcConfig;
+      const uint32_t per = 128u >> op.fa;  // items per tile
+      std::vector<uint32_t> order(op.nb);
+      std::iota(order.begin(), order.end(), 0u);
+      std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return op.ib[x] < op.ib[y]; });
+      for (size_t s0 = 0; s0 < order.size();) {
+        size_t s1 = s0;
+        while (s1 < order.size() && op.ib[order[s1]] == op.ib[order[s0]]) ++s1;
+        const uint32_t g = static_cast<uint32_t>(op.ga_groups.size());
+        op.ga_groups.push_back(op.ib[order[s0]]);
+        for (size_t t0 = s0; t0 < s1; t0 += per) {
+          op.ga_tiles.push_back(g);
+          for (uint32_t k = 0; k < per; ++k)
+            op.ga_tiles.push_back(t0 + k < s1 ? order[t0 + k] : ~0u);
+        }
+        s0 = s1;
+      }
     } else if (grouped && op.fb <= 4 && op.kc <= 5 && op.fa >= 8 &&
                ((uint64_t{g_max} << (op.fb + op.kc)) * c.elem_bytes) <= kGroupSmemBytes) {
       op.config = kRowsGroupedConfig;
@@ -860,7 +901,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     if (op.config == kTcConfig && op.nb > 0) {
       // scratch: B̂ hi/lo (2N x 2K floats per item each)
       op.a_entries = ti.distinct[op.child_a];
-      const uint64_t units = op.grp_max ? uint64_t{op.grp_start.size() - 1} * op.grp_max : op.nb;
+      const uint64_t units = !op.ga_groups.empty() ? uint64_t{op.ga_groups.size()}
+                             : op.grp_max ? uint64_t{op.grp_start.size() - 1} * op.grp_max : op.nb;
       const uint64_t bhat = units << (op.fb + op.kc + 1);
       // B̂ hi / lo (A is split in shared memory) + 4 KB of operand-max partials
       op.scratch_elems = 2 * bhat + 4096 / c.elem_bytes;
@@ -1288,6 +1330,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     op.grp_items_off = put_index(op.grp_items);
     op.grp_start_off = put_index(op.grp_start);
     op.out_rows_off = put_index(op.out_rows);
+    op.ga_groups_off = put_index(op.ga_groups);
+    op.ga_tiles_off = put_index(op.ga_tiles);
   }
   for (Chain& ch : c.chains) {
     put_table(ch.tu_in);

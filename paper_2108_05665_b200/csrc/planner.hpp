@@ -85,6 +85,12 @@ struct Op {
   // chain's last op launches the fused kernel; the others launch nothing.
   int chain = -1;
   bool chain_tail = false;
+  // Tensor-core gather mode (small M, shared B): items grouped by B entry;
+  // each 128-row tile stacks 128 / M items of one group (TMA gathers their A
+  // entries). ga_groups: B entry per group; ga_tiles: per tile the group and
+  // its 128 / M items (~0u pads a group's last tile).
+  std::vector<uint32_t> ga_groups, ga_tiles;
+  uint64_t ga_groups_off = 0, ga_tiles_off = 0;
 };
 
 // A run of consecutive skinny ops along one operand chain (each op's A is the

@@ -284,6 +284,11 @@ struct TcParams {
   int transpose;             // epilogue transposes 32-row chunks through smem
   unsigned long long* dbg;   // MTCG_TC_TRACE: per-tile role timestamps of CTA 0
   const uint32_t* partials;  // 3xFP16: absmax partials (A, then B)
+  // gather mode: tile m-index = entry of ga_tiles ({group, 128 / M items});
+  // the A box is M rows, one per item; B̂ unit = group
+  const uint32_t* ga_tiles;
+  int ga_per;                // items per tile (0: not gather mode)
+  uint32_t nb_ga_tiles;
   int n_conv;                // converter warps (4 or 8); the other 12 - n_conv warps
                              // form (12 - n_conv) / 4 epilogue groups
   // grouped mode (slots > 0): unit = group of items sharing the A entry;
@@ -489,7 +494,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // the root accumulates into the accumulator on every slice but the first
   const int accumulate = p.root ? static_cast<int>(__ldg(p.cur + 1)) : 0;
   const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
-  const uint32_t tiles_m = (p.M + kTM - 1) / kTM;
+  const uint32_t tiles_m = p.ga_per ? p.nb_ga_tiles : (p.M + kTM - 1) / kTM;
   const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
   const int k_stages = p.Kr / BK;
   // wide mode (bn <= 128): each accumulator holds [hi-B half | lo-B half]
@@ -589,8 +594,18 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const uint32_t first = p.slots ? p.grp_items[p.grp_start[item]] : item;
           a_entry = p.ia ? p.ia[first] : first;
         }
-        const int a_row0 = static_cast<int>(a_entry * static_cast<uint64_t>(p.M)) + m0;
-        const int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
+        int a_row0 = static_cast<int>(a_entry * static_cast<uint64_t>(p.M)) + m0;
+        int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
+        int ga_rows[4] = {0, 0, 0, 0};
+        if (!PAIR && p.ga_per) {  // the tile's items' A entries; pads repeat the first
+          const uint32_t* tl = p.ga_tiles + static_cast<uint64_t>(w.m) * (1 + p.ga_per);
+          b_row0 = static_cast<int>(__ldg(tl) * static_cast<uint64_t>(p.Nr)) + n0;
+          for (int k = 0; k < p.ga_per; ++k) {
+            uint32_t itk = __ldg(tl + 1 + k);
+            if (itk == ~0u) itk = __ldg(tl + 1);
+            ga_rows[k] = static_cast<int>(__ldg(p.ia + itk) * static_cast<uint64_t>(p.M));
+          }
+        }
         for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
           const int st = rg.slot;
           if (rg.round > 0) {
@@ -601,7 +616,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
           uint8_t* sp = base + st * stage_bytes;
           mbar_expect_tx(&full[st], a_bytes + 2 * b_bytes);
-          tma_load_2d(sp, &map_a, &full[st], s * BK, a_row0);
+          if (!PAIR && p.ga_per) {
+            for (int k = 0; k < p.ga_per; ++k)
+              tma_load_2d(sp + k * p.M * BK * 4, &map_a, &full[st], s * BK, ga_rows[k]);
+          } else {
+            tma_load_2d(sp, &map_a, &full[st], s * BK, a_row0);
+          }
           tma_load_2d(sp + a_span, &map_bhi, &full[st], s * BK, b_row0);
           tma_load_2d(sp + a_span + b_bytes, &map_blo, &full[st], s * BK, b_row0);
         }
@@ -760,6 +780,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const int c = n0c + r;
       uint32_t item = u;
       int n = c;
+      if (p.ga_per) return static_cast<int64_t>(ton_cached ? ton_s[n] : p.ton(n));  // items: row side
       if (p.slots) {
         const uint32_t g0 = p.grp_start[u], g = p.grp_start[u + 1] - g0;
         const uint32_t slot = static_cast<uint32_t>(c) >> p.fb;
@@ -776,7 +797,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t it = eg;
     uint32_t nxt_unit = 0;
     int m0 = 0, nxt_m0 = 0, nxt_n0 = 0;
-    uint32_t om = 0, nxt_om = 0;
+    uint64_t om = 0, nxt_om = 0;  // row offset; ~0: padding row
     uint64_t key = ~uint64_t{0}, nxt_key = ~uint64_t{0}, table_key = ~uint64_t{0};
     int64_t my_coff = -1, nxt_coff = -1;
     TileWalk w;  // walks the group's tiles one fetch ahead
@@ -786,7 +807,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
       nxt_m0 = static_cast<int>(w.m) * kTM + m_off;
       nxt_n0 = static_cast<int>(w.n) * p.bn;
       w.advance();
-      nxt_om = nxt_m0 + r < p.M ? p.tom(nxt_m0 + r) : 0u;
+      if (p.ga_per) {  // row r = item slot r / M, m = r % M
+        const uint32_t* tl = p.ga_tiles + static_cast<uint64_t>(nxt_m0 / kTM) * (1 + p.ga_per);
+        const uint32_t itm = __ldg(tl + 1 + r / p.M);
+        nxt_om = itm == ~0u ? ~uint64_t{0}
+                            : (p.out_rows ? uint64_t{__ldg(p.out_rows + itm)} : uint64_t{itm}) * p.out_item +
+                                  p.tom(r % p.M);
+      } else {
+        nxt_om = nxt_m0 + r < p.M ? uint64_t{p.tom(nxt_m0 + r)} : ~uint64_t{0};
+      }
       const uint64_t k = (uint64_t{nxt_unit} << 16) | static_cast<uint32_t>(nxt_n0);
       if (k != nxt_key) {
         nxt_key = k;
@@ -814,7 +843,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
       if (warp == e0 && lane == 0) trace(p, it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int m = m0 + r;
       const uint32_t tacc = tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16);
       for (int c0 = 0; c0 < p.bn; c0 += 32) {
         // bn is a multiple of 32 real columns: every chunk is 16 complex columns
@@ -843,8 +871,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll 4
           for (int e = lane; e < 32 * 16; e += 32) {
             const int row = e >> 4, cj = e & 15;
-            const uint32_t row_om = __shfl_sync(0xffffffffu, om, row);
-            if (m0 + quarter * 32 + row >= p.M || co < 0) continue;
+            const uint64_t row_om = __shfl_sync(0xffffffffu, om, row);
+            if (row_om == ~uint64_t{0} || co < 0) continue;
             float2 val = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
             float2* dst = p.out + co + row_om;
             if (accumulate) {
@@ -872,7 +900,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * osa * osb);
           }
-          if (m >= p.M) continue;
+          if (om == ~uint64_t{0}) continue;
           // the 8 column offsets (uniform across lanes): 4 LDS.128 up front,
           // then back-to-back predicated stores
           int64_t co[8];
@@ -1108,7 +1136,7 @@ bool tc_f16() {
 // units * N_eff >= 192 * a_entries (cfg2: nodes 279, 227; not the low-K,
 // HBM-bound ops such as 337 or 285).
 bool tc_use_f16(const TcOp& op) {
-  if (!tc_f16()) return false;
+  if (!tc_f16() || op.ga_tiles) return false;  // gather mode: 3xTF32 (A streamed once)
   static const bool always = std::getenv("MTCG_TC_F16_ALL") != nullptr;
   if (always) return true;
   const uint64_t units = op.slots ? op.n_groups : op.nb;
@@ -1123,8 +1151,10 @@ int tc_tile_n(int Nr) {
 
 int tc_contract(const TcOp& op, cudaStream_t st) {
   const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb, K = uint64_t{1} << op.kc;
-  // units: items, or groups of items sharing the A entry (N_eff = slots x N)
-  const uint32_t units = op.slots ? op.n_groups : op.nb;
+  // units: items, groups of items sharing the A entry (N_eff = slots x N), or
+  // (gather mode) groups of items sharing the B entry
+  const bool ga = op.ga_tiles != nullptr;
+  const uint32_t units = ga ? op.n_ga_groups : op.slots ? op.n_groups : op.nb;
   const uint64_t Nr = 2 * N * (op.slots ? op.slots : 1u), Kr = 2 * K;
   const bool f16 = tc_use_f16(op);
   // 1) B̂ hi / lo (small: per unit 2N_eff x 2K); A is split in the kernel. The
@@ -1134,7 +1164,7 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   BhatSrc src;
   src.b = op.b;
   src.b_item = op.b_item;
-  src.ib = op.ib;
+  src.ib = ga ? op.ga_groups : op.ib;
   src.b_sstr = op.b_sstr;
   src.s_bits = op.s_bits;
   src.cur = op.cur;
@@ -1176,7 +1206,7 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   // CTA pairs for 3xFP16 ops with full-width (256-column) tiles and at least
   // one 256-row tile (MTCG_TC_PAIR=0 disables)
   static const bool pair_env = !(std::getenv("MTCG_TC_PAIR") && std::atoi(std::getenv("MTCG_TC_PAIR")) == 0);
-  const bool pair = f16 && pair_env && bn == 256 && M >= 256 && n_sms >= 2;
+  const bool pair = f16 && !ga && pair_env && bn == 256 && M >= 256 && n_sms >= 2;
   const int bn_cta = pair ? bn / 2 : bn;
   auto stage_of = [&](int bk) {
     return f16 ? kBM * bk * 4 + 2 * bn_cta * bk * 2 : 2 * kBM * bk * 4 + 2 * bn * bk * 4;
@@ -1190,7 +1220,7 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   const int stage_bytes = stage_of(bk);
   const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
   const size_t smem = extra + static_cast<size_t>(n_stages) * stage_bytes;
-  const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, kBM, bk);
+  const CUtensorMap ma = make_map(op.a, Kr, op.a_entries * M, ga ? static_cast<uint32_t>(M) : kBM, bk);
   const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn_cta, bk, f16);
   const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn_cta, bk, f16);
   TcParams p;
@@ -1198,7 +1228,10 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   p.Nr = static_cast<int>(Nr);
   p.Kr = static_cast<int>(Kr);
   p.bn = bn;
-  p.nb = units;
+  p.nb = ga ? 1u : units;
+  p.ga_tiles = op.ga_tiles;
+  p.ga_per = ga ? static_cast<int>(128u >> op.fa) : 0;
+  p.nb_ga_tiles = ga ? op.n_ga_tiles : 0u;
   p.ia = op.ia;
   p.grp_items = op.grp_items;
   p.grp_start = op.grp_start;
@@ -1230,7 +1263,8 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
     smem_set[kv] = smem;
   }
   const uint64_t tile_m = pair ? 2 * kBM : kBM;
-  const uint64_t tiles = ((M + tile_m - 1) / tile_m) * ((Nr + bn - 1) / bn) * units;
+  const uint64_t tiles = ga ? uint64_t{op.n_ga_tiles} * ((Nr + bn - 1) / bn)
+                            : ((M + tile_m - 1) / tile_m) * ((Nr + bn - 1) / bn) * units;
   // pairs: two CTAs per tile, an even grid of whole clusters
   const unsigned grid = pair ? static_cast<unsigned>(std::min<uint64_t>(2 * tiles, n_sms & ~1))
                              : static_cast<unsigned>(std::min<uint64_t>(tiles, n_sms));

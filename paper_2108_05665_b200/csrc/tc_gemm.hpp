@@ -43,6 +43,12 @@ struct TcOp {
   const uint32_t* grp_start;      // n_groups + 1 offsets
   uint32_t n_groups;
   uint32_t slots;
+  // Gather mode (ga_tiles != null): tiles stack 128 / M items sharing a B
+  // entry; ga_tiles = per tile {group, items...}, ga_groups = B entry per group
+  const uint32_t* ga_tiles;
+  uint32_t n_ga_tiles;
+  const uint32_t* ga_groups;
+  uint32_t n_ga_groups;
 };
 
 // Launches the op's kernels on `st`; returns how many.

@@ -55,3 +55,19 @@ def test_cfg2_tensor_core_path_matches_exact_path(engine):
     print(f"tensor cores: max rel {e_tc:.2e}, L2 {l2:.2e}; CUDA cores: max rel {e_cuda:.2e}")
     assert e_tc <= 1e-4 and l2 <= 1e-4
     assert e_cuda <= 1e-4
+
+
+def test_gather_mode_matches_cuda_cores(engine, monkeypatch):
+    """Tensor-core gather mode (node 349: 9,992 items of 32 x 32 x 128 sharing
+    128 B entries, stacked 4 items per 128-row tile) against the same op on
+    the CUDA-core tile kernel (MTCG_NO_GATHER=1), over a slice range."""
+    p, c, bits = workload("cfg2")
+    cp, ga = run_range(engine, p, EvalOptions(precision="c64"), 0, 2)
+    assert any(k[0] == 349 and k[1] == 12 for k in op_kernels(cp)), "node 349 not in gather mode"
+    monkeypatch.setenv("MTCG_NO_GATHER", "1")
+    cp2, plain = run_range(engine, p, EvalOptions(precision="c64"), 0, 2)
+    assert not any(k[0] == 349 and k[1] == 12 for k in op_kernels(cp2))
+    _, exact = run_range(engine, p, EvalOptions(precision="c128"), 0, 2)
+    e_ga, e_plain = rel_err(ga, exact, c.n_qubits), rel_err(plain, exact, c.n_qubits)
+    print(f"gather mode: max rel {e_ga:.2e}; CUDA-core tile: {e_plain:.2e}")
+    assert e_ga <= 1e-4 and np.linalg.norm(ga - exact) / np.linalg.norm(exact) <= 1e-4
