@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], PAIR ? 2 : 32 * p.n_conv);  // PAIR: one arrive per CTA
+      mbar_init(&conv[s], PAIR ? 2 * p.n_conv : 32 * p.n_conv);  // PAIR: one arrive per converter warp
       mbar_init(&empty[s], 1);
     }
     for (uint32_t b = 0; b < n_acc; ++b) {
@@ -740,9 +740,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           if constexpr (PAIR) {
-            // one cluster-scope release per CTA (after all converters' writes)
-            asm volatile("bar.sync 3, %0;" ::"r"(nct) : "memory");
-            if (ct == 0) mbar_arrive_cluster(conv_leader + 8u * static_cast<uint32_t>(st));
+            // one arrive on the leader's barrier per converter warp
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(conv_leader + 8u * static_cast<uint32_t>(st));
           } else {
             mbar_arrive(&conv[st]);
           }
