@@ -96,6 +96,22 @@ __device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
          (uint64_t{1} << 46) | (layout << 61);
 }
 
+// tcgen05.ld without the wait (the caller issues tmem_wait() after all loads)
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -849,12 +865,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int cc = c0 / 2;  // first complex column of this chunk in the tile
         if (p.transpose) {
           uint32_t v[32];
-          tmem_ld32(tacc + c0, v);
-          if (wide) {  // + the Âhi B̂lo half
+          if (wide) {  // + the Âhi B̂lo half: both loads in flight, one wait
             uint32_t w[32];
-            tmem_ld32(tacc + c0 + p.bn, w);
+            tmem_ld32_nowait(tacc + c0, v);
+            tmem_ld32_nowait(tacc + c0 + p.bn, w);
+            tmem_wait();
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(w[j]));
+          } else {
+            tmem_ld32(tacc + c0, v);
           }
           if constexpr (F16) {
 #pragma unroll
@@ -868,7 +887,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
           __syncwarp();
           const int64_t co = coff[cc + (lane & 15)];
-#pragma unroll 4
+#pragma unroll
           for (int e = lane; e < 32 * 16; e += 32) {
             const int row = e >> 4, cj = e & 15;
             const uint64_t row_om = __shfl_sync(0xffffffffu, om, row);
