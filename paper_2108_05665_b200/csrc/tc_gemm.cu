@@ -7,19 +7,28 @@
 // product Ĉ = Â B̂ᵀ is C in interleaved (re, im) layout: 8 real flops per
 // complex MAC, no 4M/3M overhead.
 //
-// fp32 accuracy on TF32 tensor cores: each operand x = hi + lo with
-// hi = rna_tf32(x) and lo = x - hi (exact), and Ĉ = Âhi B̂hi + Âhi B̂lo +
-// Âlo B̂hi (3xTF32; the dropped lo·lo term is < 2^-22 |ab|).
+// fp32 accuracy from 11-bit-significand tensor-core inputs: each operand
+// x = hi + lo, Ĉ = Âhi B̂hi + Âhi B̂lo + Âlo B̂hi (the dropped lo·lo term is
+// < 2^-22 |ab|), either
+//   3xFP16 (kind::f16, 2x the TF32 rate): operands scaled by exact powers of
+//     two from their max |x| (absmax_kernel) into fp16's range, hi/lo fp16,
+//     the epilogue undoes the scales — where A is reused enough that the
+//     extra max pass pays (tc_use_f16);
+//   3xTF32 (kind::tf32): hi = rna_tf32(x), lo = x - hi.
 //
-// Kernel (tc_gemm_persistent): one persistent CTA per SM walks 128 x BN output
-// tiles (BN <= 256 real columns), K in 32-float (128-byte) stages. TMA
-// (SWIZZLE_128B) lands raw A and B̂ hi/lo in an mbarrier-guarded smem ring;
-// converter warps split A into TF32 hi/lo in place; one elected thread issues
-// 3 x 4 tcgen05.mma.kind::tf32 per stage into a ring of TMEM accumulators and
-// tcgen05.commit frees the stage; epilogue warps tcgen05.ld finished
-// accumulators and scatter complex results through the output offset tables
-// (the parent's layout / the root accumulator), optionally accumulating,
-// while the next tiles' main loop runs.
+// Kernel (tc_gemm_persistent<BK, F16, PAIR>): persistent CTAs walk 128 x BN
+// output tiles (BN <= 256 real columns). Warp roles: a TMA producer lands raw
+// A and B̂ hi/lo stages in an mbarrier-guarded smem ring; converter warps split
+// A into hi/lo in place; one converged MMA warp issues the tcgen05.mma chain
+// into a ring of TMEM accumulators and tcgen05.commit frees stages;
+// epilogue warpgroups tcgen05.ld finished accumulators and scatter complex
+// results through the output offset tables (the parent's layout / the root
+// accumulator) while later tiles' main loops run. Modes:
+//   wide (BN <= 128): [B̂hi; B̂lo] as one N = 2 BN operand (2 MMAs per k-step);
+//   grouped: items sharing an A entry form one GEMM (N_eff = slots x N);
+//   gather: small-M items sharing a B entry stack into 128-row tiles;
+//   PAIR (3xFP16, BN = 256): a 2-CTA cluster computes 256-row tiles with
+//     cta_group::2, each CTA loading half of the B̂ tile.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
