@@ -13,8 +13,15 @@
 //                     [kept legs][legs the parent closes]); output written
 //                     through per-tile offset tables, lanes along the output's
 //                     contiguous dimension.
+//   contract_rows[_grouped]  HBM-streaming skinny ops (N <= 16, K <= 32): a
+//                     thread per A row, B in shared memory; grouped: every
+//                     item sharing an A entry reads the row once.
 //   contract_generic  one thread per output element, for items with < 256
-//                     outputs.
+//                     outputs; contract_dot: a warp per output (long K, C64).
+//   chain_kernel      fused operand chains (planner.hpp Chain): a run of
+//                     skinny ops applied to a shared-memory block of the
+//                     running tensor, in the reference's per-step order.
+//   tc_contract       tensor-core ops (tc_gemm.cu).
 //   leaf_root         single-slot networks.
 //   xeb_*             fused |amp|^2 -> compensated fp64 reductions.
 //
