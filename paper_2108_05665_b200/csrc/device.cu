@@ -619,9 +619,9 @@ __device__ __forceinline__ void chain_step(const T* X, T* Y, const T* Bs, const 
   constexpr int K = 1 << KC, G = 1 << GB;
   constexpr bool b_regs = K * G * sizeof(T) <= 64;  // small B tiles in registers
   const int F = 1 << f_bits;
+  // kept legs keep their row positions: in_base[f] is also f's output base
   const uint32_t* in_base = tb;
-  const uint32_t* out_f = tb + F;
-  const uint32_t* out_g = out_f + F;
+  const uint32_t* out_g = tb + F;
   const uint32_t* in_c = out_g + G;
   uint32_t ic[K], og[G];
 #pragma unroll
@@ -637,11 +637,12 @@ __device__ __forceinline__ void chain_step(const T* X, T* Y, const T* Bs, const 
   const int umask = (1 << inner_bits) - 1;
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const int uu = e & umask, f = e >> inner_bits;
-    const T* x = X + uu * pitch + in_base[f];
+    const uint32_t base = uu * pitch + in_base[f];
+    const T* x = X + base;
     T xv[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) xv[c] = x[ic[c]];
-    T* y = Y + uu * pitch + out_f[f];
+    T* y = Y + base;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       T acc = czero<T>();
@@ -694,7 +695,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2)
     const auto& st = d.steps[l];
     const int KG = 1 << (st.kc + st.g_bits);
     if (threadIdx.x < KG) {
-      const uint32_t* boff = st.tbl + (2 << st.f_bits) + (1 << st.g_bits) + (1 << st.kc);
+      const uint32_t* boff = st.tbl + (1 << st.f_bits) + (1 << st.g_bits) + (1 << st.kc);
       const uint64_t b_slice = st.b_sstr ? slice_offset_dev(st.b_sstr, d.s_bits, slice) : 0;
       const T* B = st.b + uint64_t{__ldg(d.entries + uint64_t{d.nb} * (l + 1) + item)} * st.b_item + b_slice;
       Bs[64 * l + threadIdx.x] = B[__ldg(boff + threadIdx.x)];

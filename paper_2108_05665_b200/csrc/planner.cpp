@@ -1087,13 +1087,10 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         // B tile: (closed combo c, opened combo g) at c * G + g, loaded from
         // the entry at boff[c * G + g]
         const uint32_t G = 1u << opened.size(), F = 1u << kept.size();
-        std::vector<uint32_t> in_base(F), out_f(F), out_g(G);
+        std::vector<uint32_t> in_base(F), out_g(G);  // (kept legs keep their positions)
         for (uint32_t f = 0; f < F; ++f)
           for (size_t x = 0; x < kept.size(); ++x)
-            if (f >> x & 1) {
-              in_base[f] += 1u << pos[kept[x]];
-              out_f[f] += 1u << npos[kept[x]];
-            }
+            if (f >> x & 1) in_base[f] += 1u << pos[kept[x]];
         for (uint32_t g = 0; g < G; ++g)
           for (size_t x = 0; x < opened.size(); ++x)
             if (g >> x & 1) out_g[g] += 1u << npos[opened[x]];
@@ -1117,7 +1114,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         }
         st.g_bits = static_cast<int>(opened.size());
         st.f_bits = static_cast<int>(kept.size());
-        for (auto* v : {&in_base, &out_f, &out_g, &in_c, &boff})
+        for (auto* v : {&in_base, &out_g, &in_c, &boff})
           st.tbl.insert(st.tbl.end(), v->begin(), v->end());
         ch.steps.push_back(std::move(st));
         std::vector<uint32_t> next;

@@ -102,17 +102,17 @@ struct Op {
 //   in shared-memory positions [0, 2^q) per untouched-leg combination u;
 //   closed legs free their positions for the legs opened after them.
 constexpr int kMaxChainSteps = 8;
-constexpr int kMaxChainTable = 2 * 256 + 8 + 8 + 64;  // words of one step's tables (q <= 8, K, G <= 8)
+constexpr int kMaxChainTable = 256 + 8 + 8 + 64;  // words of one step's tables (q <= 8, K, G <= 8)
 struct ChainStep {
   int op = -1;                 // op index (B operand, ib, slice strides)
   int kc = 0;
   int g_bits = 0;              // legs the step's B opens
   int f_bits = 0;              // touched legs the step keeps
   uint32_t n_out = 0;          // combos of the active touched legs after the step
-  // in_base[2^f] | out_f[2^f] | out_g[2^g] | in_c[2^kc] | boff[2^(kc + g)]:
-  // row positions of the kept-leg combination f in the input and output
-  // rows, of the opened-leg combination g, of the closed combination c, and
-  // the B tile's element offsets (c * 2^g + g) in the B entry
+  // in_base[2^f] | out_g[2^g] | in_c[2^kc] | boff[2^(kc + g)]: row positions
+  // of the kept-leg combination f (the same in the input and output rows),
+  // of the opened-leg combination g, of the closed combination c, and the B
+  // tile's element offsets (c * 2^g + g) in the B entry
   std::vector<uint32_t> tbl;
   uint64_t tbl_off = 0;        // word offset in the index blob
 };
