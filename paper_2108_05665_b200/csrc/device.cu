@@ -961,7 +961,7 @@ template <class R, int K, int N>
 void launch_rows_grouped_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
   using T = typename V2<R>::T;
   // rows per thread: RPT x K complex of A in registers
-  constexpr int RA = sizeof(R) == 8 ? 16 : (K <= 4 ? 16 : 32);
+  constexpr int RA = sizeof(R) == 8 ? 16 : (K <= 4 || K >= 16 ? 16 : 32);
   constexpr int RPT0 = RA / K;
   constexpr int RPT = RPT0 < 1 ? 1 : (RPT0 > 8 ? 8 : RPT0);
   const size_t smem = sizeof(T) * op.grp_max * K * N + sizeof(uint32_t) * (K + N + op.grp_max);
