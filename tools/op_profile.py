@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--precision", default="c64")
     ap.add_argument("--top", type=int, default=40)
     ap.add_argument("--slice", type=int, default=0)
+    ap.add_argument("--warm", type=int, default=3, help="untimed passes first (0 under ncu)")
     a = ap.parse_args()
     import torch
 
@@ -50,7 +51,7 @@ def main():
     ms = (C.c_float * n)()
     err = C.create_string_buffer(512)
     stream = torch.cuda.current_stream().cuda_stream
-    for _ in range(3):  # warm
+    for _ in range(a.warm):  # warm
         L.mtcg_time_ops(cp.h, a.slice, C.c_void_p(acc.data_ptr()), 0, C.c_void_p(stream), ms, err, 512)
     rows = []
     for i in range(n):
@@ -61,7 +62,7 @@ def main():
                          kernel=oi.kernel, ms=t, bytes=int(oi.bytes), flops=8 * int(oi.mults),
                          gbs=oi.bytes / (t * 1e-3) / 1e9 if t else 0.0,
                          tflops=8 * oi.mults / (t * 1e-3) / 1e12 if t else 0.0))
-    total = sum(r["ms"] for r in rows)
+    total = sum(r["ms"] for r in rows) or 1e-30
     rows.sort(key=lambda r: -r["ms"])
     print(f"slice {a.slice}: {n} ops, {total:.3f} ms serialised")
     print(f"{'node':>5} {'M':>3} {'N':>3} {'K':>3} {'batch':>6} {'cfg':>3} {'ms':>8} "
