@@ -617,38 +617,44 @@ template <class T, int KC, int GB>
 __device__ __forceinline__ void chain_step(const T* X, T* Y, const T* Bs, const uint32_t* tb, int pitch,
                                            int inner_bits, int f_bits) {
   constexpr int K = 1 << KC, G = 1 << GB;
-  constexpr bool b_regs = K * G * sizeof(T) <= 64;  // small B tiles in registers
+  // small B tiles in registers (complex64: up to 4 x 4 — else 16 broadcast
+  // shared loads in a 4 x 4 work item's ~114 instructions)
+  constexpr bool b_regs = K * G * sizeof(T) <= (sizeof(T) == 8 ? 128 : 64);
   const int F = 1 << f_bits;
   // kept legs keep their row positions: in_base[f] is also f's output base
   const uint32_t* in_base = tb;
   const uint32_t* out_g = tb + F;
   const uint32_t* in_c = out_g + G;
+  // byte offsets: one add per shared access (an element index costs an add
+  // and a scale)
   uint32_t ic[K], og[G];
 #pragma unroll
-  for (int c = 0; c < K; ++c) ic[c] = in_c[c];
+  for (int c = 0; c < K; ++c) ic[c] = in_c[c] * static_cast<uint32_t>(sizeof(T));
 #pragma unroll
-  for (int g = 0; g < G; ++g) og[g] = out_g[g];
+  for (int g = 0; g < G; ++g) og[g] = out_g[g] * static_cast<uint32_t>(sizeof(T));
   T br[b_regs ? K * G : 1];
   if constexpr (b_regs) {
 #pragma unroll
     for (int i = 0; i < K * G; ++i) br[i] = Bs[i];
   }
+  const char* const Xb = reinterpret_cast<const char*>(X);
+  char* const Yb = reinterpret_cast<char*>(Y);
   const int n = F << inner_bits;
   const int umask = (1 << inner_bits) - 1;
   for (int e = threadIdx.x; e < n; e += blockDim.x) {
     const int uu = e & umask, f = e >> inner_bits;
-    const uint32_t base = uu * pitch + in_base[f];
-    const T* x = X + base;
+    const uint32_t base = (uu * pitch + in_base[f]) * static_cast<uint32_t>(sizeof(T));
+    const char* x = Xb + base;
     T xv[K];
 #pragma unroll
-    for (int c = 0; c < K; ++c) xv[c] = x[ic[c]];
-    T* y = Y + base;
+    for (int c = 0; c < K; ++c) xv[c] = *reinterpret_cast<const T*>(x + ic[c]);
+    char* y = Yb + base;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       T acc = czero<T>();
 #pragma unroll
       for (int c = 0; c < K; ++c) cmac(acc, xv[c], b_regs ? br[c * G + g] : Bs[c * G + g], c == 0);
-      y[og[g]] = acc;
+      *reinterpret_cast<T*>(y + og[g]) = acc;
     }
   }
 }
@@ -675,7 +681,7 @@ __device__ __forceinline__ void chain_step_any(int kc, int gb, const T* X, T* Y,
 // contracted and stored (the load latency is the kernel's critical path; a
 // block per chunk left most blocks outside their load phase).
 template <class R>
-__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2)
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
     chain_kernel(const __grid_constant__ ChainDev<typename V2<R>::T> d) {
   using T = typename V2<R>::T;
   extern __shared__ __align__(16) uint8_t chain_smem[];
@@ -725,12 +731,21 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2)
       if (8 + i < bits && (u >> i & 1)) x += tab[8 + i];
     return x;
   };
+  // the per-u parts of the maps are the same for every chunk: once
+  uint32_t hlo[kU], hlp[kU], hso[kU], hsp[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    hlo[u] = lo + hi(d.ld_o, d.ld_bits, u);
+    hlp[u] = lp + hi(d.ld_p, d.ld_bits, u);
+    hso[u] = so + hi(d.st_o, d.st_bits, u);
+    hsp[u] = sp + hi(d.st_p, d.st_bits, u);
+  }
   T v[kU];
   auto fetch = [&](uint64_t outer) {
-    const T* A = Aitem + d.tu_in(outer) + lo;
+    const T* A = Aitem + d.tu_in(outer);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_ld) v[u] = A[hi(d.ld_o, d.ld_bits, u)];
+      if (threadIdx.x + 256 * u < d.n_ld) v[u] = A[hlo[u]];
   };
   fetch(outer0);
   const int n_chunks = 1 << d.cpb_bits;
@@ -738,7 +753,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2)
     __syncthreads();  // the previous chunk's results are stored
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_ld) X0[lp + hi(d.ld_p, d.ld_bits, u)] = v[u];
+      if (threadIdx.x + 256 * u < d.n_ld) X0[hlp[u]] = v[u];
     if (k + 1 < n_chunks) fetch(outer0 + k + 1);  // in flight during the steps
     T* X = X0;
     T* Y = Y0;
@@ -751,10 +766,10 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 4 : 2)
       Y = t;
     }
     __syncthreads();
-    T* O = Oitem + d.tu_out(outer0 + k) + so;
+    T* O = Oitem + d.tu_out(outer0 + k);
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_st) O[hi(d.st_o, d.st_bits, u)] = X[sp + hi(d.st_p, d.st_bits, u)];
+      if (threadIdx.x + 256 * u < d.n_st) O[hso[u]] = X[hsp[u]];
   }
 }
 
