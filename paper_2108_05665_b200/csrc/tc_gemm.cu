@@ -896,19 +896,34 @@ __global__ void __launch_bounds__(kPThreads, 1)
           for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
           __syncwarp();
           const int64_t co = coff[cc + (lane & 15)];
+          // 8 shared reads and row offsets first, then the 8 stores back
+          // to back (twice): interleaved, every shared read waited on the
+          // previous global store (the compiler cannot rule out that p.out
+          // aliases the staging buffer), ~100 cycles per element
 #pragma unroll
-          for (int e = lane; e < 32 * 16; e += 32) {
-            const int row = e >> 4, cj = e & 15;
-            const uint64_t row_om = __shfl_sync(0xffffffffu, om, row);
-            if (row_om == ~uint64_t{0} || co < 0) continue;
-            float2 val = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
-            float2* dst = p.out + co + row_om;
-            if (accumulate) {
-              const float2 old = *dst;
-              val.x += old.x;
-              val.y += old.y;
+          for (int h = 0; h < 2; ++h) {
+            float2 vals[8];
+            uint64_t roms[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int e = lane + 32 * (8 * h + i);
+              const int row = e >> 4, cj = e & 15;
+              roms[i] = __shfl_sync(0xffffffffu, om, row);
+              vals[i] = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
             }
-            *dst = val;
+            if (co < 0) continue;
+            if (accumulate) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (roms[i] != ~uint64_t{0}) {
+                  const float2 old = p.out[co + roms[i]];
+                  vals[i].x += old.x;
+                  vals[i].y += old.y;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (roms[i] != ~uint64_t{0}) p.out[co + roms[i]] = vals[i];
           }
           __syncwarp();
           continue;
