@@ -644,6 +644,90 @@ def grid_circuit(rows: int, cols: int, layers: int, seed: int) -> Circuit:
     return c
 
 
+# The 54-site Sycamore layout (rows of a rotated square lattice; '#' = a
+# qubit): site (r, c) couples to (r+1, c) and (r, c+1) when both exist.
+SYCAMORE_ROWS = (
+    "-----##---",
+    "----####--",
+    "---######-",
+    "--########",
+    "-#########",
+    "#########-",
+    "-#######--",
+    "--#####---",
+    "---###----",
+    "----#-----",
+)
+# the site left out of the 53-qubit layout (a synthetic-workload convention;
+# it is a degree-2 corner site, so 86 of the 88 couplers remain)
+SYCAMORE_DROPPED = (0, 6)
+SYCAMORE_PATTERN = "ABCDCDAB"
+
+
+def sycamore_sites(n_qubits: int = 53) -> List[Tuple[int, int]]:
+    """Qubit index -> (row, col), row-major over the layout."""
+    sites = [(r, c) for r, row in enumerate(SYCAMORE_ROWS) for c, ch in enumerate(row) if ch == "#"]
+    if n_qubits == 53:
+        sites.remove(SYCAMORE_DROPPED)
+    elif n_qubits != 54:
+        raise DataError("Sycamore layout has 53 or 54 qubits")
+    return sites
+
+
+def sycamore_layer(sites: Sequence[Tuple[int, int]], pattern: str) -> List[Tuple[int, int]]:
+    """Coupler layer A/B/C/D as qubit-index pairs: A, B = vertical couplers
+    (r, c)-(r+1, c) with (r + c) even / odd; C, D = horizontal couplers
+    (r, c)-(r, c+1) with (r + c) odd / even. Each layer is a matching and the
+    four together cover every coupler once."""
+    index = {s: i for i, s in enumerate(sites)}
+    vertical = pattern in "AB"
+    parity = {"A": 0, "B": 1, "C": 1, "D": 0}[pattern]
+    pairs = []
+    for (r, c), i in sorted(index.items(), key=lambda kv: kv[1]):
+        if (r + c) % 2 != parity:
+            continue
+        j = index.get((r + 1, c) if vertical else (r, c + 1))
+        if j is not None:
+            pairs.append((i, j))
+    return pairs
+
+
+def sycamore_circuit(cycles: int, seed: int, n_qubits: int = 53) -> Circuit:
+    """Synthetic Sycamore supremacy-style circuit (BASELINE configs 3-5):
+    `cycles` cycles of a random single-qubit moment ({x_1_2, y_1_2, hz_1_2},
+    never the same gate twice in a row on a qubit) followed by fSim(pi/2,
+    pi/6) on the couplers of layer ABCDCDAB[cycle % 8], then a final
+    single-qubit moment. Randomness from the reference's splitmix64 Rng, as
+    grid_circuit (gen.cpp:54-95) draws it; gate set and fSim angles as
+    grid_circuit's."""
+    rng = Rng(seed)
+    sites = sycamore_sites(n_qubits)
+    layers = {p: sycamore_layer(sites, p) for p in "ABCD"}
+    one_q = ["x_1_2", "y_1_2", "hz_1_2"]
+    c = Circuit(len(sites))
+    last = [-1] * len(sites)
+    moment = 0
+
+    def single_qubit_moment():
+        for q in range(c.n_qubits):
+            if last[q] < 0:
+                g = rng.uniform_index(3)
+            else:
+                g = rng.uniform_index(2)
+                g += g >= last[q]  # skip the previous gate
+            last[q] = g
+            c.gates.append(Gate(moment, one_q[g], q))
+
+    for cycle in range(cycles):
+        single_qubit_moment()
+        moment += 1
+        for a, b in layers[SYCAMORE_PATTERN[cycle % len(SYCAMORE_PATTERN)]]:
+            c.gates.append(Gate(moment, "fs", a, b, math.pi / 2, math.pi / 6))
+        moment += 1
+    single_qubit_moment()
+    return c
+
+
 def random_bitstrings(rng: Rng, n_qubits: int, count: int) -> List[str]:
     """gen.cpp:97-107"""
     out = []

@@ -99,3 +99,65 @@ def test_generators_match_reference():
     assert refimpl.random_bitstrings(99, 30, 64) == N.random_bitstrings(N.Rng(99), 30, 64)
     for s in range(20):
         assert refimpl.random_circuit(s, 5, 18) == N.format_circuit(N.random_circuit(N.Rng(s), 5, 18))
+
+
+def test_sycamore_layout_and_cycle_pattern():
+    # BASELINE configs 3-5: the 53-qubit Sycamore layout (86 couplers; 88 with
+    # all 54 sites), layers A-D partition the couplers into matchings, cycle i
+    # uses layer ABCDCDAB[i % 8], fSim(pi/2, pi/6), single-qubit gates never
+    # repeat on a qubit, and a final single-qubit moment closes the circuit
+    for n, n_couplers in [(53, 86), (54, 88)]:
+        sites = N.sycamore_sites(n)
+        assert len(sites) == n == len(set(sites))
+        layers = {p: N.sycamore_layer(sites, p) for p in "ABCD"}
+        every = [tuple(sorted(e)) for p in "ABCD" for e in layers[p]]
+        assert len(every) == len(set(every)) == n_couplers
+        for p, pairs in layers.items():
+            used = [q for e in pairs for q in e]
+            assert len(used) == len(set(used)), p  # a matching
+            for a, b in pairs:
+                (ra, ca), (rb, cb) = sites[a], sites[b]
+                assert abs(ra - rb) + abs(ca - cb) == 1
+    with pytest.raises(DataError):
+        N.sycamore_sites(50)
+    m = 12
+    c = N.sycamore_circuit(m, 12345)
+    assert c.n_qubits == 53
+    sites = N.sycamore_sites(53)
+    moments = {}
+    for g in c.gates:
+        moments.setdefault(g.moment, []).append(g)
+    assert sorted(moments) == list(range(2 * m + 1))
+    prev = [None] * 53
+    for t in range(2 * m + 1):
+        gs = moments[t]
+        if t % 2 == 0:  # single-qubit moment over every qubit
+            assert sorted(g.q0 for g in gs) == list(range(53))
+            for g in gs:
+                assert g.name in ("x_1_2", "y_1_2", "hz_1_2") and g.name != prev[g.q0]
+                prev[g.q0] = g.name
+        else:
+            want = N.sycamore_layer(sites, "ABCDCDAB"[(t // 2) % 8])
+            assert [(g.q0, g.q1) for g in gs] == want
+            assert all(g.name == "fs" and g.p0 == pytest.approx(np.pi / 2) and
+                       g.p1 == pytest.approx(np.pi / 6) for g in gs)
+    # round trip through the reference's circuit text format
+    assert N.format_circuit(N.parse_circuit(N.format_circuit(c))) == N.format_circuit(c)
+    # deterministic in the seed
+    assert N.format_circuit(N.sycamore_circuit(m, 12345)) == N.format_circuit(c)
+    assert N.format_circuit(N.sycamore_circuit(m, 1)) != N.format_circuit(c)
+
+
+@pytest.mark.skipif(not refimpl.available(), reason="reference build absent (GPU box)")
+def test_sycamore_circuit_consumed_by_reference():
+    # the reference's loader builds the same fused 53-qubit network (311
+    # slots, 516 closed legs at m = 12) and the same leaves, bit for bit
+    c = N.format_circuit(N.sycamore_circuit(12, 12345))
+    bits = N.random_bitstrings(N.Rng(99), 53, 8)
+    rp = refimpl.RefProblem(c, bits, None, fuse=True)
+    d = N.to_diagram(N.parse_circuit(c), True)
+    assert (d.slot_count, d.n_closed) == (rp.n_slots, rp.n_closed) == (311, 516)
+    for j in range(d.slot_count):
+        legs, data = rp.slot_tensor(j)
+        assert legs == d.slot_tensors[j].legs
+        assert np.array_equal(data.view(np.float64), d.slot_tensors[j].data.view(np.float64))
