@@ -315,8 +315,45 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
         ceiling = peak / (6.0 if tf32 else 3.0)
         scheme = {"scheme": "3xTF32" if tf32 else "3xFP16 (power-of-2 scaled fp16 hi/lo)",
                   "scheme_ceiling": ceiling, "frac_of_scheme_ceiling": achieved / ceiling}
+    # The whole slice against SURVEY §8(d)'s roofline: T_roof = sum over ops of
+    # max(F_n / P_cplx, B_n / BW), F_n and B_n the reference's algorithmic
+    # flops (8 per complex MAC) and bytes (rw x 8 B), P_cplx the 3xFP16
+    # scheme ceiling, BW the measured copy peak. Fused-chain members launch
+    # nothing of their own (0 ms): their work is charged to the chain's tail.
+    p_cplx = tensor_tflops * 1e12 / 3.0
+    bw = hbm_gbs * 1e9
+    t_roof = 0.0
+    cls = {"tensor": [0.0, 0.0, 0.0, 0], "hbm": [0.0, 0.0, 0.0, 0]}  # t_roof, ms, work, ops
+    pend_f = pend_b = 0.0
+    for m, oi in ops:
+        f = 8.0 * oi.mults + pend_f
+        b = float(oi.bytes) + pend_b
+        if m <= 0.0:
+            pend_f, pend_b = f, b
+            continue
+        pend_f = pend_b = 0.0
+        tf, tb = f / p_cplx, b / bw
+        t_roof += max(tf, tb)
+        c = cls["tensor" if tf > tb else "hbm"]
+        c[0] += max(tf, tb)
+        c[1] += m * 1e-3
+        c[2] += f if tf > tb else b
+        c[3] += 1
+    path = {
+        "t_roof_ms": t_roof * 1e3, "t_meas_ms": slice_ms, "frac": t_roof * 1e3 / slice_ms,
+        "p_cplx_tflops": p_cplx / 1e12, "bw_gbs": hbm_gbs,
+        "tensor_bound_ops": cls["tensor"][3],
+        "tensor_bound_frac_of_scheme_ceiling": cls["tensor"][0] / cls["tensor"][1] if cls["tensor"][1] else None,
+        "tensor_bound_tflops": cls["tensor"][2] / cls["tensor"][1] / 1e12 if cls["tensor"][1] else None,
+        "hbm_bound_ops": cls["hbm"][3],
+        "hbm_bound_frac": cls["hbm"][0] / cls["hbm"][1] if cls["hbm"][1] else None,
+        "note": ("per slice (slice 0, ops serialised with CUDA events); algorithmic bytes "
+                 "count an operand once per item, so grouped ops (A shared by a group) can "
+                 "exceed the copy peak — measured DRAM bytes per op: profiles/r01/op_traffic.txt"),
+    }
     return {
         **scheme,
+        "path": path,
         "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
         "frac": achieved / peak, "traffic": traffic,
         "kernel": (f"node {top.node}: M=2^{top.fa} N=2^{top.fb} K=2^{top.kc} x{top.batch} "
