@@ -1202,7 +1202,30 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
   const T* leaves = static_cast<const T*>(dp.d_leaves);
   T* acc = static_cast<T*>(d_acc);
   auto sstr = [&](int64_t off) -> const uint64_t* { return off < 0 ? nullptr : dp.d_sstr + off; };
-  for (size_t oi = op0; oi < std::min(op1, c.ops.size()); ++oi) {
+  // Split-integer tensor-core ops whose A table is slice-invariant (slice
+  // reuse): their A rows are quantized in place once, right after the
+  // prologue (tc_quantize_a), not in every slice.
+  const size_t n_pro = c.n_prologue_ops;
+  auto prequant = [&](cudaStream_t st) {
+    if constexpr (sizeof(R) == 4) {
+      for (size_t j = n_pro; j < c.ops.size(); ++j) {
+        const Op& q = c.ops[j];
+        if (!q.a_prequant || q.nb == 0 || q.config != kTcConfig) continue;
+        TcOp t{};
+        t.node = q.node;
+        t.fa = q.fa;
+        t.fb = q.fb;
+        t.kc = q.kc;
+        t.a_entries = q.a_entries;
+        t.a = reinterpret_cast<const float*>(arena + q.a_base);
+        t.row_exp = reinterpret_cast<int8_t*>(arena + q.row_exp_off);
+        dp.engine->launches += tc_quantize_a(t, st);
+      }
+    }
+  };
+  const size_t op_end = std::min(op1, c.ops.size());
+  for (size_t oi = op0; oi < op_end; ++oi) {
+    if (n_pro && oi == n_pro && op0 < n_pro && !dag) prequant(st_main);
     const Op& op = c.ops[oi];
     if (op.nb == 0) continue;
     if (op.chain >= 0 && !op.chain_tail) continue;  // evaluated by its chain's tail
@@ -1289,6 +1312,10 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
         t.bhat_hi = reinterpret_cast<float*>(arena + op.scratch_off);
         t.bhat_lo = reinterpret_cast<float*>(arena + op.scratch_off + bhat_elems);
         t.partials = reinterpret_cast<uint32_t*>(arena + op.scratch_off + 2 * bhat_elems);
+        t.col_exp = reinterpret_cast<int8_t*>(arena + op.scratch_off + 2 * bhat_elems + 4096 / sizeof(T));
+        t.row_exp = op.a_prequant ? reinterpret_cast<int8_t*>(arena + op.row_exp_off)
+                                  : t.col_exp + (units << op.fb);
+        t.quantize_a = !op.a_prequant;
         t.out = reinterpret_cast<float2*>(d.out);
         t.out_rows = d.out_rows;
         t.out_item = op.out_item;
@@ -1312,6 +1339,7 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
     if (dag) dag->end(oi);
   }
   if (dag) dag->join();
+  if (n_pro && op_end == n_pro && op0 < n_pro) prequant(st_main);
   const cudaStream_t st = st_main;
   if (c.has_leaf_root && c.n_rows > 0) {
     const LeafRoot& lr = c.leaf_root;

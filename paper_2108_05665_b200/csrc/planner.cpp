@@ -904,8 +904,15 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       const uint64_t units = !op.ga_groups.empty() ? uint64_t{op.ga_groups.size()}
                              : op.grp_max ? uint64_t{op.grp_start.size() - 1} * op.grp_max : op.nb;
       const uint64_t bhat = units << (op.fb + op.kc + 1);
-      // B̂ hi / lo (A is split in shared memory) + 4 KB of operand-max partials
-      op.scratch_elems = 2 * bhat + 4096 / c.elem_bytes;
+      // B̂ hi / lo (3xFP16 / 3xTF32; the split-integer digit planes use both)
+      // + 4 KB of operand-max partials + the split-integer column exponents
+      // (one byte per B̂ column pair) and A row exponents (one per A row)
+      const uint64_t col_exps = units << op.fb, row_exps = op.a_entries << op.fa;
+      // (kc > 5: A rows quantized by a pre-pass, tc_i8_prequant)
+      op.a_prequant = invariant[op.child_a] && !invariant[node] && op.kc > 5;
+      op.scratch_elems = 2 * bhat + 4096 / c.elem_bytes +
+                         (col_exps + (op.a_prequant ? 0 : row_exps) + c.elem_bytes) / c.elem_bytes + 1;
+      if (op.a_prequant) op.row_exp_off = alloc((row_exps + c.elem_bytes - 1) / c.elem_bytes, node);
       if (op.scratch_elems <= private_elems) {
         scratch_private.push_back(c.ops.size());
         op.scratch_off = private_top;

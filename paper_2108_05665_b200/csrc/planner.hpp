@@ -72,6 +72,11 @@ struct Op {
   uint64_t a_entries = 0;          // tensor-core path: entries in A's table
   uint64_t scratch_off = 0;        // tensor-core path: arena scratch (elements)
   uint64_t scratch_elems = 0;
+  // tensor-core split-integer path, slice reuse: the A table is slice-
+  // invariant and its rows are quantized once by the prologue (K > 32
+  // complex); the row exponents then live at row_exp_off (never released)
+  bool a_prequant = false;
+  uint64_t row_exp_off = 0;
   bool a_kcontig = false;          // A rows are K-contiguous (tak(k) == k)
   bool o_ncontig = false;          // output n index is contiguous (ton(n) == n)
   bool o_mcontig = false;          // output m bit 0 has stride 1

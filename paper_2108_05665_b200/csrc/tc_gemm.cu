@@ -42,6 +42,7 @@
 #include <string>
 #include <vector>
 
+#include "device.hpp"
 #include "tc_gemm.hpp"
 
 namespace mtcg {
@@ -323,6 +324,10 @@ struct TcParams {
   const uint32_t* grp_start;
   int slots;
   int fb;
+  // split-integer path: row exponents of A (pre-quantized rows: a_entry * M +
+  // m) and column exponents of B̂ (unit * Nr / 2 + complex column)
+  const int8_t* sa;
+  const int8_t* sb;
 };
 
 // Role timestamps of CTA 0's first kTraceTiles tiles (MTCG_TC_TRACE=<node>).
@@ -999,6 +1004,588 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
 }
 
+// ---- split-integer GEMM (3 int8 digits, exact s32 accumulation; default) --------
+//
+// The tensor core's fp32 accumulator truncates (round toward zero) on every
+// MMA, so a K-long fp32-accumulated product shrinks systematically by ~2^-24
+// per accumulated MMA (cfg2: amplitude scale -1.76e-5 under 3xFP16, 17x the
+// F_XEB gate of BASELINE §3; tools/bias_sweep.sh). Integer MMAs accumulate
+// exactly. Each operand row (A: per row over K; B: per column n over K) is
+// scaled by an exact power of two 2^s so that its max |x| 2^s lies in
+// [2^21, 2^22), rounded to the nearest integer X (unbiased) and split into
+// balanced base-256 digits X = 2^16 d0 + 2^8 d1 + d2 (d1, d2 in [-128, 127],
+// d0 in [-64, 64]): the bytes of X + 0x808080, each XOR 0x80. Then
+//   Σ_k X Y = 2^32 acc0 + 2^24 acc1 + 2^16 acc2 + (dropped: 2^8 (d1 g2 + d2 g1) + d2 g2)
+//   acc0 = Σ d0 g0, acc1 = Σ d0 g1 + d1 g0, acc2 = Σ d0 g2 + d1 g1 + d2 g0
+// with 6 kind::i8 MMAs per 32-deep k-step into three s32 TMEM accumulators
+// (exact), combined in fp32 round-to-nearest in the epilogue. The dropped
+// terms are zero-mean (balanced digits), 2^-20 of each product. Same tensor
+// time as 3xFP16 (i8 runs at twice the f16 rate) with no systematic error.
+// Rows of A are scaled by a pre-pass (K > 32 complex: quantize_rows_kernel
+// turns each A row into its three digit planes in place, [d0 | d1 | d2 | -]
+// per row, plus the row exponent) or, for whole-K stages (K <= 32 complex),
+// by the converter warps in shared memory; B̂ is built as digit planes with
+// per-column exponents (build_bhat_i8_kernel).
+constexpr int kI8Kb = 64;    // K bytes (= int8 elements) per stage row: 2 k-steps of 32
+constexpr int kSaRing = 32;  // whole-K mode: row-exponent ring slots (tiles)
+
+__device__ __forceinline__ int i8_scale_exp(float mx) {
+  if (!(mx > 0.f)) return 0;
+  const int e = static_cast<int>((__float_as_uint(mx) >> 23) & 0xFFu) - 127;  // mx in [2^e, 2^(e+1))
+  return max(-125, min(125, 21 - e));
+}
+
+// X + 0x808080 for X = rn(x * scale), |x * scale| <= 2^22: the magic-number
+// rounding (1.5 * 2^23 + X has ulp 1) in one FFMA.
+__device__ __forceinline__ uint32_t i8_biased(float x, float scale) {
+  return __float_as_uint(fmaf(x, scale, 12582912.0f)) - 0x4ABF7F80u;
+}
+
+// Digit words of 4 consecutive elements: w[p] byte j = digit p of element j.
+__device__ __forceinline__ void i8_pack4(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t& w0,
+                                         uint32_t& w1, uint32_t& w2) {
+  const uint32_t lo = __byte_perm(v0, v1, 0x5140), hi = __byte_perm(v2, v3, 0x5140);
+  w2 = __byte_perm(lo, hi, 0x5410) ^ 0x80808080u;  // least significant digits
+  w1 = __byte_perm(lo, hi, 0x7632) ^ 0x80808080u;
+  w0 = __byte_perm(__byte_perm(v0, v1, 0x0062), __byte_perm(v2, v3, 0x6200), 0x7610) ^ 0x80808080u;
+}
+
+// 32 real columns of the three accumulators at tcol (+ bn, + 2 bn), combined:
+// v = acc0 2^16 + acc1 2^8 + acc2 (fp32, one rounding at the end).
+__device__ __forceinline__ void i8_load_combine(uint32_t tcol, int bn, float (&v)[32]) {
+  uint32_t a0[32], a1[32], a2[32];
+  tmem_ld32_nowait(tcol, a0);
+  tmem_ld32_nowait(tcol + bn, a1);
+  tmem_ld32_nowait(tcol + 2 * bn, a2);
+  tmem_wait();
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    v[j] = fmaf(__int2float_rn(static_cast<int>(a0[j])), 65536.f,
+                fmaf(__int2float_rn(static_cast<int>(a1[j])), 256.f, __int2float_rn(static_cast<int>(a2[j]))));
+}
+
+// One stage (2 k-steps) of the 3-digit product: per k-step acc0 += A0 B0,
+// acc1 += A0 B1 + A1 B0, acc2 += A0 B2 + A1 B1 + A2 B0 (accumulators
+// interleaved so consecutive MMAs are independent). a / b: descriptors of
+// plane 0; planes are pa / pb bytes apart (>> 4 in the descriptor).
+template <bool PAIR>
+__device__ __forceinline__ void mma_stage_i8(uint32_t d, uint32_t bn, uint64_t a, uint64_t b, uint32_t pa,
+                                             uint32_t pb, uint32_t idesc, uint32_t acc) {
+  const uint64_t a1 = a + (pa >> 4), a2 = a + 2 * (pa >> 4);
+  const uint64_t b1 = b + (pb >> 4), b2 = b + 2 * (pb >> 4);
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    const uint64_t o = 2 * ks;  // 32 bytes further along the swizzled row
+    const uint32_t f = ks ? 1u : acc;
+    if constexpr (PAIR) {
+      asm volatile(
+          "{\n\t.reg .pred e, p;\n\t"
+          "setp.ne.b32 p, %10, 0;\n\t"
+          "elect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %3, %6, %9, p;\n\t"
+          "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %3, %7, %9, p;\n\t"
+          "@e tcgen05.mma.cta_group::2.kind::i8 [%2], %3, %8, %9, p;\n\t"
+          "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %4, %6, %9, 1;\n\t"
+          "@e tcgen05.mma.cta_group::2.kind::i8 [%2], %4, %7, %9, 1;\n\t"
+          "@e tcgen05.mma.cta_group::2.kind::i8 [%2], %5, %6, %9, 1;\n\t}" ::"r"(d),
+          "r"(d + bn), "r"(d + 2 * bn), "l"(a + o), "l"(a1 + o), "l"(a2 + o), "l"(b + o), "l"(b1 + o),
+          "l"(b2 + o), "r"(idesc), "r"(f));
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred e, p;\n\t"
+          "setp.ne.b32 p, %10, 0;\n\t"
+          "elect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %3, %6, %9, p;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%1], %3, %7, %9, p;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%2], %3, %8, %9, p;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%1], %4, %6, %9, 1;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%2], %4, %7, %9, 1;\n\t"
+          "@e tcgen05.mma.cta_group::1.kind::i8 [%2], %5, %6, %9, 1;\n\t}" ::"r"(d),
+          "r"(d + bn), "r"(d + 2 * bn), "l"(a + o), "l"(a1 + o), "l"(a2 + o), "l"(b + o), "l"(b1 + o),
+          "l"(b2 + o), "r"(idesc), "r"(f));
+    }
+  }
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ float pow2f_wide(int s) { return __int_as_float((max(-126, min(127, s)) + 127) << 23); }
+
+// QA: A is pre-quantized (three digit planes per row, map_a 3-D {Kr, rows,
+// plane}); otherwise map_a is the raw fp32 A (2-D, 32-float boxes) and the
+// whole K (<= 64 floats) of a tile is one stage, split by the converter warps
+// (one row per thread: row max -> exponent -> digits, in place).
+// map_b: B̂ digit planes, 3-D {Kr_pad, units * Nr, plane}.
+// PAIR: M = 256 tiles over a CTA pair (cta_group::2), each CTA loading its 128
+// A rows and half of the B̂ tile. Epilogue: two warpgroups; with a single
+// accumulator buffer (bn = 128: 3 x 128 TMEM columns) both drain every tile
+// (alternate 32-column chunks), otherwise they take alternate tiles.
+template <bool PAIR, bool QA>
+__global__ void __launch_bounds__(kPThreads, 1)
+    tc_i8_persistent(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                     const TcParams p, int n_stages) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const uint32_t cta0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const uint32_t ncta = PAIR ? gridDim.x / 2 : gridDim.x;
+  constexpr int kTM = PAIR ? 2 * kBM : kBM;
+  const int m_off = static_cast<int>(rank) * kBM;
+  const int bn_cta = PAIR ? p.bn / 2 : p.bn;
+  constexpr int kPlaneA = kBM * kI8Kb;                          // 8 KB per digit plane
+  constexpr int a_span = QA ? 3 * kPlaneA : 2 * kBM * 128;      // raw: two 128 x 32-float halves
+  const int plane_b = bn_cta * kI8Kb;
+  const int stage_bytes = a_span + 3 * plane_b;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + n_stages * stage_bytes);
+  uint64_t* conv = full + kMaxStages;
+  uint64_t* empty = conv + kMaxStages;
+  uint64_t* acc_full = empty + kMaxStages;
+  uint64_t* acc_empty = acc_full + kMaxAcc;
+  uint64_t* sa_full = acc_empty + kMaxAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sa_full + kSaRing);
+  uint32_t* ton_s = tmem_slot + 4;
+  const int n_item_cols = p.slots ? (1 << p.fb) : p.Nr / 2;
+  int64_t* coff_s = reinterpret_cast<int64_t*>(ton_s + ((min(n_item_cols, kMaxTonCache) + 3) & ~3));
+  float* cs_s = reinterpret_cast<float*>(coff_s + kEpiGroups * (kMaxBn / 2));
+  int8_t* sa_ring = reinterpret_cast<int8_t*>(cs_s + kEpiGroups * (kMaxBn / 2));
+  float* stage_out = reinterpret_cast<float*>(sa_ring + kSaRing * kBM);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int accumulate = p.root ? static_cast<int>(__ldg(p.cur + 1)) : 0;
+  const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
+  const uint32_t tiles_m = p.ga_per ? p.nb_ga_tiles : (p.M + kTM - 1) / kTM;
+  const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
+  const int k_stages = QA ? p.Kr / kI8Kb : 1;
+  const uint32_t buf_cols = 3 * p.bn;
+  const uint32_t n_acc = min(static_cast<uint32_t>(kMaxAcc), 512u / buf_cols);
+  const bool split = n_acc == 1;  // both epilogue groups drain every tile
+  constexpr int n_epi = kEpiGroups;
+  const bool ton_cached = n_item_cols <= kMaxTonCache;
+  if (ton_cached)
+    for (int n = threadIdx.x; n < n_item_cols; n += blockDim.x) ton_s[n] = p.ton(n);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < n_stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], PAIR ? 2 * p.n_conv : 32 * p.n_conv);
+      mbar_init(&empty[s], 1);
+    }
+    const uint32_t epi_arrivals = (PAIR ? 8u : 128u) * (split ? n_epi : 1u);
+    for (uint32_t b = 0; b < n_acc; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], epi_arrivals);
+    }
+    for (int s = 0; s < kSaRing; ++s) mbar_init(&sa_full[s], max(1, p.n_conv));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(tmem_slot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if constexpr (PAIR)
+    cluster_sync_all();
+  else
+    __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  struct TileWalk {
+    uint32_t n, m, u, dn, dm, du, tn, tm;
+    __device__ void init(uint64_t t0, uint64_t step, uint32_t tn_, uint32_t tm_) {
+      tn = tn_;
+      tm = tm_;
+      n = static_cast<uint32_t>(t0 % tn);
+      m = static_cast<uint32_t>((t0 / tn) % tm);
+      u = static_cast<uint32_t>(t0 / (uint64_t{tn} * tm));
+      dn = static_cast<uint32_t>(step % tn);
+      dm = static_cast<uint32_t>((step / tn) % tm);
+      du = static_cast<uint32_t>(step / (uint64_t{tn} * tm));
+    }
+    __device__ void advance() {
+      n += dn;
+      uint32_t c = n >= tn;
+      n -= c ? tn : 0u;
+      m += dm + c;
+      c = m >= tm;
+      m -= c ? tm : 0u;
+      u += du + c;
+    }
+  };
+  // A entry of a unit (its first item's)
+  auto unit_a_entry = [&](uint32_t u) -> uint32_t {
+    const uint32_t first = p.slots ? __ldg(p.grp_items + __ldg(p.grp_start + u)) : u;
+    return p.ia ? __ldg(p.ia + first) : first;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer ----
+      Ring rg;
+      uint32_t cached_item = ~0u, a_entry = 0;
+      uint64_t pit = 0;
+      TileWalk w;
+      w.init(cta0, ncta, tiles_n, tiles_m);
+      const uint32_t a_box_bytes = QA ? kPlaneA : kBM * 128u;
+      const int raw_halves = p.Kr > 32 ? 2 : 1;
+      for (uint64_t t = cta0; t < tiles; t += ncta, ++pit, w.advance()) {
+        const uint32_t item = w.u;
+        const int m0 = static_cast<int>(w.m) * kTM + m_off;
+        const int n0 = static_cast<int>(w.n) * p.bn + static_cast<int>(rank) * bn_cta;
+        trace(p, pit, 0);
+        if (item != cached_item) {
+          cached_item = item;
+          a_entry = unit_a_entry(item);
+        }
+        int a_row0 = static_cast<int>(a_entry * static_cast<uint64_t>(p.M)) + m0;
+        int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
+        int ga_rows[4] = {0, 0, 0, 0};
+        if (p.ga_per) {
+          const uint32_t* tl = p.ga_tiles + static_cast<uint64_t>(w.m) * (1 + p.ga_per);
+          b_row0 = static_cast<int>(__ldg(tl) * static_cast<uint64_t>(p.Nr)) + n0;
+          for (int k = 0; k < p.ga_per; ++k) {
+            uint32_t itk = __ldg(tl + 1 + k);
+            if (itk == ~0u) itk = __ldg(tl + 1);
+            ga_rows[k] = static_cast<int>(__ldg(p.ia + itk) * static_cast<uint64_t>(p.M));
+          }
+        }
+        for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
+          const int st = rg.slot;
+          if (rg.round > 0) mbar_wait(&empty[st], (rg.round - 1) & 1);
+          uint8_t* sp = base + st * stage_bytes;
+          const uint32_t a_bytes = QA ? 3 * a_box_bytes : raw_halves * a_box_bytes;
+          mbar_expect_tx(&full[st], a_bytes + 3 * plane_b);
+          if constexpr (QA) {  // digit plane pl of a row at byte pl * Kr of it
+            for (int pl = 0; pl < 3; ++pl) {
+              if (p.ga_per) {  // M rows per item
+                for (int k = 0; k < p.ga_per; ++k)
+                  tma_load_2d(sp + pl * kPlaneA + k * p.M * kI8Kb, &map_a, &full[st], pl * p.Kr + s * kI8Kb,
+                              ga_rows[k]);
+              } else {
+                tma_load_2d(sp + pl * kPlaneA, &map_a, &full[st], pl * p.Kr + s * kI8Kb, a_row0);
+              }
+            }
+          } else {
+            for (int h = 0; h < raw_halves; ++h) {
+              if (p.ga_per) {
+                for (int k = 0; k < p.ga_per; ++k)
+                  tma_load_2d(sp + h * kBM * 128 + k * p.M * 128, &map_a, &full[st], 32 * h, ga_rows[k]);
+              } else {
+                tma_load_2d(sp + h * kBM * 128, &map_a, &full[st], 32 * h, a_row0);
+              }
+            }
+          }
+          tma_load_3d(sp + a_span, &map_b, &full[st], s * kI8Kb, b_row0, 0);
+        }
+        trace(p, pit, 1);
+      }
+    }
+  } else if (warp == 1) {  // ---- MMA issuer (converged warp, one elected lane issues) ----
+    // c_format S32 (2), a / b format S8 (1); K-major; N >> 3; M >> 4
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(p.bn >> 3) << 17) |
+                           ((kTM >> 4) << 24);
+    Ring rg, ra;
+    uint64_t it = 0;
+    for (uint64_t t = cta0; t < tiles && (!PAIR || rank == 0); t += ncta, ++it, ra.next(static_cast<int>(n_acc))) {
+      const uint32_t tb = static_cast<uint32_t>(ra.slot);
+      if (ra.round > 0) mbar_wait(&acc_empty[tb], (ra.round - 1) & 1);
+      if (lane == 0) trace(p, it, 2);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t dacc = tmem + tb * buf_cols;
+      for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
+        const int st = rg.slot;
+        if constexpr (QA && !PAIR)
+          mbar_wait(&full[st], rg.round & 1);
+        else
+          mbar_wait(&conv[st], rg.round & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sp = smem_u32(base + st * stage_bytes);
+        mma_stage_i8<PAIR>(dacc, static_cast<uint32_t>(p.bn), sw_desc<16>(sp), sw_desc<16>(sp + a_span), kPlaneA,
+                           static_cast<uint32_t>(plane_b), idesc, s > 0 ? 1u : 0u);
+        if constexpr (PAIR)
+          mma_commit_pair_elect(&empty[st]);
+        else
+          mma_commit_elect(&empty[st]);
+      }
+      if constexpr (PAIR)
+        mma_commit_pair_elect(&acc_full[tb]);
+      else
+        mma_commit_elect(&acc_full[tb]);
+      if (lane == 0) trace(p, it, 3);
+    }
+  } else if (QA && PAIR && warp == 2) {  // ---- relay: both CTAs' stages landed ----
+    // (the leader's MMA issues over both CTAs' shared memory: each CTA's
+    // landed stage is signalled on the leader's conv barrier)
+    Ring rg;
+    const uint32_t conv_leader = mapa(conv, 0);
+    for (uint64_t t = cta0; t < tiles; t += ncta)
+      for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
+        mbar_wait(&full[rg.slot], rg.round & 1);
+        if (lane == 0) mbar_arrive_cluster(conv_leader + 8u * static_cast<uint32_t>(rg.slot));
+        __syncwarp();
+      }
+  } else if (!QA && warp < 2 + p.n_conv) {  // ---- converters (whole-K stages) ----
+    // one row per thread: 64 raw floats (two SWIZZLE_128B halves; the second
+    // is zero when K = 16 complex) -> row max -> exponent -> 3 x 64 digit
+    // bytes in SWIZZLE_64B rows at plane p * 8 KB, in place
+    const int r = threadIdx.x - 64;
+    Ring rg;
+    uint64_t cit = 0;
+    const uint32_t conv_leader = PAIR ? mapa(conv, 0) : 0u;
+    const bool two = p.Kr > 32;
+    for (uint64_t t = cta0; t < tiles; t += ncta, ++cit, rg.next(n_stages)) {
+      const int st = rg.slot;
+      mbar_wait(&full[st], rg.round & 1);
+      if (r == 0) trace(p, cit, 4);
+      uint8_t* sp = base + st * stage_bytes;
+      float4 v[16];
+      float mx = 0.f;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const int h = c >> 3, cc = c & 7;
+        if (h && !two) {
+          v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          continue;
+        }
+        v[c] = reinterpret_cast<const float4*>(sp + h * kBM * 128 + r * 128)[cc ^ (r & 7)];
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w))));
+      }
+      const int sa = i8_scale_exp(mx);
+      const float sc = pow2f_wide(sa);
+      asm volatile("bar.sync 3, %0;" ::"r"(32 * p.n_conv) : "memory");  // every raw read done (in place)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {  // 16-byte chunk j of each plane row = elements 16j .. 16j + 15
+        uint32_t w[3][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float4 x = v[4 * j + q];
+          i8_pack4(i8_biased(x.x, sc), i8_biased(x.y, sc), i8_biased(x.z, sc), i8_biased(x.w, sc), w[0][q],
+                   w[1][q], w[2][q]);
+        }
+        const int off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+          *reinterpret_cast<uint4*>(sp + pl * kPlaneA + off) = make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // row exponent for this tile's epilogue (ring slot released by the
+      // pipeline depth: converters run at most n_stages + n_acc tiles ahead)
+      const int slot = static_cast<int>(cit % kSaRing);
+      sa_ring[slot * kBM + r] = static_cast<int8_t>(sa);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sa_full[slot]);
+      if constexpr (PAIR) {
+        if (lane == 0) mbar_arrive_cluster(conv_leader + 8u * static_cast<uint32_t>(st));
+      } else {
+        mbar_arrive(&conv[st]);
+      }
+    }
+  } else if (warp >= 2 + p.n_conv && warp < 2 + p.n_conv + 4 * n_epi) {  // ---- epilogue ----
+    const int e0 = 2 + p.n_conv;
+    const int eg = (warp - e0) / 4;
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    int64_t* coff = coff_s + eg * (kMaxBn / 2);
+    float* csf = cs_s + eg * (kMaxBn / 2);
+    // output offset of complex column r of a tile, -1 for a padding slot
+    auto col_offset = [&](uint32_t u, int n0c) -> int64_t {
+      if (r >= p.bn / 2) return -1;
+      const int c = n0c + r;
+      uint32_t item = u;
+      int n = c;
+      if (p.ga_per) return static_cast<int64_t>(ton_cached ? ton_s[n] : p.ton(n));
+      if (p.slots) {
+        const uint32_t g0 = p.grp_start[u], g = p.grp_start[u + 1] - g0;
+        const uint32_t slot = static_cast<uint32_t>(c) >> p.fb;
+        if (slot >= g) return -1;
+        item = p.grp_items[g0 + slot];
+        n = c & ((1 << p.fb) - 1);
+      }
+      const uint64_t entry = p.out_rows ? uint64_t{p.out_rows[item]} : uint64_t{item};
+      return static_cast<int64_t>(entry * p.out_item + (ton_cached ? ton_s[n] : p.ton(n)));
+    };
+    const uint64_t t_step = split ? uint64_t{ncta} : n_epi * uint64_t{ncta};
+    uint64_t t = cta0 + (split ? 0 : uint64_t{static_cast<uint32_t>(eg)} * ncta);
+    uint64_t it = split ? 0 : eg;
+    const uint64_t it_step = split ? 1 : n_epi;
+    uint32_t nxt_bunit = 0;
+    int nxt_m0 = 0, nxt_n0 = 0, nxt_sa = 0;
+    uint64_t om = 0, nxt_om = 0;
+    uint64_t key = ~uint64_t{0}, nxt_key = ~uint64_t{0}, table_key = ~uint64_t{0};
+    int64_t my_coff = -1, nxt_coff = -1;
+    float my_cs = 0.f, nxt_cs = 0.f;
+    uint32_t cached_u = ~0u, cached_entry = 0;
+    TileWalk w;
+    w.init(t, t_step, tiles_n, tiles_m);
+    auto fetch = [&]() {
+      const uint32_t u = w.u;
+      nxt_m0 = static_cast<int>(w.m) * kTM + m_off;
+      nxt_n0 = static_cast<int>(w.n) * p.bn;
+      nxt_bunit = u;
+      if (p.ga_per) {  // row r = item slot r / M, m = r % M
+        const uint32_t* tl = p.ga_tiles + static_cast<uint64_t>(w.m) * (1 + p.ga_per);
+        nxt_bunit = __ldg(tl);
+        const uint32_t itm = __ldg(tl + 1 + r / p.M);
+        nxt_om = itm == ~0u ? ~uint64_t{0}
+                            : (p.out_rows ? uint64_t{__ldg(p.out_rows + itm)} : uint64_t{itm}) * p.out_item +
+                                  p.tom(r % p.M);
+        if (QA) nxt_sa = itm == ~0u ? 0 : __ldg(p.sa + uint64_t{__ldg(p.ia + itm)} * p.M + r % p.M);
+      } else {
+        nxt_om = nxt_m0 + r < p.M ? uint64_t{p.tom(nxt_m0 + r)} : ~uint64_t{0};
+        if (QA) {
+          if (u != cached_u) {
+            cached_u = u;
+            cached_entry = unit_a_entry(u);
+          }
+          nxt_sa = nxt_m0 + r < p.M ? __ldg(p.sa + uint64_t{cached_entry} * p.M + nxt_m0 + r) : 0;
+        }
+      }
+      w.advance();
+      const uint64_t k = (uint64_t{nxt_bunit} << 20) | static_cast<uint32_t>(nxt_n0);
+      if (k != nxt_key) {
+        nxt_key = k;
+        nxt_coff = col_offset(nxt_bunit, nxt_n0 / 2);
+        nxt_cs = r < p.bn / 2 ? pow2f_wide(-__ldg(p.sb + uint64_t{nxt_bunit} * (p.Nr / 2) + nxt_n0 / 2 + r)) : 0.f;
+      }
+    };
+    if (t < tiles) fetch();
+    const uint32_t acc_empty_leader = PAIR ? mapa(acc_empty, 0) : 0u;
+    for (; t < tiles; t += t_step, it += it_step) {
+      const int m0 = nxt_m0;
+      om = nxt_om;
+      key = nxt_key;
+      my_coff = nxt_coff;
+      my_cs = nxt_cs;
+      int sa = nxt_sa;
+      (void)m0;
+      if (t + t_step < tiles) fetch();
+      if (key != table_key) {  // uniform across the group
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));
+        if (r < kMaxBn / 2) {
+          coff[r] = my_coff;
+          csf[r] = my_cs;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));
+        table_key = key;
+      }
+      const uint32_t tb = static_cast<uint32_t>(it % n_acc);
+      mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
+      if constexpr (!QA) {
+        const int slot = static_cast<int>(it % kSaRing);
+        mbar_wait(&sa_full[slot], static_cast<uint32_t>(it / kSaRing) & 1);
+        sa = sa_ring[slot * kBM + r];
+      }
+      const float rs = pow2f_wide(16 - sa);
+      if (warp == e0 && lane == 0) trace(p, it, 5);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tacc = tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16);
+      const int c_first = split ? 32 * eg : 0, c_step = split ? 32 * n_epi : 32;
+      for (int c0 = c_first; c0 < p.bn; c0 += c_step) {
+        const int cc = c0 / 2;  // first complex column of this chunk
+        float v[32];
+        i8_load_combine(tacc + c0, p.bn, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= rs * csf[cc + j / 2];
+        if (p.transpose) {
+          float* buf = stage_out + (warp - e0) * 32 * 33;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = v[j];
+          __syncwarp();
+          const int64_t co = coff[cc + (lane & 15)];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float2 vals[8];
+            uint64_t roms[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int e = lane + 32 * (8 * h + i);
+              const int row = e >> 4, cj = e & 15;
+              roms[i] = __shfl_sync(0xffffffffu, om, row);
+              vals[i] = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
+            }
+            if (co < 0) continue;
+            if (accumulate) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                if (roms[i] != ~uint64_t{0}) {
+                  const float2 old = p.out[co + roms[i]];
+                  vals[i].x += old.x;
+                  vals[i].y += old.y;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (roms[i] != ~uint64_t{0}) p.out[co + roms[i]] = vals[i];
+          }
+          __syncwarp();
+          continue;
+        }
+        if (om == ~uint64_t{0}) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int64_t co[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const longlong2 t2 = reinterpret_cast<const longlong2*>(coff + cc + 8 * h)[j];
+            co[2 * j] = t2.x;
+            co[2 * j + 1] = t2.y;
+          }
+          const float* vh = v + 16 * h;
+          if (p.n_contig && !accumulate) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (co[2 * j] >= 0)
+                *reinterpret_cast<float4*>(p.out + co[2 * j] + om) =
+                    make_float4(vh[4 * j], vh[4 * j + 1], vh[4 * j + 2], vh[4 * j + 3]);
+          } else if (!accumulate) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (co[j] >= 0) p.out[co[j] + om] = make_float2(vh[2 * j], vh[2 * j + 1]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (co[j] >= 0) {
+                const float2 old = p.out[co[j] + om];
+                p.out[co[j] + om] = make_float2(old.x + vh[2 * j], old.y + vh[2 * j + 1]);
+              }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * tb);
+      } else {
+        mbar_arrive(&acc_empty[tb]);
+      }
+      if (warp == e0 && lane == 0) trace(p, it, 6);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  if constexpr (PAIR) {
+    cluster_sync_all();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  } else {
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // B operand element e of the B̂ build (e = (blk * N + n) * K + k, blk = unit *
 // slots + slot in grouped mode; zero for the padding blocks of a group).
 struct BhatSrc {
@@ -1143,6 +1730,91 @@ __global__ void build_bhat_f16_kernel(const BhatSrc src, uint64_t total, const u
   }
 }
 
+// B̂ digit planes (split-integer path): one warp per B̂ column pair (blk, n),
+// e = (blk * N + n) * K + k. Exponent sb from max over k of |br|, |bi|; rows
+// 2n = [Yr, -Yi]_k and 2n + 1 = [Yi, Yr]_k of plane p at p * plane_bytes +
+// row * kr_pad (kr_pad >= 2K: zero padding up to a whole stage).
+__global__ void build_bhat_i8_kernel(const BhatSrc src, uint64_t n_cols, int kr_pad, uint64_t plane_bytes,
+                                     uint8_t* bhat, int8_t* sb_out) {
+  const uint64_t K = uint64_t{1} << src.kc;
+  const int lane = threadIdx.x % 32;
+  const uint64_t b_slice = src.slice_offset();
+  for (uint64_t col = (blockIdx.x * uint64_t{blockDim.x} + threadIdx.x) / 32; col < n_cols;
+       col += uint64_t{gridDim.x} * blockDim.x / 32) {
+    float mx = 0.f;
+    for (uint64_t k = lane; k < K; k += 32) {
+      uint64_t kk, n, blk;
+      const float2 v = src.value(col * K + k, b_slice, kk, n, blk);
+      mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int sb = i8_scale_exp(mx);
+    const float sc = pow2f_wide(sb);
+    if (lane == 0) sb_out[col] = static_cast<int8_t>(sb);
+    uint8_t* r0 = bhat + 2 * col * kr_pad;
+    uint8_t* r1 = r0 + kr_pad;
+    for (uint64_t k = lane; 2 * k < static_cast<uint64_t>(kr_pad); k += 32) {
+      uint32_t q[4] = {0x808080u, 0x808080u, 0x808080u, 0x808080u};  // zero digits
+      if (k < K) {
+        uint64_t kk, n, blk;
+        const float2 v = src.value(col * K + k, b_slice, kk, n, blk);
+        q[0] = i8_biased(v.x, sc);
+        q[1] = i8_biased(-v.y, sc);
+        q[2] = i8_biased(v.y, sc);
+        q[3] = i8_biased(v.x, sc);
+      }
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl) {
+        const int sh = 8 * (2 - pl);  // plane 0: the most significant digit (byte 2)
+        auto dig = [&](uint32_t x) { return ((x >> sh) & 0xFFu) ^ 0x80u; };
+        *reinterpret_cast<uint16_t*>(r0 + pl * plane_bytes + 2 * k) =
+            static_cast<uint16_t>(dig(q[0]) | (dig(q[1]) << 8));
+        *reinterpret_cast<uint16_t*>(r1 + pl * plane_bytes + 2 * k) =
+            static_cast<uint16_t>(dig(q[2]) | (dig(q[3]) << 8));
+      }
+    }
+  }
+}
+
+// In-place row quantization of the A table (split-integer path, K > 32
+// complex): each row of kr floats (VPL float4 per lane, one warp per row) ->
+// exponent sa_out[row] and digit planes [d0 | d1 | d2] in the row's first
+// 3 kr bytes. The whole row is held in registers before any byte is written.
+template <int VPL>
+__global__ void __launch_bounds__(256) quantize_rows_kernel(float* a, uint64_t rows, int8_t* sa_out) {
+  constexpr int kr = VPL * 128;
+  const int lane = threadIdx.x % 32;
+  for (uint64_t row = (blockIdx.x * uint64_t{blockDim.x} + threadIdx.x) / 32; row < rows;
+       row += uint64_t{gridDim.x} * blockDim.x / 32) {
+    float4* src = reinterpret_cast<float4*>(a + row * kr);
+    float4 v[VPL];
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      v[i] = src[lane + 32 * i];
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[i].x), fabsf(v[i].y)), fmaxf(fabsf(v[i].z), fabsf(v[i].w))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const int sa = i8_scale_exp(mx);
+    const float sc = pow2f_wide(sa);
+    if (lane == 0) sa_out[row] = static_cast<int8_t>(sa);
+    __syncwarp();  // every lane's loads of the row precede the first store
+    uint32_t* dst = reinterpret_cast<uint32_t*>(a + row * kr);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      uint32_t w0, w1, w2;
+      i8_pack4(i8_biased(v[i].x, sc), i8_biased(v[i].y, sc), i8_biased(v[i].z, sc), i8_biased(v[i].w, sc), w0, w1,
+               w2);
+      const int wi = lane + 32 * i;  // elements 4 wi .. 4 wi + 3 -> byte 4 wi of each plane
+      dst[wi] = w0;
+      dst[kr / 4 + wi] = w1;
+      dst[kr / 2 + wi] = w2;
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -1179,17 +1851,22 @@ CUtensorMap make_map(const void* base, uint64_t cols, uint64_t rows, uint32_t bo
 
 }  // namespace
 
-bool tc_f16() {
-  // 3xFP16 (default) or 3xTF32 (MTCG_TC_KIND=tf32) split operands
-  static const bool f16 = !(std::getenv("MTCG_TC_KIND") && std::string(std::getenv("MTCG_TC_KIND")) == "tf32");
-  return f16;
+int tc_kind() {
+  static const int kind = [] {
+    const char* k = std::getenv("MTCG_TC_KIND");
+    if (k && std::string(k) == "f16") return 1;
+    if (k && std::string(k) == "tf32") return 2;
+    return 0;
+  }();
+  return kind;
 }
 
-// 3xFP16 halves the MMA time but needs max |A| first (one extra pass over
-// the A table, until the producers emit it). Take it when the op reuses each
-// A entry across enough output columns that the tensor-core time dominates:
-// units * N_eff >= 192 * a_entries (cfg2: nodes 279, 227; not the low-K,
-// HBM-bound ops such as 337 or 285).
+bool tc_f16() { return tc_kind() == 1; }
+
+// Legacy 3xFP16 (MTCG_TC_KIND=f16) halves the MMA time of 3xTF32 but needs
+// max |A| first (one extra pass over the A table). Taken when the op reuses
+// each A entry across enough output columns that the tensor-core time
+// dominates: units * N_eff >= 192 * a_entries.
 bool tc_use_f16(const TcOp& op) {
   if (!tc_f16() || op.ga_tiles) return false;  // gather mode: 3xTF32 (A streamed once)
   static const bool always = std::getenv("MTCG_TC_F16_ALL") != nullptr;
@@ -1204,7 +1881,235 @@ int tc_tile_n(int Nr) {
   return Nr >= cap ? cap : Nr;
 }
 
+namespace {
+
+#define TCK(x)                                                                 \
+  do {                                                                         \
+    cudaError_t err__ = (x);                                                   \
+    if (err__ != cudaSuccess)                                                  \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(err__));     \
+  } while (0)
+
+// Per-device launch state: SM count and the dynamic shared-memory size each
+// kernel variant has been opted into (function attributes are per device).
+struct DevAttr {
+  int n_sms = 0;
+  size_t smem_set[16] = {};
+};
+DevAttr& dev_attr() {
+  static DevAttr attrs[64];
+  int dev = 0;
+  TCK(cudaGetDevice(&dev));
+  DevAttr& a = attrs[dev & 63];
+  if (!a.n_sms) TCK(cudaDeviceGetAttribute(&a.n_sms, cudaDevAttrMultiProcessorCount, dev));
+  return a;
+}
+
+template <class Kern>
+void ensure_smem(DevAttr& da, int slot, Kern kern, size_t smem, bool cluster) {
+  if (smem > da.smem_set[slot]) {
+    TCK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (cluster) TCK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+    da.smem_set[slot] = smem;
+  }
+}
+
+// 3-D int8 map over digit planes: dims {kr, rows, 3} with rows row_stride
+// bytes apart and planes plane_stride bytes apart; box {64, box_rows, depth}.
+CUtensorMap make_map_i8(const void* base, uint64_t kr, uint64_t rows, uint64_t row_stride, uint64_t plane_stride,
+                        uint32_t box_rows, uint32_t depth) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {kr, rows, 3};
+  cuuint64_t strides[2] = {row_stride, plane_stride};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kI8Kb), box_rows, depth};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (i8) failed: " + std::to_string(r));
+  return m;
+}
+
+// 2-D int8 map over rows of `cols` bytes; box {64, box_rows}, SWIZZLE_64B.
+CUtensorMap make_map_i8_rows(const void* base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kI8Kb), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (i8 rows) failed: " + std::to_string(r));
+  return m;
+}
+
+int launch_quantize(const TcOp& op, cudaStream_t st) {
+  const uint64_t rows = op.a_entries << op.fa;
+  const int kr = 2 << op.kc;
+  float* a = const_cast<float*>(op.a);
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((rows + 7) / 8, 148 * 16));
+  switch (kr) {
+    case 128: quantize_rows_kernel<1><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
+    case 256: quantize_rows_kernel<2><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
+    case 512: quantize_rows_kernel<4><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
+    case 1024: quantize_rows_kernel<8><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
+    case 2048: quantize_rows_kernel<16><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
+    case 4096: quantize_rows_kernel<32><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
+    default: throw std::runtime_error("split-integer path: unsupported K = 2^" + std::to_string(op.kc));
+  }
+  return 1;
+}
+
+BhatSrc bhat_src(const TcOp& op) {
+  const bool ga = op.ga_tiles != nullptr;
+  BhatSrc src;
+  src.b = op.b;
+  src.b_item = op.b_item;
+  src.ib = ga ? op.ga_groups : op.ib;
+  src.b_sstr = op.b_sstr;
+  src.s_bits = op.s_bits;
+  src.cur = op.cur;
+  src.tbn = TcTable{op.tbn_lo, op.tbn_hi, op.tbn_bits};
+  src.tbk = TcTable{op.tbk_lo, op.tbk_hi, op.tbk_bits};
+  src.fb = op.fb;
+  src.kc = op.kc;
+  src.slots = op.slots;
+  src.grp_items = op.grp_items;
+  src.grp_start = op.grp_start;
+  return src;
+}
+
+// Split-integer GEMM: [quantize A rows +] B̂ digit planes + persistent GEMM.
+int tc_contract_i8(const TcOp& op, cudaStream_t st) {
+  const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb;
+  const bool ga = op.ga_tiles != nullptr;
+  const uint32_t units = ga ? op.n_ga_groups : op.slots ? op.n_groups : op.nb;
+  const uint64_t Nr = 2 * N * (op.slots ? op.slots : 1u), Kr = uint64_t{2} << op.kc;
+  const bool qa = tc_i8_prequant(op.kc);
+  if (op.kc > 11) throw std::runtime_error("split-integer path: K > 2^11");
+  int launches = 0;
+  if (qa && op.quantize_a) launches += launch_quantize(op, st);
+  // B̂ digit planes [plane][units * Nr rows][kr_pad], column exponents
+  const int kr_pad = static_cast<int>(std::max<uint64_t>(Kr, kI8Kb));
+  const uint64_t b_rows = uint64_t{units} * Nr;
+  const uint64_t plane_bytes = b_rows * kr_pad;
+  uint8_t* bplanes = reinterpret_cast<uint8_t*>(op.bhat_hi);
+  {
+    const uint64_t n_cols = b_rows / 2;
+    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n_cols + 7) / 8, 148 * 16));
+    build_bhat_i8_kernel<<<blocks, 256, 0, st>>>(bhat_src(op), n_cols, kr_pad, plane_bytes, bplanes, op.col_exp);
+    ++launches;
+  }
+  DevAttr& da = dev_attr();
+  const int bn = static_cast<int>(std::min<uint64_t>(Nr, 128));
+  const bool pair = !ga && bn == 128 && M >= 256 && da.n_sms >= 2 &&
+                    !(std::getenv("MTCG_TC_PAIR") && std::atoi(std::getenv("MTCG_TC_PAIR")) == 0);
+  const int bn_cta = pair ? bn / 2 : bn;
+  const bool transpose = !op.m_contig && bn <= 64;
+  const int n_conv = qa ? (pair ? 1 : 0) : 4;  // QA pair: one relay warp
+  const int extra = 1024 + 8 * (3 * kMaxStages + 2 * kMaxAcc + kSaRing) + 16 +
+                    4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) + 16 + 8 * kEpiGroups * (kMaxBn / 2) +
+                    4 * kEpiGroups * (kMaxBn / 2) + kSaRing * kBM + (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
+  constexpr int kSmemMax = 227 * 1024;
+  const int stage_bytes = (qa ? 3 * kBM * kI8Kb : 2 * kBM * 128) + 3 * bn_cta * kI8Kb;
+  const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
+  const size_t smem = extra + static_cast<size_t>(n_stages) * stage_bytes;
+  if (smem > static_cast<size_t>(kSmemMax)) throw std::runtime_error("split-integer GEMM: shared memory");
+  CUtensorMap ma;
+  if (qa)  // digit planes in place: rows of 4 Kr bytes, plane p at byte p Kr
+    ma = make_map_i8_rows(op.a, 4 * Kr, op.a_entries * M, ga ? static_cast<uint32_t>(M) : kBM);
+  else
+    ma = make_map(op.a, Kr, op.a_entries * M, ga ? static_cast<uint32_t>(M) : kBM, 32);
+  const CUtensorMap mb = make_map_i8(bplanes, kr_pad, b_rows, kr_pad, plane_bytes, bn_cta, 3);
+  TcParams p;
+  p.M = static_cast<int>(M);
+  p.Nr = static_cast<int>(Nr);
+  p.Kr = static_cast<int>(Kr);
+  p.bn = bn;
+  p.nb = ga ? 1u : units;
+  p.ga_tiles = op.ga_tiles;
+  p.ga_per = ga ? static_cast<int>(128u >> op.fa) : 0;
+  p.nb_ga_tiles = ga ? op.n_ga_tiles : 0u;
+  p.ia = op.ia;
+  p.grp_items = op.grp_items;
+  p.grp_start = op.grp_start;
+  p.slots = static_cast<int>(op.slots);
+  p.fb = op.fb;
+  p.out = op.out;
+  p.out_rows = op.out_rows;
+  p.out_item = op.out_item;
+  p.tom = TcTable{op.tom_lo, op.tom_hi, op.tom_bits};
+  p.ton = TcTable{op.ton_lo, op.ton_hi, op.ton_bits};
+  p.cur = op.cur;
+  p.root = op.root;
+  p.n_contig = op.n_contig && (op.slots == 0 || op.fb >= 1);
+  p.m_contig = op.m_contig;
+  p.transpose = transpose ? 1 : 0;
+  p.partials = nullptr;
+  p.n_conv = n_conv;
+  p.sa = op.row_exp;
+  p.sb = op.col_exp;
+  p.dbg = nullptr;
+  const int slot = 4 + (pair ? 2 : 0) + (qa ? 1 : 0);
+  auto kern = pair ? (qa ? tc_i8_persistent<true, true> : tc_i8_persistent<true, false>)
+                   : (qa ? tc_i8_persistent<false, true> : tc_i8_persistent<false, false>);
+  ensure_smem(da, slot, kern, smem, pair);
+  const uint64_t tile_m = pair ? 2 * kBM : kBM;
+  const uint64_t tiles = ga ? uint64_t{op.n_ga_tiles} * ((Nr + bn - 1) / bn)
+                            : ((M + tile_m - 1) / tile_m) * ((Nr + bn - 1) / bn) * units;
+  const unsigned grid = pair ? static_cast<unsigned>(std::min<uint64_t>(2 * tiles, da.n_sms & ~1))
+                             : static_cast<unsigned>(std::min<uint64_t>(tiles, da.n_sms));
+  const unsigned threads = 64 + 32 * n_conv + 128 * kEpiGroups;
+  const char* tr = std::getenv("MTCG_TC_TRACE");
+  const bool tracing = tr && std::atoi(tr) == op.node;
+  if (tracing) {
+    TCK(cudaMalloc(&p.dbg, sizeof(unsigned long long) * kTraceTiles * 8));
+    TCK(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * kTraceTiles * 8, st));
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pair ? 1 : 0;
+  TCK(cudaLaunchKernelEx(&cfg, kern, ma, mb, p, n_stages));
+  ++launches;
+  if (tracing) {
+    std::vector<unsigned long long> h(kTraceTiles * 8);
+    TCK(cudaMemcpyAsync(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    TCK(cudaStreamSynchronize(st));
+    TCK(cudaFree(p.dbg));
+    const unsigned long long t0 = h[0];
+    std::fprintf(stderr, "[tc trace node %d] i8 pair=%d qa=%d stages=%d bn=%d tiles=%llu grid=%u\n", op.node,
+                 pair ? 1 : 0, qa ? 1 : 0, n_stages, bn, static_cast<unsigned long long>(tiles), grid);
+    std::fprintf(stderr, " tile  prod0  prod1  conv  mma0  mma1  epi0  epi1   (cycles from tile0 prod0)\n");
+    for (int i = 0; i < kTraceTiles; ++i) {
+      if (!h[i * 8]) break;
+      if (i < 24 || i % 32 == 0)
+        std::fprintf(stderr, " %4d %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", i, (long long)(h[i * 8] - t0),
+                     (long long)(h[i * 8 + 1] - t0), (long long)(h[i * 8 + 4] - t0), (long long)(h[i * 8 + 2] - t0),
+                     (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 5] - t0), (long long)(h[i * 8 + 6] - t0));
+    }
+  }
+  return launches;
+}
+
+}  // namespace
+
+int tc_quantize_a(const TcOp& op, cudaStream_t st) {
+  if (tc_kind() != 0 || !tc_i8_prequant(op.kc)) return 0;
+  return launch_quantize(op, st);
+}
+
 int tc_contract(const TcOp& op, cudaStream_t st) {
+  if (tc_kind() == 0) return tc_contract_i8(op, st);
   const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb, K = uint64_t{1} << op.kc;
   // units: items, groups of items sharing the A entry (N_eff = slots x N), or
   // (gather mode) groups of items sharing the B entry

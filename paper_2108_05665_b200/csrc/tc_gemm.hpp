@@ -49,10 +49,26 @@ struct TcOp {
   uint32_t n_ga_tiles;
   const uint32_t* ga_groups;
   uint32_t n_ga_groups;
+  // split-integer path (default): B̂ digit planes live in [bhat_hi, bhat_lo +
+  // its size), column exponents in col_exp; A rows (K > 32 complex) are
+  // quantized in place into digit planes with exponents in row_exp, unless
+  // quantize_a is false (done once by the slice-reuse prologue).
+  int8_t* col_exp;
+  int8_t* row_exp;
+  bool quantize_a;
 };
 
 // Launches the op's kernels on `st`; returns how many.
 int tc_contract(const TcOp& op, cudaStream_t st);
+// Split-integer path: the in-place A row quantization alone (slice-reuse
+// prologue for ops whose A table is slice-invariant); returns launches.
+int tc_quantize_a(const TcOp& op, cudaStream_t st);
+// Tensor-core scheme: 0 = split integer (3 int8 digits, exact accumulation;
+// default), 1 = 3xFP16, 2 = 3xTF32 (MTCG_TC_KIND=i8|f16|tf32).
+int tc_kind();
+// A rows of this op are quantized by a pre-pass (K > 32 complex) under the
+// split-integer scheme.
+inline bool tc_i8_prequant(int kc) { return kc > 5; }
 bool tc_f16();                   // 3xFP16 split operands allowed (default) vs 3xTF32 only
 bool tc_use_f16(const TcOp& op);  // this op takes the 3xFP16 path
 int tc_tile_n(int n_real);
