@@ -912,7 +912,12 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       op.a_prequant = invariant[op.child_a] && !invariant[node] && op.kc > 5;
       op.scratch_elems = 2 * bhat + 4096 / c.elem_bytes +
                          (col_exps + (op.a_prequant ? 0 : row_exps) + c.elem_bytes) / c.elem_bytes + 1;
-      if (op.a_prequant) op.row_exp_off = alloc((row_exps + c.elem_bytes - 1) / c.elem_bytes, node);
+      // (prologue-written, read by every slice: a private region above the
+      // first-fit arena, which earlier slice ops reuse)
+      if (op.a_prequant) {
+        op.row_exp_off = private_top;
+        private_top += ((row_exps + c.elem_bytes - 1) / c.elem_bytes + align - 1) / align * align;
+      }
       if (op.scratch_elems <= private_elems) {
         scratch_private.push_back(c.ops.size());
         op.scratch_off = private_top;
@@ -943,6 +948,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     if (!op.root && node_private[op.node]) op.out_base += arena_top;
   }
   for (size_t i : scratch_private) c.ops[i].scratch_off += arena_top;
+  for (Op& op : c.ops)
+    if (op.a_prequant) op.row_exp_off += arena_top;
   c.arena_elems = arena_top + private_top;
   c.private_elems = private_top;
   // --- fused operand chains ---------------------------------------------------------

@@ -285,6 +285,27 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31]));
+}
+
 struct TcTable {
   const uint32_t* lo;
   const uint32_t* hi;
@@ -328,6 +349,7 @@ struct TcParams {
   // m) and column exponents of B̂ (unit * Nr / 2 + complex column)
   const int8_t* sa;
   const int8_t* sb;
+  int tom_cache;  // > 0: words of the tom table (lo, then hi) staged in shared memory
 };
 
 // Role timestamps of CTA 0's first kTraceTiles tiles (MTCG_TC_TRACE=<node>).
@@ -1050,18 +1072,44 @@ __device__ __forceinline__ void i8_pack4(uint32_t v0, uint32_t v1, uint32_t v2, 
   w0 = __byte_perm(__byte_perm(v0, v1, 0x0062), __byte_perm(v2, v3, 0x6200), 0x7610) ^ 0x80808080u;
 }
 
-// 32 real columns of the three accumulators at tcol (+ bn, + 2 bn), combined:
-// v = acc0 2^16 + acc1 2^8 + acc2 (fp32, one rounding at the end).
-__device__ __forceinline__ void i8_load_combine(uint32_t tcol, int bn, float (&v)[32]) {
-  uint32_t a0[32], a1[32], a2[32];
-  tmem_ld32_nowait(tcol, a0);
-  tmem_ld32_nowait(tcol + bn, a1);
-  tmem_ld32_nowait(tcol + 2 * bn, a2);
-  tmem_wait();
+// 32 real columns of the three accumulators at tcol (+ bn, + 2 bn), combined
+// in integer arithmetic: 2^16 acc0 + 2^8 acc1 + acc2 = 2^8 (W + acc2 / 2^8)
+// with W = 2^8 acc0 + acc1, v = I2F(W + rn(acc2 / 2^8)) — one conversion per
+// element (the conversion unit, 16 per SM per clock, bounds this epilogue).
+// W fits in int32 whenever |acc0| < 2^22, always true for Kr <= 1024 (|d0|,
+// |g0| <= 64); otherwise `wide` checks the chunk and falls back to two
+// conversions, 2^8 I2F(acc0) + I2F(acc1 + t). The dropped low bits of acc2
+// carry weight 2^-8 of W's unit (round half up; ties are 1/256 of values).
+__device__ __forceinline__ void i8_load_combine(uint32_t t0, uint32_t t1, uint32_t t2, bool wide, float (&v)[32]) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    v[j] = fmaf(__int2float_rn(static_cast<int>(a0[j])), 65536.f,
-                fmaf(__int2float_rn(static_cast<int>(a1[j])), 256.f, __int2float_rn(static_cast<int>(a2[j]))));
+  for (int h = 0; h < 2; ++h) {  // 16 columns at a time (bounded register use)
+    uint32_t a0[16], a1[16], a2[16];
+    tmem_ld16_nowait(t0 + 16 * h, a0);
+    tmem_ld16_nowait(t1 + 16 * h, a1);
+    tmem_ld16_nowait(t2 + 16 * h, a2);
+    tmem_wait();
+    bool big = false;
+    if (wide) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) m |= (a0[j] + 0x400000u) & 0xFF800000u;
+      big = __any_sync(0xffffffffu, m != 0);
+    }
+    if (!big) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int t = (static_cast<int>(a2[j]) + 128) >> 8;
+        v[16 * h + j] = __int2float_rn(static_cast<int>(a0[j] << 8) + static_cast<int>(a1[j]) + t);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int t = (static_cast<int>(a2[j]) + 128) >> 8;
+        v[16 * h + j] =
+            fmaf(__int2float_rn(static_cast<int>(a0[j])), 256.f, __int2float_rn(static_cast<int>(a1[j]) + t));
+      }
+    }
+  }
 }
 
 // One stage (2 k-steps) of the 3-digit product: per k-step acc0 += A0 B0,
@@ -1069,8 +1117,8 @@ __device__ __forceinline__ void i8_load_combine(uint32_t tcol, int bn, float (&v
 // interleaved so consecutive MMAs are independent). a / b: descriptors of
 // plane 0; planes are pa / pb bytes apart (>> 4 in the descriptor).
 template <bool PAIR>
-__device__ __forceinline__ void mma_stage_i8(uint32_t d, uint32_t bn, uint64_t a, uint64_t b, uint32_t pa,
-                                             uint32_t pb, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_stage_i8(uint32_t d, uint32_t d1, uint32_t d2, uint64_t a, uint64_t b,
+                                             uint32_t pa, uint32_t pb, uint32_t idesc, uint32_t acc) {
   const uint64_t a1 = a + (pa >> 4), a2 = a + 2 * (pa >> 4);
   const uint64_t b1 = b + (pb >> 4), b2 = b + 2 * (pb >> 4);
 #pragma unroll
@@ -1088,7 +1136,7 @@ __device__ __forceinline__ void mma_stage_i8(uint32_t d, uint32_t bn, uint64_t a
           "@e tcgen05.mma.cta_group::2.kind::i8 [%1], %4, %6, %9, 1;\n\t"
           "@e tcgen05.mma.cta_group::2.kind::i8 [%2], %4, %7, %9, 1;\n\t"
           "@e tcgen05.mma.cta_group::2.kind::i8 [%2], %5, %6, %9, 1;\n\t}" ::"r"(d),
-          "r"(d + bn), "r"(d + 2 * bn), "l"(a + o), "l"(a1 + o), "l"(a2 + o), "l"(b + o), "l"(b1 + o),
+          "r"(d1), "r"(d2), "l"(a + o), "l"(a1 + o), "l"(a2 + o), "l"(b + o), "l"(b1 + o),
           "l"(b2 + o), "r"(idesc), "r"(f));
     } else {
       asm volatile(
@@ -1101,7 +1149,7 @@ __device__ __forceinline__ void mma_stage_i8(uint32_t d, uint32_t bn, uint64_t a
           "@e tcgen05.mma.cta_group::1.kind::i8 [%1], %4, %6, %9, 1;\n\t"
           "@e tcgen05.mma.cta_group::1.kind::i8 [%2], %4, %7, %9, 1;\n\t"
           "@e tcgen05.mma.cta_group::1.kind::i8 [%2], %5, %6, %9, 1;\n\t}" ::"r"(d),
-          "r"(d + bn), "r"(d + 2 * bn), "l"(a + o), "l"(a1 + o), "l"(a2 + o), "l"(b + o), "l"(b1 + o),
+          "r"(d1), "r"(d2), "l"(a + o), "l"(a1 + o), "l"(a2 + o), "l"(b + o), "l"(b1 + o),
           "l"(b2 + o), "r"(idesc), "r"(f));
     }
   }
@@ -1148,7 +1196,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   uint64_t* empty = conv + kMaxStages;
   uint64_t* acc_full = empty + kMaxStages;
   uint64_t* acc_empty = acc_full + kMaxAcc;
-  uint64_t* sa_full = acc_empty + kMaxAcc;
+  uint64_t* res_free = acc_empty + kMaxAcc;  // split mode: combined-result slot (tile parity) drained
+  uint64_t* sa_full = res_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sa_full + kSaRing);
   uint32_t* ton_s = tmem_slot + 4;
   const int n_item_cols = p.slots ? (1 << p.fb) : p.Nr / 2;
@@ -1156,6 +1205,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
   float* cs_s = reinterpret_cast<float*>(coff_s + kEpiGroups * (kMaxBn / 2));
   int8_t* sa_ring = reinterpret_cast<int8_t*>(cs_s + kEpiGroups * (kMaxBn / 2));
   float* stage_out = reinterpret_cast<float*>(sa_ring + kSaRing * kBM);
+  // the output row offset table (both halves) cached in shared memory when
+  // small (p.tom_cache): the epilogue's per-tile row offsets are then shared
+  // loads (global ones stalled the loop on the load's address registers)
+  uint32_t* tom_s = reinterpret_cast<uint32_t*>(stage_out + (p.transpose ? 4 * kEpiGroups * 32 * 33 : 0));
+  const uint32_t tom_lo_n = 1u << p.tom.lo_bits;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int accumulate = p.root ? static_cast<int>(__ldg(p.cur + 1)) : 0;
@@ -1165,11 +1219,21 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int k_stages = QA ? p.Kr / kI8Kb : 1;
   const uint32_t buf_cols = 3 * p.bn;
   const uint32_t n_acc = min(static_cast<uint32_t>(kMaxAcc), 512u / buf_cols);
-  const bool split = n_acc == 1;  // both epilogue groups drain every tile
+  // One 3 x bn accumulator set (bn = 128): both epilogue groups drain every
+  // tile in two phases — (1) combine the three accumulators into fp32 in the
+  // acc0 columns and release acc1 / acc2 at once, (2) store the result — and
+  // acc0 alternates between columns [0, bn) and [3 bn, 4 bn) by tile parity,
+  // so the next tile's main loop runs while phase 2 drains.
+  const bool split = n_acc == 1;
   constexpr int n_epi = kEpiGroups;
   const bool ton_cached = n_item_cols <= kMaxTonCache;
   if (ton_cached)
     for (int n = threadIdx.x; n < n_item_cols; n += blockDim.x) ton_s[n] = p.ton(n);
+  if (p.tom_cache) {
+    for (uint32_t i = threadIdx.x; i < tom_lo_n; i += blockDim.x) tom_s[i] = __ldg(p.tom.lo + i);
+    for (uint32_t i = threadIdx.x; i < static_cast<uint32_t>(p.tom_cache) - tom_lo_n; i += blockDim.x)
+      tom_s[tom_lo_n + i] = __ldg(p.tom.hi + i);
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < n_stages; ++s) {
@@ -1182,6 +1246,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], epi_arrivals);
     }
+    mbar_init(&res_free[0], epi_arrivals);
+    mbar_init(&res_free[1], epi_arrivals);
     for (int s = 0; s < kSaRing; ++s) mbar_init(&sa_full[s], max(1, p.n_conv));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1206,27 +1272,38 @@ __global__ void __launch_bounds__(kPThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // Tile t = (unit, m-tile, n-tile) with n fastest; each role walks t0, t0 +
+  // step, ... with the step decomposed once in the same mixed radix and added
+  // with carries (no 64-bit divisions per tile). The step digits are kernel
+  // constants outside the walker, so a walker is three registers.
+  struct Steps {
+    uint32_t dn, dm, du, tn, tm;
+  };
   struct TileWalk {
-    uint32_t n, m, u, dn, dm, du, tn, tm;
-    __device__ void init(uint64_t t0, uint64_t step, uint32_t tn_, uint32_t tm_) {
-      tn = tn_;
-      tm = tm_;
+    uint32_t n, m, u;
+    __device__ void init(uint64_t t0, uint32_t tn, uint32_t tm) {
       n = static_cast<uint32_t>(t0 % tn);
       m = static_cast<uint32_t>((t0 / tn) % tm);
       u = static_cast<uint32_t>(t0 / (uint64_t{tn} * tm));
-      dn = static_cast<uint32_t>(step % tn);
-      dm = static_cast<uint32_t>((step / tn) % tm);
-      du = static_cast<uint32_t>(step / (uint64_t{tn} * tm));
     }
-    __device__ void advance() {
-      n += dn;
-      uint32_t c = n >= tn;
-      n -= c ? tn : 0u;
-      m += dm + c;
-      c = m >= tm;
-      m -= c ? tm : 0u;
-      u += du + c;
+    __device__ __forceinline__ void advance(const Steps& s) {
+      n += s.dn;
+      uint32_t c = n >= s.tn;
+      n -= c ? s.tn : 0u;
+      m += s.dm + c;
+      c = m >= s.tm;
+      m -= c ? s.tm : 0u;
+      u += s.du + c;
     }
+  };
+  auto make_steps = [&](uint64_t step) {
+    Steps s;
+    s.tn = tiles_n;
+    s.tm = tiles_m;
+    s.dn = static_cast<uint32_t>(step % tiles_n);
+    s.dm = static_cast<uint32_t>((step / tiles_n) % tiles_m);
+    s.du = static_cast<uint32_t>(step / (uint64_t{tiles_n} * tiles_m));
+    return s;
   };
   // A entry of a unit (its first item's)
   auto unit_a_entry = [&](uint32_t u) -> uint32_t {
@@ -1240,10 +1317,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
       uint32_t cached_item = ~0u, a_entry = 0;
       uint64_t pit = 0;
       TileWalk w;
-      w.init(cta0, ncta, tiles_n, tiles_m);
+      w.init(cta0, tiles_n, tiles_m);
+      const Steps ws = make_steps(ncta);
       const uint32_t a_box_bytes = QA ? kPlaneA : kBM * 128u;
       const int raw_halves = p.Kr > 32 ? 2 : 1;
-      for (uint64_t t = cta0; t < tiles; t += ncta, ++pit, w.advance()) {
+      for (uint64_t t = cta0; t < tiles; t += ncta, ++pit, w.advance(ws)) {
         const uint32_t item = w.u;
         const int m0 = static_cast<int>(w.m) * kTM + m_off;
         const int n0 = static_cast<int>(w.n) * p.bn + static_cast<int>(rank) * bn_cta;
@@ -1254,11 +1332,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         int a_row0 = static_cast<int>(a_entry * static_cast<uint64_t>(p.M)) + m0;
         int b_row0 = static_cast<int>(item * static_cast<uint64_t>(p.Nr)) + n0;
-        int ga_rows[4] = {0, 0, 0, 0};
+        int ga_rows[4] = {0, 0, 0, 0};  // (unrolled: registers, not local memory)
         if (p.ga_per) {
           const uint32_t* tl = p.ga_tiles + static_cast<uint64_t>(w.m) * (1 + p.ga_per);
           b_row0 = static_cast<int>(__ldg(tl) * static_cast<uint64_t>(p.Nr)) + n0;
-          for (int k = 0; k < p.ga_per; ++k) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k >= p.ga_per) break;
             uint32_t itk = __ldg(tl + 1 + k);
             if (itk == ~0u) itk = __ldg(tl + 1);
             ga_rows[k] = static_cast<int>(__ldg(p.ia + itk) * static_cast<uint64_t>(p.M));
@@ -1273,9 +1353,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
           if constexpr (QA) {  // digit plane pl of a row at byte pl * Kr of it
             for (int pl = 0; pl < 3; ++pl) {
               if (p.ga_per) {  // M rows per item
-                for (int k = 0; k < p.ga_per; ++k)
-                  tma_load_2d(sp + pl * kPlaneA + k * p.M * kI8Kb, &map_a, &full[st], pl * p.Kr + s * kI8Kb,
-                              ga_rows[k]);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  if (k < p.ga_per)
+                    tma_load_2d(sp + pl * kPlaneA + k * p.M * kI8Kb, &map_a, &full[st], pl * p.Kr + s * kI8Kb,
+                                ga_rows[k]);
               } else {
                 tma_load_2d(sp + pl * kPlaneA, &map_a, &full[st], pl * p.Kr + s * kI8Kb, a_row0);
               }
@@ -1283,8 +1365,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
           } else {
             for (int h = 0; h < raw_halves; ++h) {
               if (p.ga_per) {
-                for (int k = 0; k < p.ga_per; ++k)
-                  tma_load_2d(sp + h * kBM * 128 + k * p.M * 128, &map_a, &full[st], 32 * h, ga_rows[k]);
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  if (k < p.ga_per)
+                    tma_load_2d(sp + h * kBM * 128 + k * p.M * 128, &map_a, &full[st], 32 * h, ga_rows[k]);
               } else {
                 tma_load_2d(sp + h * kBM * 128, &map_a, &full[st], 32 * h, a_row0);
               }
@@ -1303,10 +1387,22 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t it = 0;
     for (uint64_t t = cta0; t < tiles && (!PAIR || rank == 0); t += ncta, ++it, ra.next(static_cast<int>(n_acc))) {
       const uint32_t tb = static_cast<uint32_t>(ra.slot);
-      if (ra.round > 0) mbar_wait(&acc_empty[tb], (ra.round - 1) & 1);
+      uint32_t dacc, d1, d2;
+      if (split) {
+        const uint32_t i32 = static_cast<uint32_t>(it);
+        if (i32 >= 1) mbar_wait(&acc_empty[0], (i32 - 1) & 1);
+        if (i32 >= 2) mbar_wait(&res_free[i32 & 1], ((i32 - 2) >> 1) & 1);
+        dacc = tmem + ((i32 & 1) ? 3 * p.bn : 0);
+        d1 = tmem + p.bn;
+        d2 = tmem + 2 * p.bn;
+      } else {
+        if (ra.round > 0) mbar_wait(&acc_empty[tb], (ra.round - 1) & 1);
+        dacc = tmem + tb * buf_cols;
+        d1 = dacc + p.bn;
+        d2 = dacc + 2 * p.bn;
+      }
       if (lane == 0) trace(p, it, 2);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t dacc = tmem + tb * buf_cols;
       for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
         const int st = rg.slot;
         if constexpr (QA && !PAIR)
@@ -1315,7 +1411,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           mbar_wait(&conv[st], rg.round & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sp = smem_u32(base + st * stage_bytes);
-        mma_stage_i8<PAIR>(dacc, static_cast<uint32_t>(p.bn), sw_desc<16>(sp), sw_desc<16>(sp + a_span), kPlaneA,
+        mma_stage_i8<PAIR>(dacc, d1, d2, sw_desc<16>(sp), sw_desc<16>(sp + a_span), kPlaneA,
                            static_cast<uint32_t>(plane_b), idesc, s > 0 ? 1u : 0u);
         if constexpr (PAIR)
           mma_commit_pair_elect(&empty[st]);
@@ -1354,17 +1450,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
       if (r == 0) trace(p, cit, 4);
       uint8_t* sp = base + st * stage_bytes;
       float4 v[16];
-      float mx = 0.f;
+      float m[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         const int h = c >> 3, cc = c & 7;
-        if (h && !two) {
-          v[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-          continue;
-        }
-        v[c] = reinterpret_cast<const float4*>(sp + h * kBM * 128 + r * 128)[cc ^ (r & 7)];
-        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w))));
+        v[c] = h && !two ? make_float4(0.f, 0.f, 0.f, 0.f)
+                         : reinterpret_cast<const float4*>(sp + h * kBM * 128 + r * 128)[cc ^ (r & 7)];
+        m[c] = fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w)));
       }
+#pragma unroll
+      for (int w = 8; w > 0; w >>= 1)  // tree: 4 dependent steps, not 16
+#pragma unroll
+        for (int c = 0; c < w; ++c) m[c] = fmaxf(m[c], m[c + w]);
+      const float mx = m[0];
       const int sa = i8_scale_exp(mx);
       const float sc = pow2f_wide(sa);
       asm volatile("bar.sync 3, %0;" ::"r"(32 * p.n_conv) : "memory");  // every raw read done (in place)
@@ -1425,18 +1523,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const uint64_t it_step = split ? 1 : n_epi;
     uint32_t nxt_bunit = 0;
     int nxt_m0 = 0, nxt_n0 = 0, nxt_sa = 0;
+    // next tile's row offset: the table halves are loaded one tile ahead and
+    // added when consumed (no stall on the loads inside fetch)
     uint64_t om = 0, nxt_om = 0;
+    uint32_t nxt_om_lo = 0, nxt_om_hi = 0;
+    bool nxt_direct = false;
     uint64_t key = ~uint64_t{0}, nxt_key = ~uint64_t{0}, table_key = ~uint64_t{0};
     int64_t my_coff = -1, nxt_coff = -1;
     float my_cs = 0.f, nxt_cs = 0.f;
     uint32_t cached_u = ~0u, cached_entry = 0;
     TileWalk w;
-    w.init(t, t_step, tiles_n, tiles_m);
+    w.init(t, tiles_n, tiles_m);
+    const Steps ws = make_steps(t_step);
     auto fetch = [&]() {
       const uint32_t u = w.u;
       nxt_m0 = static_cast<int>(w.m) * kTM + m_off;
       nxt_n0 = static_cast<int>(w.n) * p.bn;
       nxt_bunit = u;
+      nxt_direct = p.ga_per != 0;
       if (p.ga_per) {  // row r = item slot r / M, m = r % M
         const uint32_t* tl = p.ga_tiles + static_cast<uint64_t>(w.m) * (1 + p.ga_per);
         nxt_bunit = __ldg(tl);
@@ -1446,7 +1550,16 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                   p.tom(r % p.M);
         if (QA) nxt_sa = itm == ~0u ? 0 : __ldg(p.sa + uint64_t{__ldg(p.ia + itm)} * p.M + r % p.M);
       } else {
-        nxt_om = nxt_m0 + r < p.M ? uint64_t{p.tom(nxt_m0 + r)} : ~uint64_t{0};
+        const bool valid = nxt_m0 + r < p.M;
+        const uint32_t x = valid ? static_cast<uint32_t>(nxt_m0 + r) : 0u;
+        if (p.tom_cache) {
+          nxt_om_lo = tom_s[x & (tom_lo_n - 1)];
+          nxt_om_hi = tom_s[tom_lo_n + (x >> p.tom.lo_bits)];
+        } else {
+          nxt_om_lo = __ldg(p.tom.lo + (x & (tom_lo_n - 1)));
+          nxt_om_hi = __ldg(p.tom.hi + (x >> p.tom.lo_bits));
+        }
+        nxt_om = valid ? 0 : ~uint64_t{0};
         if (QA) {
           if (u != cached_u) {
             cached_u = u;
@@ -1455,7 +1568,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           nxt_sa = nxt_m0 + r < p.M ? __ldg(p.sa + uint64_t{cached_entry} * p.M + nxt_m0 + r) : 0;
         }
       }
-      w.advance();
+      w.advance(ws);
       const uint64_t k = (uint64_t{nxt_bunit} << 20) | static_cast<uint32_t>(nxt_n0);
       if (k != nxt_key) {
         nxt_key = k;
@@ -1465,14 +1578,109 @@ __global__ void __launch_bounds__(kPThreads, 1)
     };
     if (t < tiles) fetch();
     const uint32_t acc_empty_leader = PAIR ? mapa(acc_empty, 0) : 0u;
+    // ring positions of this group's current tile: accumulator buffer and
+    // row-exponent slot (no 64-bit divisions per tile)
+    uint32_t tb = split ? 0u : static_cast<uint32_t>(it) % n_acc, tb_round = split ? 0u : static_cast<uint32_t>(it) / n_acc;
+    uint32_t sa_slot = static_cast<uint32_t>(it), sa_round = 0;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const bool wide = p.Kr > 1024;
+    // scatter one 32-column chunk (16 complex columns from cc) of this lane's
+    // row, scaled, to the output
+    auto store_chunk = [&](float (&v)[32], int cc, float rs) {
+      float cs[16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 c4 = reinterpret_cast<const float4*>(csf + cc)[j];
+        cs[4 * j] = c4.x * rs;
+        cs[4 * j + 1] = c4.y * rs;
+        cs[4 * j + 2] = c4.z * rs;
+        cs[4 * j + 3] = c4.w * rs;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= cs[j / 2];
+      if (p.transpose) {
+        float* buf = stage_out + (warp - e0) * 32 * 33;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = v[j];
+        __syncwarp();
+        const int64_t co = coff[cc + (lane & 15)];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float2 vals[8];
+          uint64_t roms[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int e = lane + 32 * (8 * h + i);
+            const int row = e >> 4, cj = e & 15;
+            roms[i] = __shfl_sync(0xffffffffu, om, row);
+            vals[i] = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
+          }
+          if (co < 0) continue;
+          float2* colp = p.out + co;
+          if (accumulate) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (roms[i] != ~uint64_t{0}) {
+                const float2 old = colp[roms[i]];
+                vals[i].x += old.x;
+                vals[i].y += old.y;
+              }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (roms[i] != ~uint64_t{0}) colp[roms[i]] = vals[i];
+        }
+        __syncwarp();
+        return;
+      }
+      if (om == ~uint64_t{0}) return;
+      float2* rowp = p.out + om;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int64_t co[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const longlong2 t2 = reinterpret_cast<const longlong2*>(coff + cc + 8 * h)[j];
+          co[2 * j] = t2.x;
+          co[2 * j + 1] = t2.y;
+        }
+        const float* vh = v + 16 * h;
+        if (p.n_contig && !accumulate) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (co[2 * j] >= 0)
+              *reinterpret_cast<float4*>(rowp + co[2 * j]) =
+                  make_float4(vh[4 * j], vh[4 * j + 1], vh[4 * j + 2], vh[4 * j + 3]);
+        } else if (!accumulate) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (co[j] >= 0) rowp[co[j]] = make_float2(vh[2 * j], vh[2 * j + 1]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (co[j] >= 0) {
+              const float2 old = rowp[co[j]];
+              rowp[co[j]] = make_float2(old.x + vh[2 * j], old.y + vh[2 * j + 1]);
+            }
+        }
+      }
+    };
+    auto epi_arrive = [&](uint64_t* bar, uint32_t leader_addr) {
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      if constexpr (PAIR) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_addr);
+      } else {
+        mbar_arrive(bar);
+      }
+    };
+    const uint32_t res_free_leader = PAIR ? mapa(res_free, 0) : 0u;
     for (; t < tiles; t += t_step, it += it_step) {
-      const int m0 = nxt_m0;
-      om = nxt_om;
+      om = nxt_direct || nxt_om == ~uint64_t{0} ? nxt_om : uint64_t{nxt_om_lo + nxt_om_hi};
       key = nxt_key;
       my_coff = nxt_coff;
       my_cs = nxt_cs;
       int sa = nxt_sa;
-      (void)m0;
       if (t + t_step < tiles) fetch();
       if (key != table_key) {  // uniform across the group
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));
@@ -1483,97 +1691,56 @@ __global__ void __launch_bounds__(kPThreads, 1)
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));
         table_key = key;
       }
-      const uint32_t tb = static_cast<uint32_t>(it % n_acc);
-      mbar_wait(&acc_full[tb], static_cast<uint32_t>(it / n_acc) & 1);
+      if (warp == e0 && lane == 0) trace(p, it, 7);
+      mbar_wait(&acc_full[tb], tb_round & 1);
       if constexpr (!QA) {
-        const int slot = static_cast<int>(it % kSaRing);
-        mbar_wait(&sa_full[slot], static_cast<uint32_t>(it / kSaRing) & 1);
-        sa = sa_ring[slot * kBM + r];
+        mbar_wait(&sa_full[sa_slot], sa_round & 1);
+        sa = sa_ring[sa_slot * kBM + r];
       }
-      const float rs = pow2f_wide(16 - sa);
+      const float rs = pow2f_wide(24 - sa);  // result = 2^(24 - sa - sb) v
       if (warp == e0 && lane == 0) trace(p, it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t tacc = tmem + tb * buf_cols + (static_cast<uint32_t>(quarter * 32) << 16);
-      const int c_first = split ? 32 * eg : 0, c_step = split ? 32 * n_epi : 32;
-      for (int c0 = c_first; c0 < p.bn; c0 += c_step) {
-        const int cc = c0 / 2;  // first complex column of this chunk
-        float v[32];
-        i8_load_combine(tacc + c0, p.bn, v);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= rs * csf[cc + j / 2];
-        if (p.transpose) {
-          float* buf = stage_out + (warp - e0) * 32 * 33;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = v[j];
-          __syncwarp();
-          const int64_t co = coff[cc + (lane & 15)];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float2 vals[8];
-            uint64_t roms[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int e = lane + 32 * (8 * h + i);
-              const int row = e >> 4, cj = e & 15;
-              roms[i] = __shfl_sync(0xffffffffu, om, row);
-              vals[i] = make_float2(buf[row * 33 + 2 * cj], buf[row * 33 + 2 * cj + 1]);
-            }
-            if (co < 0) continue;
-            if (accumulate) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (roms[i] != ~uint64_t{0}) {
-                  const float2 old = p.out[co + roms[i]];
-                  vals[i].x += old.x;
-                  vals[i].y += old.y;
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              if (roms[i] != ~uint64_t{0}) p.out[co + roms[i]] = vals[i];
-          }
-          __syncwarp();
-          continue;
+      if (split) {
+        const uint32_t i32 = static_cast<uint32_t>(it);
+        const uint32_t t0 = tmem + ((i32 & 1) ? 3 * p.bn : 0) + lane_base;
+        // phase 1: combined fp32 into the acc0 columns; acc1 / acc2 released
+        for (int c0 = 32 * eg; c0 < p.bn; c0 += 32 * n_epi) {
+          float v[32];
+          i8_load_combine(t0 + c0, tmem + p.bn + lane_base + c0, tmem + 2 * p.bn + lane_base + c0, wide, v);
+          tmem_st32(t0 + c0, v);
         }
-        if (om == ~uint64_t{0}) continue;
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        epi_arrive(&acc_empty[0], acc_empty_leader);
+        // phase 2: scatter (overlaps the next tile's main loop)
+        for (int c0 = 32 * eg; c0 < p.bn; c0 += 32 * n_epi) {
+          float v[32];
+          uint32_t u[32];
+          tmem_ld32(t0 + c0, u);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          int64_t co[8];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const longlong2 t2 = reinterpret_cast<const longlong2*>(coff + cc + 8 * h)[j];
-            co[2 * j] = t2.x;
-            co[2 * j + 1] = t2.y;
-          }
-          const float* vh = v + 16 * h;
-          if (p.n_contig && !accumulate) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              if (co[2 * j] >= 0)
-                *reinterpret_cast<float4*>(p.out + co[2 * j] + om) =
-                    make_float4(vh[4 * j], vh[4 * j + 1], vh[4 * j + 2], vh[4 * j + 3]);
-          } else if (!accumulate) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (co[j] >= 0) p.out[co[j] + om] = make_float2(vh[2 * j], vh[2 * j + 1]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (co[j] >= 0) {
-                const float2 old = p.out[co[j] + om];
-                p.out[co[j] + om] = make_float2(old.x + vh[2 * j], old.y + vh[2 * j + 1]);
-              }
-          }
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(u[j]);
+          store_chunk(v, c0 / 2, rs);
         }
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      if constexpr (PAIR) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(acc_empty_leader + 8u * tb);
+        epi_arrive(&res_free[i32 & 1], res_free_leader + 8u * (i32 & 1));
       } else {
-        mbar_arrive(&acc_empty[tb]);
+        const uint32_t tacc = tmem + tb * buf_cols + lane_base;
+        for (int c0 = 0; c0 < p.bn; c0 += 32) {
+          float v[32];
+          i8_load_combine(tacc + c0, tacc + p.bn + c0, tacc + 2 * p.bn + c0, wide, v);
+          store_chunk(v, c0 / 2, rs);
+        }
+        epi_arrive(&acc_empty[tb], acc_empty_leader + 8u * tb);
       }
       if (warp == e0 && lane == 0) trace(p, it, 6);
+      tb += static_cast<uint32_t>(it_step);
+      while (tb >= n_acc) {
+        tb -= n_acc;
+        ++tb_round;
+      }
+      sa_slot += static_cast<uint32_t>(it_step);
+      if (sa_slot >= kSaRing) {
+        sa_slot -= kSaRing;
+        ++sa_round;
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -2008,9 +2175,13 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   const int bn_cta = pair ? bn / 2 : bn;
   const bool transpose = !op.m_contig && bn <= 64;
   const int n_conv = qa ? (pair ? 1 : 0) : 4;  // QA pair: one relay warp
-  const int extra = 1024 + 8 * (3 * kMaxStages + 2 * kMaxAcc + kSaRing) + 16 +
+  const int extra0 = 1024 + 8 * (3 * kMaxStages + 2 * kMaxAcc + 2 + kSaRing) + 16 +
                     4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) + 16 + 8 * kEpiGroups * (kMaxBn / 2) +
                     4 * kEpiGroups * (kMaxBn / 2) + kSaRing * kBM + (transpose ? 4 * 4 * kEpiGroups * 32 * 33 : 0);
+  // output row offset table in shared memory when it is small (<= 12 KB)
+  const uint64_t tom_words = (uint64_t{1} << op.tom_bits) + ((M >> op.tom_bits) ? (M >> op.tom_bits) : 1);
+  const int tom_cache = !ga && tom_words <= 3072 ? static_cast<int>(tom_words) : 0;
+  const int extra = extra0 + 4 * tom_cache;
   constexpr int kSmemMax = 227 * 1024;
   const int stage_bytes = (qa ? 3 * kBM * kI8Kb : 2 * kBM * 128) + 3 * bn_cta * kI8Kb;
   const int n_stages = std::max(2, std::min(kMaxStages, (kSmemMax - extra) / stage_bytes));
@@ -2050,6 +2221,7 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   p.n_conv = n_conv;
   p.sa = op.row_exp;
   p.sb = op.col_exp;
+  p.tom_cache = tom_cache;
   p.dbg = nullptr;
   const int slot = 4 + (pair ? 2 : 0) + (qa ? 1 : 0);
   auto kern = pair ? (qa ? tc_i8_persistent<true, true> : tc_i8_persistent<true, false>)
@@ -2089,13 +2261,14 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
     const unsigned long long t0 = h[0];
     std::fprintf(stderr, "[tc trace node %d] i8 pair=%d qa=%d stages=%d bn=%d tiles=%llu grid=%u\n", op.node,
                  pair ? 1 : 0, qa ? 1 : 0, n_stages, bn, static_cast<unsigned long long>(tiles), grid);
-    std::fprintf(stderr, " tile  prod0  prod1  conv  mma0  mma1  epi0  epi1   (cycles from tile0 prod0)\n");
+    std::fprintf(stderr, " tile  prod0  prod1  conv  mma0  mma1  epi-top epi0  epi1   (cycles from tile0 prod0)\n");
     for (int i = 0; i < kTraceTiles; ++i) {
       if (!h[i * 8]) break;
       if (i < 24 || i % 32 == 0)
-        std::fprintf(stderr, " %4d %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", i, (long long)(h[i * 8] - t0),
+        std::fprintf(stderr, " %4d %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", i, (long long)(h[i * 8] - t0),
                      (long long)(h[i * 8 + 1] - t0), (long long)(h[i * 8 + 4] - t0), (long long)(h[i * 8 + 2] - t0),
-                     (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 5] - t0), (long long)(h[i * 8 + 6] - t0));
+                     (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 7] - t0), (long long)(h[i * 8 + 5] - t0),
+                     (long long)(h[i * 8 + 6] - t0));
     }
   }
   return launches;
