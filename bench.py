@@ -36,6 +36,10 @@ WORKLOADS = {
     "cfg1": dict(rows=3, cols=4, layers=8, k=1000,
                  text="cfg1: synthetic 12-qubit 3x4 grid, m=8 (grid_circuit seed 12345, "
                       "fused), 1000 random bitstrings (seed 99), plans/cfg1.plan (no slicing)"),
+    "cal45": dict(rows=4, cols=5, layers=10, k=1000,
+                  text="cal45: synthetic 20-qubit 4x5 grid, m=10 (grid_circuit seed 12345, fused), "
+                       "1000 random bitstrings (seed 99), plans/cal45.plan (3 sliced legs); the "
+                       "reference arm's calibration run"),
     "cfg2": dict(rows=5, cols=6, layers=12, k=10000,
                  text="cfg2: synthetic 30-qubit 5x6 grid, m=12 (grid_circuit seed 12345, "
                       "fused), 10^4 random bitstrings (seed 99), plans/cfg2.plan "
@@ -124,135 +128,141 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(problem, circ, bits, plan_text, threads: int):
-    """Reference CPU path on this host: bounded sample of the same workload.
+# The one full run of the reference on the bench workload (cfg2): the
+# unmodified reference's eval_sliced over all 16 slices with 8 workers in the
+# dev container (8-core Xeon), tests/golden/make_cfg2_reference.py, which also
+# wrote tests/golden/cfg2_reference.npz; the contract_pair sampler below
+# estimated 1,667 s for that same run on that host.
+CFG2_FULL_RUN = {"seconds": 3952.0, "threads": 8, "host": "dev container, 8-core Intel Xeon",
+                 "sampler_estimate_seconds": 1667.0,
+                 "source": "tests/golden/make_cfg2_reference.py (DESIGN.md §5b)"}
 
-    oracle/_ref (the unmodified reference library): its contract_pair is
-    timed on every node shape of the plan (sub-blocks above 2^24 MACs, scaled
-    linearly) and weighted by the exact per-node evaluation counts ->
-    single-thread time of eval_sliced; eval_sliced runs slices on `threads`
-    workers, so T = T1 / min(threads, S). Returns the dict for the JSON line.
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ref_problem(R, name: str):
+    """The workload built by the REFERENCE's own producers: its grid_circuit
+    and random_bitstrings test generators (proj/tests/support/gen.cpp:54-107)
+    and its circuit / diagram / assignment / plan parsers."""
+    w = WORKLOADS[name]
+    circ = R.grid_circuit(w["rows"], w["cols"], w["layers"], 12345)
+    bits = R.random_bitstrings(99, w["rows"] * w["cols"], w["k"])
+    plan = open(os.path.join(ROOT, "plans", f"{name}.plan")).read()
+    return R.RefProblem(circ, bits, plan, fuse=True)
+
+
+def ref_calibration(R, threads: int):
+    """Real end-to-end runs of the unmodified reference on this host, timed
+    beside the sampler's estimate of the same runs: cal45 (4x5 grid, m=10,
+    10^3 bitstrings, 3 sliced legs; eval_sliced with all threads) and cfg1
+    (eval_all, single-threaded by the reference's contract)."""
+    out = {}
+    for name, mode, workers in (("cal45", "sliced", threads), ("cfg1", "all", 1)):
+        p = ref_problem(R, name)
+        S = 1 << len(p.plan_sliced())
+        p.eval(mode, workers)  # warm
+        best = min(_timed(lambda: p.eval(mode, workers)) for _ in range(3))
+        est1, _, _ = p.sample_eval_time(1 << 24, threads)
+        est = est1 / min(workers, S)
+        out[name] = {"real_seconds": best, "sampler_seconds": est, "ratio": best / est,
+                     "workers": workers, "amplitudes_per_s": p.n_requests / best,
+                     "mode": f"eval_{mode}"}
+    return out
+
+
+def _timed(f):
+    t0 = time.perf_counter()
+    f()
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(threads: int, config: str = "cfg2"):
+    """The reference CPU path on this host, on a bounded sample of the same
+    workload, entirely through oracle/_ref (the unmodified reference library;
+    nothing of this engine is loaded on this path):
+
+      * a full cfg2 evaluation costs hours of CPU (CFG2_FULL_RUN), so the
+        sample times the reference's own contract_pair (tensor.cpp:150-253)
+        on every node shape of the plan (nodes above 2^24 MACs on projected
+        sub-blocks, scaled linearly), weighted by the exact per-node
+        evaluation counts x slices (ref_sample_eval_time) -> T1, single-
+        thread seconds; eval_sliced runs slices on the host's threads, so
+        T = T1 / min(threads, S);
+      * that estimate is scaled by the ratio real / sampled measured in the
+        same job on the calibration workload (a real end-to-end eval_sliced);
+      * the algorithmic flops come from the reference's CostedPlan exact
+        totals (plan.cpp:338-371), not from this engine.
     """
-    from oracle import refimpl
+    from oracle import refimpl as R
 
-    from paper_2108_05665_b200 import network as N
-
-    S = 1 << len(problem.sliced)
-    if refimpl.available():
-        p = refimpl.RefProblem(N.format_circuit(circ), bits, plan_text, fuse=True)
-        est1, wall, frac = p.sample_eval_time(1 << 24, threads)
-        kind = "reference"
-    else:
-        est1, wall, frac = port_sample_eval_time(problem, threads)
-        kind = "port"
-    t = est1 / min(threads, S)
-    k = problem.n_requests
+    if not R.available():
+        raise RuntimeError("reference library oracle/_ref/libmtcref.so not built")
+    p = ref_problem(R, config)
+    S = 1 << len(p.plan_sliced())
+    cal = ref_calibration(R, threads)
+    est1, wall, frac = p.sample_eval_time(1 << 24, threads)
+    ratio = cal["cal45"]["ratio"]
+    t = est1 / min(threads, S) * ratio
+    k = p.n_requests
+    full = dict(CFG2_FULL_RUN)
+    full["ratio_real_over_sampler"] = full["seconds"] / full["sampler_estimate_seconds"]
+    full["amplitudes_per_s_if_that_ratio_applies_here"] = (
+        k / (est1 / min(threads, S) * full["ratio_real_over_sampler"]))
     return {
-        "value": k / t, "unit": "amplitudes/s", "cores": min(threads, S), "kind": kind,
-        "sample": (f"contract_pair (tensor.cpp:150-253, ~94% of eval time) timed on all "
-                   f"{sum(1 for s in problem.node_slot if s < 0)} node shapes of the plan "
-                   f"({frac * 100:.2f}% of per-slice MACs executed, larger nodes on projected "
-                   f"sub-blocks scaled linearly), weighted by exact per-node counts x {S} "
-                   f"slices; eval_sliced with {min(threads, S)} workers; sampling took "
-                   f"{wall:.1f}s on {threads} threads"),
-        "est_seconds_full_eval": t,
-        "est_seconds_1thread": est1,
+        "value": k / t, "unit": "amplitudes/s", "cores": min(threads, S), "kind": "reference",
+        "sample": (f"reference contract_pair timed on all node shapes of the plan "
+                   f"({frac * 100:.2f}% of per-slice MACs executed; larger nodes on projected "
+                   f"sub-blocks, scaled linearly), weighted by exact per-node counts x {S} slices, "
+                   f"eval_sliced with {min(threads, S)} workers, scaled by real/sampled = "
+                   f"{ratio:.3f} from a real end-to-end eval_sliced of cal45 in this job; "
+                   f"sampling {wall:.1f}s on {threads} threads of {cpu_model()}"),
+        "seconds_per_evaluation": t,
+        "sampler_seconds_1thread": est1,
+        "calibration": cal,
+        "cfg2_full_run": full,
+        "cpu_model": cpu_model(),
+        "mults": int(p.exact_totals()["mults"]),
     }
-
-
-def port_sample_eval_time(problem, threads):
-    """Same sampling with the C restatement (oracle/liboracle.so) when the
-    reference build is absent."""
-    import ctypes as C
-
-    from oracle import oracle as O
-    from paper_2108_05665_b200.engine import emulate_arrays
-
-    em = emulate_arrays(problem)
-    L = O.lib()
-    sl = set(int(x) for x in problem.sliced)
-    legs = {}
-    n = problem.n_nodes
-    order = []
-
-    def visit(x):
-        if problem.node_slot[x] >= 0:
-            j = int(problem.node_slot[x])
-            legs[x] = [int(l) for l in problem.slot_legs[problem.slot_leg_begin[j]:
-                                                         problem.slot_leg_begin[j + 1]]
-                       if int(l) not in sl]
-            return
-        visit(int(problem.node_left[x]))
-        visit(int(problem.node_right[x]))
-        a, b = legs[int(problem.node_left[x])], legs[int(problem.node_right[x])]
-        legs[x] = sorted(set(a) ^ set(b))
-        order.append(x)
-
-    visit(int(problem.root))
-    rng = np.random.default_rng(0)
-    total, t0 = 0.0, time.time()
-    for x in order:
-        if em.node_contractions[x] == 0:
-            continue
-        a = list(legs[int(problem.node_left[x])])
-        b = list(legs[int(problem.node_right[x])])
-        closed = sorted(set(a) & set(b))
-        scale = 1.0
-        while (1 << (len(set(a) ^ set(b)) + len(closed))) > (1 << 24):
-            big = a if len(a) >= len(b) else b
-            free = [l for l in big if l not in closed]
-            if not free:
-                break
-            big.remove(free[0])
-            scale *= 2
-        da = (rng.random(2 << len(a)) - 0.5)
-        db = (rng.random(2 << len(b)) - 0.5)
-        nr = len(set(a) ^ set(b))
-        out = np.zeros(2 << nr)
-        ol, od = np.zeros(64, np.uint32), np.zeros(64, np.uint32)
-        u32 = lambda v: np.array(v, dtype=np.uint32)
-        aa, bb, cc = u32(a), u32(b), u32(closed)
-        dims_a, dims_b = u32([2] * len(a)), u32([2] * len(b))
-        P = lambda arr, ct: arr.ctypes.data_as(C.POINTER(ct))
-        s = time.perf_counter()
-        L.orc_contract_pair(len(a), P(aa, C.c_uint32), P(dims_a, C.c_uint32), P(da, C.c_double),
-                            len(b), P(bb, C.c_uint32), P(dims_b, C.c_uint32), P(db, C.c_double),
-                            len(closed), P(cc, C.c_uint32), P(ol, C.c_uint32), P(od, C.c_uint32),
-                            P(out, C.c_double), None)
-        total += (time.perf_counter() - s) * scale * float(em.node_contractions[x])
-    return total, time.time() - t0, float("nan")
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    problem, circ, bits, plan_text = load_workload(args.config)
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_baseline(problem, circ, bits, plan_text, threads)
+        cpu_baseline(threads, args.config)
     times, base = [], None
     for _ in range(args.steps):
-        base = cpu_baseline(problem, circ, bits, plan_text, threads)
-        times.append(base["est_seconds_full_eval"])
+        base = cpu_baseline(threads, args.config)
+        times.append(base["seconds_per_evaluation"])
     t = statistics.mean(times)
-    k = problem.n_requests
-    from paper_2108_05665_b200.engine import emulate_arrays
-
-    mults = emulate_arrays(problem).counters.mults
+    w = WORKLOADS[args.config]
+    k = w["k"]
     value = k / t
     line = {
         "metric": METRIC, "value": value, "unit": "amplitudes/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config]["text"], "n_qubits": circ.n_qubits,
-                   "bitstrings": k, "slices": 1 << len(problem.sliced)},
-        "effective_tflops": 8 * mults / t / 1e12,
+        "config": {"workload": w["text"], "n_qubits": w["rows"] * w["cols"], "bitstrings": k},
+        "effective_tflops": 8 * base["mults"] / t / 1e12,
         "cpu_baseline": {key: base[key] for key in ("value", "unit", "cores", "kind", "sample")},
+        "calibration": base["calibration"],
+        "cfg2_full_run": base["cfg2_full_run"],
+        "cpu_model": base["cpu_model"],
         "e2e": {"value": value, "unit": "amplitudes/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    line["cpu_baseline"]["value"] = value
     print(json.dumps(line))
     return 0
 
@@ -280,7 +290,8 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
     class OpInfo(C.Structure):
         _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
                     ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
-                    ("mults", C.c_uint64), ("bytes", C.c_uint64)]
+                    ("mults", C.c_uint64), ("bytes", C.c_uint64),
+                    ("compulsory_bytes", C.c_uint64)]
 
     L.mtcg_plan_op_info.argtypes = [C.c_void_p, C.c_int32, C.POINTER(OpInfo)]
     ops = []
@@ -308,18 +319,25 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
             traffic = None
     scheme = {}
     if bound == "tensor" and top.kernel == 12:
-        # split-precision complex GEMM: every real MAC costs 3 tensor-core MMAs
-        # (hi*hi + hi*lo + lo*hi) at the fp16 rate (3xFP16, default) or at half
-        # of it (3xTF32, MTCG_TC_KIND=tf32)
-        tf32 = os.environ.get("MTCG_TC_KIND") == "tf32"
-        ceiling = peak / (6.0 if tf32 else 3.0)
-        scheme = {"scheme": "3xTF32" if tf32 else "3xFP16 (power-of-2 scaled fp16 hi/lo)",
+        # complex GEMM as one real GEMM (8 flops per complex MAC); default:
+        # split integer — 6 int8 MMAs per real MAC (3 balanced digits per
+        # operand, digit products of weight 0..2) at twice the bf16 rate =
+        # 3 bf16-MMA equivalents, so the ceiling is the bf16 peak / 3 (the
+        # int8 peak is not measured on this pool: 2x bf16, as nominal);
+        # legacy MTCG_TC_KIND=f16 (3xFP16) / tf32 (3xTF32, half rate)
+        kind = os.environ.get("MTCG_TC_KIND", "i8")
+        ceiling = peak / (6.0 if kind == "tf32" else 3.0)
+        scheme = {"scheme": {"tf32": "3xTF32", "f16": "3xFP16 (power-of-2 scaled fp16 hi/lo)"}.get(
+                      kind, "split integer: 3 balanced int8 digits per operand, 6 kind::i8 MMAs per "
+                            "real MAC, exact s32 accumulation"),
                   "scheme_ceiling": ceiling, "frac_of_scheme_ceiling": achieved / ceiling}
     # The whole slice against SURVEY §8(d)'s roofline: T_roof = sum over ops of
-    # max(F_n / P_cplx, B_n / BW), F_n and B_n the reference's algorithmic
-    # flops (8 per complex MAC) and bytes (rw x 8 B), P_cplx the 3xFP16
-    # scheme ceiling, BW the measured copy peak. Fused-chain members launch
-    # nothing of their own (0 ms): their work is charged to the chain's tail.
+    # max(F_n / P_cplx, B_n / BW), F_n the reference's algorithmic flops (8 per
+    # complex MAC), B_n the op's compulsory bytes (every distinct operand
+    # entry read once, every output written once; fused-chain intermediates
+    # never reach HBM), P_cplx the scheme ceiling, BW the measured copy peak.
+    # Fused-chain members launch nothing of their own (0 ms): their work is
+    # charged to the chain's tail.
     p_cplx = tensor_tflops * 1e12 / 3.0
     bw = hbm_gbs * 1e9
     t_roof = 0.0
@@ -327,7 +345,7 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
     pend_f = pend_b = 0.0
     for m, oi in ops:
         f = 8.0 * oi.mults + pend_f
-        b = float(oi.bytes) + pend_b
+        b = float(oi.compulsory_bytes) + pend_b
         if m <= 0.0:
             pend_f, pend_b = f, b
             continue
@@ -347,9 +365,9 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
         "tensor_bound_tflops": cls["tensor"][2] / cls["tensor"][1] / 1e12 if cls["tensor"][1] else None,
         "hbm_bound_ops": cls["hbm"][3],
         "hbm_bound_frac": cls["hbm"][0] / cls["hbm"][1] if cls["hbm"][1] else None,
-        "note": ("per slice (slice 0, ops serialised with CUDA events); algorithmic bytes "
-                 "count an operand once per item, so grouped ops (A shared by a group) can "
-                 "exceed the copy peak — measured DRAM bytes per op: profiles/r01/op_traffic.txt"),
+        "note": ("per slice (slice 0, ops serialised with CUDA events); bytes are compulsory "
+                 "bytes (distinct operand entries once + outputs once), a lower bound on DRAM "
+                 "traffic — measured DRAM bytes per op: profiles/r02/op_traffic.txt"),
     }
     return {
         **scheme,
@@ -363,6 +381,37 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
         "peak_source": f"{peak_src} ({'bf16 dense' if bound == 'tensor' else 'copy'})",
         "slice_ms_serialised": slice_ms,
     }
+
+
+def parity_check(cp, acc, config, n_qubits, xeb_dev):
+    """Same-run parity of the benched output (the accumulator of the last
+    timed step) against the reference's own complex128 amplitudes
+    (tests/golden/cfg2_reference.npz: a full eval_sliced run of the
+    unmodified reference). Gates (BASELINE §3 / SURVEY §8c): per amplitude
+    |a - a_ref| <= 1e-4 max(|a_ref|, 2^-n/2), relative L2 <= 1e-4,
+    |dF| <= 1e-4 (|F| + 1/sqrt(k)); node_contractions and the exact
+    counters identical."""
+    path = os.path.join(ROOT, "tests", "golden", f"{config}_reference.npz")
+    if not os.path.exists(path):
+        return {"available": False, "reason": f"no golden for {config}"}
+    g = np.load(path)
+    r = cp.fetch(acc.data_ptr())
+    got = r.amplitudes
+    want = g["amplitudes"].reshape(got.shape)
+    floor = 2.0 ** (-n_qubits / 2)
+    max_rel = float(np.max(np.abs(got - want) / np.maximum(np.abs(want), floor)))
+    l2 = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+    k = want.shape[0]
+    f_ref = math.ldexp(math.fsum((np.abs(want) ** 2).ravel().tolist()) / want.size, n_qubits) - 1.0
+    df = float(xeb_dev - f_ref)
+    gate_f = 1e-4 * (abs(f_ref) + 1 / math.sqrt(k))
+    nc_equal = bool(np.array_equal(r.node_contractions, g["node_contractions"]))
+    cnt_equal = (r.counters.mults, r.counters.adds, r.counters.rw) == tuple(int(x) for x in g["counters"])
+    return {"against": "tests/golden/cfg2_reference.npz (reference eval_sliced, complex128)",
+            "max_rel": max_rel, "l2_rel": l2, "xeb": xeb_dev, "xeb_ref": f_ref, "dF": df,
+            "dF_gate": gate_f, "node_contractions_equal": nc_equal, "counters_equal": cnt_equal,
+            "pass": bool(max_rel <= 1e-4 and l2 <= 1e-4 and abs(df) <= gate_f and nc_equal
+                         and cnt_equal)}
 
 
 def run_engine(args):
@@ -531,14 +580,18 @@ def run_engine(args):
     h2d = int(cp.info.hbm_resident_bytes + k * cp.info.row_elems * 16)
     d2h = int(cp.info.n_rows * cp.info.row_elems * cp.complex_dtype_bytes + 2 * 8 * 592)
 
+    parity = None
+    if rank == 0:
+        parity = parity_check(cp, acc, args.config, n_qubits, xeb)
     if rank == 0:
         hbm, tflops, src = measured_peaks()
         roof = roofline_for(cp, acc, stream, ms_per_step, hbm, tflops, src)
         base = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                base = cpu_baseline(problem, circ, bits, plan_text, os.cpu_count() or 1)
-                base = {key: base[key] for key in ("value", "unit", "cores", "kind", "sample")}
+                b = cpu_baseline(os.cpu_count() or 1, args.config)
+                base = {key: b[key] for key in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
+                base["cfg2_full_run"] = b["cfg2_full_run"]
             except Exception as e:  # noqa: BLE001
                 base = {"value": None, "unit": "amplitudes/s", "cores": 0, "kind": "reference",
                         "sample": f"unavailable: {e}"}
@@ -554,6 +607,7 @@ def run_engine(args):
                               "> 126 MB L2 (no flush needed)")},
             "effective_tflops": 8 * mults * args.steps / (t_ms * 1e-3) / 1e12,
             "xeb": xeb,
+            "parity": parity,
             "roofline": roof,
             "cpu_baseline": base,
             "e2e": {"value": e2e_value, "unit": "amplitudes/s", "h2d_bytes_per_step": h2d,

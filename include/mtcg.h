@@ -250,6 +250,10 @@ typedef struct mtcg_op_info {
   uint64_t mults;        /* algorithmic complex MACs per slice */
   uint64_t bytes;        /* algorithmic HBM bytes per slice: |A|+|B|+|out|
                             per item x element size (predicted_cost rw) */
+  uint64_t compulsory_bytes; /* bytes this launch cannot avoid: every distinct
+                            A and B entry read once (slice-projected leaves at
+                            their projected size) + every output written once;
+                            fused-chain members count only what reaches HBM */
 } mtcg_op_info;
 int32_t mtcg_plan_op_count(const mtcg_plan* plan);
 mtcg_status mtcg_plan_op_info(const mtcg_plan* plan, int32_t i, mtcg_op_info* info);

@@ -80,6 +80,14 @@ class mtcg_result(C.Structure):
     ]
 
 
+class mtcg_op_info(C.Structure):
+    """include/mtcg.h mtcg_op_info: one batched launch of a compiled slice."""
+    _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
+                ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
+                ("mults", C.c_uint64), ("bytes", C.c_uint64),
+                ("compulsory_bytes", C.c_uint64)]
+
+
 class mtcg_plan_info(C.Structure):
     _fields_ = [
         ("n_requests", C.c_uint64),

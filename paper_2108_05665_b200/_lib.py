@@ -68,6 +68,10 @@ def lib():
             L.mtcg_xeb_device.argtypes = [vp, vp, C.c_int, vp, dp, cp, sz]
             L.mtcg_launch_count.argtypes = [vp]
             L.mtcg_launch_count.restype = C.c_uint64
+            L.mtcg_plan_op_count.argtypes = [vp]
+            L.mtcg_plan_op_count.restype = C.c_int32
+            L.mtcg_plan_op_info.argtypes = [vp, C.c_int32, C.POINTER(A.mtcg_op_info)]
+            L.mtcg_time_ops.argtypes = [vp, C.c_uint64, vp, C.c_int, vp, C.POINTER(C.c_float), cp, sz]
             _lib = L
         return _lib
 
@@ -77,5 +81,6 @@ EXPORTS = (
     "mtcg_version", "mtcg_create", "mtcg_destroy", "mtcg_eval", "mtcg_linear_xeb",
     "mtcg_linear_xeb_amplitudes", "mtcg_compile", "mtcg_plan_destroy",
     "mtcg_plan_get_info", "mtcg_run", "mtcg_fetch", "mtcg_xeb_device",
-    "mtcg_emulate", "mtcg_launch_count",
+    "mtcg_emulate", "mtcg_launch_count", "mtcg_plan_op_count", "mtcg_plan_op_info",
+    "mtcg_time_ops",
 )

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 
@@ -301,6 +302,16 @@ mtcg_status mtcg_plan_op_info(const mtcg_plan* plan, int32_t i, mtcg_op_info* in
   info->batch = op.nb;
   info->mults = op.mults * op.nb;
   info->bytes = op.rw * op.nb * static_cast<uint64_t>(c.elem_bytes);
+  auto distinct = [](std::vector<uint32_t> v) {
+    std::sort(v.begin(), v.end());
+    return static_cast<uint64_t>(std::unique(v.begin(), v.end()) - v.begin());
+  };
+  const Chain* ch = op.chain >= 0 ? &c.chains[op.chain] : nullptr;
+  const bool reads_a = !ch || ch->head == i, writes_out = !ch || ch->tail == i;
+  uint64_t elems = distinct(op.ib) * (op.b_item >> op.b_slice_stride.size());
+  if (reads_a) elems += distinct(op.ia) * (op.a_item >> op.a_slice_stride.size());
+  if (writes_out) elems += static_cast<uint64_t>(op.nb) * op.out_item;
+  info->compulsory_bytes = elems * static_cast<uint64_t>(c.elem_bytes);
   return MTCG_OK;
 }
 

@@ -171,6 +171,20 @@ class CompiledProblem:
             _raise(st, err)
         return _result_from(res, vals, nc[:p.n_nodes], p.n_requests, w)
 
+    def op_infos(self):
+        """Per-op introspection (mtcg_plan_op_info), in launch order."""
+        L = lib()
+        out = []
+        for i in range(L.mtcg_plan_op_count(self.h)):
+            oi = A.mtcg_op_info()
+            L.mtcg_plan_op_info(self.h, i, C.byref(oi))
+            out.append(oi)
+        return out
+
+    def op_kernels(self):
+        """Kernel configuration of every op (12: tcgen05 tensor-core GEMM)."""
+        return [oi.kernel for oi in self.op_infos()]
+
     def xeb(self, acc_ptr: int, n_qubits: int, stream: int = 0) -> float:
         out = C.c_double()
         err = C.create_string_buffer(1024)

@@ -11,6 +11,8 @@ Workloads (BASELINE.json ``configs``; seeds as in BASELINE.md §2):
         no slicing
   cfg2  grid_circuit(5, 6, 12, 12345), fuse, 10^4 random bitstrings (seed 99),
         4 sliced legs
+  cal45 grid_circuit(4, 5, 10, 12345), fuse, 1000 random bitstrings (seed 99),
+        3 sliced legs (the reference arm's calibration run)
 
 Usage: python plans/make_plans.py [cfg1|cfg2] [--steps N] [--seed S]
 """
@@ -29,6 +31,9 @@ from oracle import refimpl as R  # noqa: E402
 CONFIGS = {
     "cfg1": dict(rows=3, cols=4, layers=8, k=1000, slices=0),
     "cfg2": dict(rows=5, cols=6, layers=12, k=10000, slices=4),
+    # calibration workload of the reference CPU arm (bench.py --impl
+    # reference): small enough that the real eval_sliced runs in ~1 s
+    "cal45": dict(rows=4, cols=5, layers=10, k=1000, slices=3),
 }
 CIRCUIT_SEED = 12345
 BITS_SEED = 99
@@ -53,7 +58,7 @@ def main() -> None:
     a = ap.parse_args()
     c = CONFIGS[a.config]
     p = problem(a.config)
-    steps = a.steps or (200_000 if a.config == "cfg1" else 5_000_000)
+    steps = a.steps or {"cfg1": 200_000, "cal45": 500_000}.get(a.config, 5_000_000)
     interval = a.slice_interval
     if interval is None:
         interval = 0 if c["slices"] == 0 else max(1, steps // (c["slices"] + 1))
@@ -62,6 +67,10 @@ def main() -> None:
                          slice_interval=interval, seed=a.seed, chains=a.chains)
     dt = time.time() - t0
     p.set_plan(plan)
+    missing = c["slices"] - len(p.plan_sliced())
+    if missing > 0:  # the reference's slicing move, greedily (ref_shim ref_add_slices_greedy)
+        p.add_slices_greedy(missing, c["k"], a.m_max, "cost")
+        plan = p.plan_text()
     tot = p.exact_totals()
     n_sliced = len(p.plan_sliced())
     print(f"{a.config}: anneal {dt:.1f}s objective {obj:.3f} sliced {n_sliced} "
