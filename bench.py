@@ -438,11 +438,18 @@ def run_engine(args):
     torch.cuda.set_stream(torch.cuda.Stream())
     stream = torch.cuda.current_stream().cuda_stream
     acc = cp.new_accumulator()
+    # N > 1: deterministic gather (scheduler.py): per-slice values of each
+    # rank's block, one NCCL all-gather, ordered fold on rank 0 — amplitudes
+    # bit-identical for every GPU count
+    from paper_2108_05665_b200.scheduler import SliceScheduler
+
+    sched = SliceScheduler.for_compiled(cp, rank, world, stream=stream) if world > 1 else None
 
     def step():
-        cp.run(s0, s1, acc.data_ptr(), accumulate=False, stream=stream)
-        if world > 1:
-            dist.reduce(acc, dst=0)
+        if sched:
+            sched.step(acc)
+        else:
+            cp.run(s0, s1, acc.data_ptr(), accumulate=False, stream=stream)
         if rank == 0:
             return cp.xeb(acc.data_ptr(), n_qubits, stream=stream)
         return None
@@ -483,11 +490,13 @@ def run_engine(args):
     if not args.no_reuse:
         cpr = eng.compile(problem, 0, EvalOptions(precision=args.precision, slice_reuse=True))
         acc_r = cpr.new_accumulator()
+        sched_r = SliceScheduler.for_compiled(cpr, rank, world, stream=stream) if world > 1 else None
 
         def step_r():
-            cpr.run(s0, s1, acc_r.data_ptr(), accumulate=False, stream=stream)
-            if world > 1:
-                dist.reduce(acc_r, dst=0)
+            if sched_r:
+                sched_r.step(acc_r)
+            else:
+                cpr.run(s0, s1, acc_r.data_ptr(), accumulate=False, stream=stream)
             if rank == 0:
                 return cpr.xeb(acc_r.data_ptr(), n_qubits, stream=stream)
             return None
@@ -535,9 +544,10 @@ def run_engine(args):
         def launch():
             cpn = eng.compile(problem, 0, opts)
             accn = cpn.new_accumulator()
-            cpn.run(s0, s1, accn.data_ptr(), accumulate=False, stream=stream)
             if world > 1:
-                dist.reduce(accn, dst=0)
+                SliceScheduler.for_compiled(cpn, rank, world, stream=stream).step(accn)
+            else:
+                cpn.run(s0, s1, accn.data_ptr(), accumulate=False, stream=stream)
             done = torch.cuda.Event()
             done.record(torch.cuda.current_stream())
             return cpn, accn, done
@@ -602,7 +612,7 @@ def run_engine(args):
             "dtype": args.precision, "data": "synthetic",
             "config": {"workload": WORKLOADS[args.config]["text"], "n_qubits": n_qubits,
                        "bitstrings": k, "slices": S, "slices_per_gpu": f"{s1 - s0}",
-                       "parallelism": f"slices/{world}" + (" + 1 NCCL reduce" if world > 1 else ""),
+                       "parallelism": f"slices/{world}" + (" + 1 NCCL all-gather + ordered fold (bit-identical for any N)" if world > 1 else ""),
                        "l2": (f"per-slice working set {cp.info.hbm_arena_bytes / 1e9:.2f} GB "
                               "> 126 MB L2 (no flush needed)")},
             "effective_tflops": 8 * mults * args.steps / (t_ms * 1e-3) / 1e12,

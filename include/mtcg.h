@@ -58,7 +58,8 @@ typedef enum mtcg_status {
   MTCG_ERR_DATA = 2,
   MTCG_ERR_MEMORY_CAP = 3,
   MTCG_ERR_CUDA = 5,
-  MTCG_ERR_ARGUMENT = 6
+  MTCG_ERR_ARGUMENT = 6,
+  MTCG_ERR_NCCL = 7
 } mtcg_status;
 
 /* Arithmetic of the device path.
@@ -176,6 +177,22 @@ int mtcg_version(void);
  * device arena of every compiled plan (0 = free device memory). */
 mtcg_status mtcg_create(int device, uint64_t hbm_cap_bytes,
                         mtcg_handle** out, char* err, size_t errlen);
+/* An engine over several GPUs of one node: devices[0] is the
+ * root, which holds results and runs the XEB. mtcg_eval distributes the
+ * slices over the first min(options.workers, n_devices) devices
+ * (options.workers = 0: all) — the GPU analogue of EvalOptions.workers,
+ * multieval.hpp:26-29 — in contiguous blocks, gathers every slice's root
+ * values to the root over NVLink (NCCL point-to-point on a communicator
+ * created here) and folds them there in slice order: results are
+ * bit-identical for every device count, like the reference's for every
+ * worker count (multieval.hpp:64-68). A device may repeat (ranks sharing one
+ * GPU: the same arithmetic, device-to-device copies instead of NCCL). The
+ * staged API below runs on the root device. */
+mtcg_status mtcg_create_multi(const int* devices, int n_devices,
+                              uint64_t hbm_cap_bytes_per_gpu, mtcg_handle** out,
+                              char* err, size_t errlen);
+int32_t mtcg_device_count(const mtcg_handle* h);
+int32_t mtcg_visible_devices(void);  /* CUDA devices this process sees */
 void mtcg_destroy(mtcg_handle* h);
 
 /* One-shot evaluation: compile + run all slices + fetch. The drop-in for
@@ -215,6 +232,22 @@ mtcg_status mtcg_plan_get_info(const mtcg_plan* plan, mtcg_plan_info* info);
 mtcg_status mtcg_run(mtcg_plan* plan, uint64_t slice_begin,
                      uint64_t slice_end, void* d_acc, int accumulate,
                      void* stream, char* err, size_t errlen);
+
+/* Per-slice values instead of a fold: runs slices [slice_begin, slice_end)
+ * and writes slice s's root values (n_rows * row_elems complex, plan
+ * precision) to d_out + (s - slice_begin) * n_rows * row_elems — the
+ * per-rank half of a deterministic multi-GPU evaluation (gather, then
+ * mtcg_fold on one rank). Asynchronous with respect to the host. */
+mtcg_status mtcg_run_slices_out(mtcg_plan* plan, uint64_t slice_begin,
+                                uint64_t slice_end, void* d_out, void* stream,
+                                char* err, size_t errlen);
+/* d_acc = (accumulate ? d_acc : parts[0]) + parts[1] + ... + parts[n-1],
+ * one rounded add per part in order: the reference's slice fold
+ * (multieval.cpp:498-513). parts: n_parts consecutive n_rows * row_elems
+ * blocks on the plan's device. */
+mtcg_status mtcg_fold(mtcg_plan* plan, const void* d_parts, uint64_t n_parts,
+                      void* d_acc, int accumulate, void* stream, char* err,
+                      size_t errlen);
 
 /* Copies a device accumulator back and fans rows out to requests
  * (multieval.cpp:374-380), filling res->values / out_legs / counters for the

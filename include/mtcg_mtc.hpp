@@ -14,6 +14,7 @@
 #ifndef MTCG_MTC_HPP
 #define MTCG_MTC_HPP
 
+#include <algorithm>
 #include <complex>
 #include <memory>
 #include <stdexcept>
@@ -31,21 +32,34 @@ namespace mtc::gpu {
 // Device precision: complex64 (default, 1e-4) or bit-exact complex128.
 enum class Precision { C64 = MTCG_C64, C128 = MTCG_C128 };
 
+// One GPU, or several GPUs of the node (eval_sliced spreads slices over
+// min(EvalOptions.workers, GPUs) of them — the GPU analogue of the reference's
+// worker threads, with the same guarantee: values bit-identical for every
+// count, multieval.hpp:26-29, 64-68).
 class Device {
  public:
-  explicit Device(int device = 0, std::uint64_t hbm_cap = 0) {
+  explicit Device(int device = 0, std::uint64_t hbm_cap = 0) : Device(std::vector<int>{device}, hbm_cap) {}
+  explicit Device(const std::vector<int>& devices, std::uint64_t hbm_cap_per_gpu = 0) {
     char err[512] = {0};
-    if (mtcg_create(device, hbm_cap, &h_, err, sizeof err) != MTCG_OK)
-      throw std::runtime_error(std::string("mtcg_create: ") + err);
+    if (mtcg_create_multi(devices.data(), static_cast<int>(devices.size()), hbm_cap_per_gpu, &h_, err,
+                          sizeof err) != MTCG_OK)
+      throw std::runtime_error(std::string("mtcg_create_multi: ") + err);
   }
   ~Device() { mtcg_destroy(h_); }
   Device(const Device&) = delete;
   Device& operator=(const Device&) = delete;
   mtcg_handle* handle() const { return h_; }
+  int count() const { return mtcg_device_count(h_); }
 
+  // every visible GPU (device 0 the root)
   static Device& default_device() {
-    static Device d(0);
+    static Device d(all_visible());
     return d;
+  }
+  static std::vector<int> all_visible() {
+    std::vector<int> v(static_cast<std::size_t>(std::max(1, mtcg_visible_devices())));
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = static_cast<int>(i);
+    return v;
   }
 
  private:

@@ -196,6 +196,37 @@ int main() {
     report(7, "linear_xeb on the device", std::abs(a - b) <= 1e-12 * std::max(1.0, std::abs(a)),
            std::to_string(a) + " vs " + std::to_string(b));
   }
+  {  // 8: workers -> GPUs (multieval_test.cpp:251-283: workers=4 bit-identical
+     // to workers=1); a 4-device handle over GPU 0 listed four times when the
+     // box has one GPU (the same per-device schedule, copies for NCCL)
+    std::vector<int> devs = gpu::Device::all_visible();
+    while (devs.size() < 4) devs.push_back(0);
+    gpu::Device multi(devs);
+    Rng rng(4711);
+    bool pass = true;
+    for (int rep = 0; rep < 8 && pass; ++rep) {
+      int n = 2 + static_cast<int>(rng.uniform_index(4));
+      Circuit c = test::random_circuit(rng, n, 16);
+      NetworkDiagram d = to_diagram(c, false);
+      Plan plan = random_plan(rng, d.slot_count());
+      AssignmentSet as = build_assignments(d, test::random_bitstrings(rng, n, 5), {});
+      for (int s = 0; s < 3; ++s) {
+        LegId leg;
+        do {
+          leg = static_cast<LegId>(rng.uniform_index(d.n_closed));
+        } while (std::find(plan.sliced.begin(), plan.sliced.end(), leg) != plan.sliced.end());
+        plan.sliced.push_back(leg);
+      }
+      EvalOptions w1, w4;
+      w1.workers = 1;
+      w4.workers = 4;
+      const EvalResult ref = eval_sliced(plan, d, as, w4);
+      pass = bit_equal(gpu::eval_sliced(plan, d, as, w1, Precision::C128, multi), ref) &&
+             bit_equal(gpu::eval_sliced(plan, d, as, w4, Precision::C128, multi), ref);
+    }
+    report(8, "eval_sliced workers=4 on 4 devices == workers=1 == reference", pass,
+           std::to_string(multi.count()) + " devices, 8 instances x 8 slices, c128");
+  }
   if (g_fail) {
     std::printf("%d criterion(s) failed\n", g_fail);
     return 1;

@@ -53,6 +53,13 @@ def lib():
             u64p, i32p, dp = C.POINTER(C.c_uint64), C.POINTER(C.c_int32), C.POINTER(C.c_double)
             L.mtcg_version.restype = C.c_int
             L.mtcg_create.argtypes = [C.c_int, C.c_uint64, C.POINTER(vp), cp, sz]
+            L.mtcg_create_multi.argtypes = [C.POINTER(C.c_int), C.c_int, C.c_uint64, C.POINTER(vp), cp, sz]
+            L.mtcg_device_count.argtypes = [vp]
+            L.mtcg_device_count.restype = C.c_int32
+            L.mtcg_visible_devices.argtypes = []
+            L.mtcg_visible_devices.restype = C.c_int32
+            L.mtcg_run_slices_out.argtypes = [vp, C.c_uint64, C.c_uint64, vp, vp, cp, sz]
+            L.mtcg_fold.argtypes = [vp, vp, C.c_uint64, vp, C.c_int, vp, cp, sz]
             L.mtcg_destroy.argtypes = [vp]
             L.mtcg_destroy.restype = None
             L.mtcg_eval.argtypes = [vp, pp, op, rp, cp, sz]
@@ -82,5 +89,6 @@ EXPORTS = (
     "mtcg_linear_xeb_amplitudes", "mtcg_compile", "mtcg_plan_destroy",
     "mtcg_plan_get_info", "mtcg_run", "mtcg_fetch", "mtcg_xeb_device",
     "mtcg_emulate", "mtcg_launch_count", "mtcg_plan_op_count", "mtcg_plan_op_info",
-    "mtcg_time_ops",
+    "mtcg_time_ops", "mtcg_create_multi", "mtcg_device_count", "mtcg_visible_devices",
+    "mtcg_run_slices_out", "mtcg_fold",
 )

@@ -8,6 +8,14 @@
 #include <cstring>
 #include <memory>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <numeric>
+#include <set>
+#include <thread>
+#include <vector>
+
 #include "device.hpp"
 #include "configs.hpp"
 #include "planner.hpp"
@@ -15,7 +23,10 @@
 using namespace mtcg;
 
 struct mtcg_handle {
-  Engine* engine = nullptr;
+  Engine* engine = nullptr;          // root: engines[0]
+  std::vector<Engine*> engines;      // one per listed device (repeats allowed)
+  std::vector<int> devices;
+  std::vector<ncclComm_t> comms;     // distinct devices: one NCCL rank each
   uint64_t cap = 0;
 };
 
@@ -24,6 +35,10 @@ struct mtcg_plan {
 };
 
 namespace {
+
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 void set_err(char* err, size_t errlen, const char* msg) {
   if (err && errlen) {
@@ -47,6 +62,9 @@ mtcg_status guarded(char* err, size_t errlen, int32_t* cap_node, F&& f) {
   } catch (const CudaError& e) {
     set_err(err, errlen, e.what());
     return MTCG_ERR_CUDA;
+  } catch (const NcclError& e) {
+    set_err(err, errlen, e.what());
+    return MTCG_ERR_NCCL;
   } catch (const std::bad_alloc&) {
     set_err(err, errlen, "host allocation failed");
     return MTCG_ERR_MEMORY_CAP;
@@ -151,6 +169,172 @@ void fetch_into(mtcg_plan* plan, const void* d_acc, void* stream, mtcg_result* r
   for (size_t i = 0; i < c.out_legs.size() && i < 64; ++i) res->out_legs[i] = c.out_legs[i];
 }
 
+// ---- NCCL (loaded on first use: the process may already hold torch's
+// libnccl.so.2, which dlopen then shares) -------------------------------------
+struct Nccl {
+  decltype(&ncclCommInitAll) init_all = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclGroupStart) group_start = nullptr;
+  decltype(&ncclGroupEnd) group_end = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw NcclError(std::string("libnccl.so.2 not loadable: ") + dlerror());
+    auto sym = [&](const char* name) {
+      void* f = dlsym(h, name);
+      if (!f) throw NcclError(std::string("NCCL symbol missing: ") + name);
+      return f;
+    };
+    r.init_all = reinterpret_cast<decltype(r.init_all)>(sym("ncclCommInitAll"));
+    r.destroy = reinterpret_cast<decltype(r.destroy)>(sym("ncclCommDestroy"));
+    r.group_start = reinterpret_cast<decltype(r.group_start)>(sym("ncclGroupStart"));
+    r.group_end = reinterpret_cast<decltype(r.group_end)>(sym("ncclGroupEnd"));
+    r.send = reinterpret_cast<decltype(r.send)>(sym("ncclSend"));
+    r.recv = reinterpret_cast<decltype(r.recv)>(sym("ncclRecv"));
+    r.error_string = reinterpret_cast<decltype(r.error_string)>(sym("ncclGetErrorString"));
+    return r;
+  }();
+  return n;
+}
+
+#define NCK(x)                                                                     \
+  do {                                                                             \
+    ncclResult_t r__ = (x);                                                        \
+    if (r__ != ncclSuccess) throw NcclError(std::string(#x) + ": " + nccl().error_string(r__)); \
+  } while (0)
+
+#define CCK(x)                                                                     \
+  do {                                                                             \
+    cudaError_t e__ = (x);                                                         \
+    if (e__ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+// Device buffer owned for one call.
+struct DevBuf {
+  Engine* e = nullptr;
+  void* p = nullptr;
+  DevBuf(Engine* eng, uint64_t bytes) : e(eng), p(bytes ? device_alloc(eng, bytes) : nullptr) {}
+  ~DevBuf() {
+    if (p) device_free(e, p);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// eval_sliced over several devices: rounds of R slices per device in
+// contiguous blocks (device g: [base + g R, base + (g + 1) R)), each slice's
+// root values gathered to the root in slice order, folded there in slice
+// order (bit-identical to one device). One host thread issues every device's
+// asynchronous work; NCCL send/recv pairs (one group per round) or device
+// copies (repeated devices) carry the values; device streams order reuse of
+// the per-device and root buffers across rounds.
+void eval_multi(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, int n_use, mtcg_result* res) {
+  Compiled c = compile_problem(*p, o, device_cap(h, o));
+  std::vector<std::unique_ptr<DevicePlan>> plans;
+  for (int g = 0; g < n_use; ++g) {
+    Compiled cg = c;  // host copy per device
+    plans.push_back(upload_plan(h->engines[g], std::move(cg)));
+  }
+  const Compiled& cc = plans[0]->c;
+  const uint64_t S = cc.n_slices, ne = cc.n_rows * cc.row_elems, eb = cc.elem_bytes;
+  const uint64_t slice_bytes = ne * eb;
+  // slices per device per round: all at once when the per-slice values fit
+  // in 512 MB per device
+  uint64_t R = (S + n_use - 1) / n_use;
+  if (slice_bytes) R = std::max<uint64_t>(1, std::min<uint64_t>(R, (512ull << 20) / slice_bytes));
+  const bool use_nccl = !h->comms.empty() && static_cast<int>(h->comms.size()) >= n_use;
+  Engine* root = h->engines[0];
+  DevBuf acc(root, slice_bytes);
+  DevBuf gather(root, static_cast<uint64_t>(n_use) * R * slice_bytes);
+  std::vector<std::unique_ptr<DevBuf>> stage, parts;
+  for (int g = 0; g < n_use; ++g) {
+    stage.push_back(std::make_unique<DevBuf>(h->engines[g], slice_bytes));
+    // the root writes its per-slice values straight into the gather buffer
+    parts.push_back(std::make_unique<DevBuf>(h->engines[g], g == 0 ? 0 : R * slice_bytes));
+  }
+  std::vector<cudaEvent_t> ev_done(n_use, nullptr);
+  cudaEvent_t ev_fold = nullptr;
+  auto cleanup = [&] {
+    for (int g = 0; g < n_use; ++g)
+      if (ev_done[g]) {
+        cudaSetDevice(h->devices[g]);
+        cudaEventDestroy(ev_done[g]);
+      }
+    if (ev_fold) {
+      cudaSetDevice(h->devices[0]);
+      cudaEventDestroy(ev_fold);
+    }
+  };
+  try {
+    for (int g = 0; g < n_use; ++g) {
+      CCK(cudaSetDevice(h->devices[g]));
+      CCK(cudaEventCreateWithFlags(&ev_done[g], cudaEventDisableTiming));
+    }
+    CCK(cudaSetDevice(h->devices[0]));
+    CCK(cudaEventCreateWithFlags(&ev_fold, cudaEventDisableTiming));
+    auto dstream = [&](int g) { return static_cast<cudaStream_t>(engine_stream(h->engines[g])); };
+    uint8_t* gbuf = static_cast<uint8_t*>(gather.p);
+    for (uint64_t base = 0, round = 0; base < S; base += static_cast<uint64_t>(n_use) * R, ++round) {
+      std::vector<uint64_t> cnt(n_use, 0);
+      for (int g = 0; g < n_use; ++g) {
+        const uint64_t lo = base + g * R, hi = std::min(S, lo + R);
+        if (lo >= hi) continue;
+        cnt[g] = hi - lo;
+        CCK(cudaSetDevice(h->devices[g]));
+        void* out = g == 0 ? static_cast<void*>(gbuf) : parts[g]->p;
+        run_slices(*plans[g], lo, hi, stage[g]->p, false, nullptr, out);
+      }
+      if (use_nccl) {
+        const ncclDataType_t t = cc.precision == MTCG_C64 ? ncclFloat32 : ncclFloat64;
+        NCK(nccl().group_start());
+        for (int g = 1; g < n_use; ++g) {
+          if (!cnt[g]) continue;
+          const size_t count = cnt[g] * ne * 2;
+          NCK(nccl().recv(gbuf + g * R * slice_bytes, count, t, g, h->comms[0], dstream(0)));
+          NCK(nccl().send(parts[g]->p, count, t, 0, h->comms[g], dstream(g)));
+        }
+        NCK(nccl().group_end());
+      } else {
+        for (int g = 1; g < n_use; ++g) {
+          if (!cnt[g]) continue;
+          CCK(cudaSetDevice(h->devices[g]));
+          // the root's gather slots are free once the previous round's fold ran
+          if (round > 0) CCK(cudaStreamWaitEvent(dstream(g), ev_fold, 0));
+          CCK(cudaMemcpyPeerAsync(gbuf + g * R * slice_bytes, h->devices[0], parts[g]->p, h->devices[g],
+                                  cnt[g] * slice_bytes, dstream(g)));
+          CCK(cudaEventRecord(ev_done[g], dstream(g)));
+          CCK(cudaSetDevice(h->devices[0]));
+          CCK(cudaStreamWaitEvent(dstream(0), ev_done[g], 0));
+        }
+      }
+      uint64_t total = 0;
+      for (uint64_t x : cnt) total += x;
+      fold_slices(root, cc.precision, gbuf, total, ne, acc.p, round > 0, nullptr);
+      CCK(cudaSetDevice(h->devices[0]));
+      CCK(cudaEventRecord(ev_fold, dstream(0)));
+    }
+    for (int g = 0; g < n_use; ++g) {
+      CCK(cudaSetDevice(h->devices[g]));
+      CCK(cudaStreamSynchronize(dstream(g)));
+    }
+    CCK(cudaSetDevice(h->devices[0]));
+    mtcg_plan plan;
+    plan.dp = std::move(plans[0]);
+    fetch_into(&plan, acc.p, nullptr, res);
+    plans[0] = std::move(plan.dp);
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+}
+
 }  // namespace
 
 extern "C" {
@@ -159,18 +343,53 @@ int mtcg_version(void) { return MTCG_ABI_VERSION; }
 
 mtcg_status mtcg_create(int device, uint64_t hbm_cap_bytes, mtcg_handle** out, char* err,
                         size_t errlen) {
+  return mtcg_create_multi(&device, 1, hbm_cap_bytes, out, err, errlen);
+}
+
+mtcg_status mtcg_create_multi(const int* devices, int n_devices, uint64_t hbm_cap_bytes_per_gpu,
+                              mtcg_handle** out, char* err, size_t errlen) {
   return guarded(err, errlen, nullptr, [&] {
     if (!out) throw DataError("null output handle");
+    if (!devices || n_devices < 1) throw DataError("no devices");
+    int visible = 0;
+    CCK(cudaGetDeviceCount(&visible));
+    for (int i = 0; i < n_devices; ++i)
+      if (devices[i] < 0 || devices[i] >= visible)
+        throw DataError("device " + std::to_string(devices[i]) + " not visible (" + std::to_string(visible) +
+                        " devices)");
     auto h = std::make_unique<mtcg_handle>();
-    h->engine = engine_create(device);
-    h->cap = hbm_cap_bytes;
+    h->cap = hbm_cap_bytes_per_gpu;
+    h->devices.assign(devices, devices + n_devices);
+    try {
+      for (int d : h->devices) h->engines.push_back(engine_create(d));
+      h->engine = h->engines[0];
+      const std::set<int> distinct(h->devices.begin(), h->devices.end());
+      if (n_devices > 1 && static_cast<int>(distinct.size()) == n_devices) {
+        h->comms.assign(n_devices, nullptr);
+        NCK(nccl().init_all(h->comms.data(), n_devices, h->devices.data()));
+      }
+    } catch (...) {
+      for (ncclComm_t c : h->comms)
+        if (c) nccl().destroy(c);
+      for (Engine* e : h->engines) engine_destroy(e);
+      throw;
+    }
     *out = h.release();
   });
 }
 
+int32_t mtcg_device_count(const mtcg_handle* h) { return h ? static_cast<int32_t>(h->engines.size()) : 0; }
+
+int32_t mtcg_visible_devices(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
+
 void mtcg_destroy(mtcg_handle* h) {
   if (!h) return;
-  engine_destroy(h->engine);
+  for (ncclComm_t c : h->comms)
+    if (c) nccl().destroy(c);
+  for (Engine* e : h->engines) engine_destroy(e);
   delete h;
 }
 
@@ -221,6 +440,31 @@ mtcg_status mtcg_run(mtcg_plan* plan, uint64_t slice_begin, uint64_t slice_end, 
   });
 }
 
+mtcg_status mtcg_run_slices_out(mtcg_plan* plan, uint64_t slice_begin, uint64_t slice_end, void* d_out,
+                                void* stream, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!plan) throw DataError("null plan");
+    DevicePlan& dp = *plan->dp;
+    const Compiled& c = dp.c;
+    if (slice_begin > slice_end || slice_end > c.n_slices)
+      throw DataError("slice range outside [0, " + std::to_string(c.n_slices) + ")");
+    if (!d_out && c.n_rows && slice_end > slice_begin) throw DataError("null output buffer");
+    if (!dp.d_stage) dp.d_stage = device_alloc(dp.engine, c.n_rows * c.row_elems * c.elem_bytes);
+    run_slices(dp, slice_begin, slice_end, dp.d_stage, false, stream, d_out);
+  });
+}
+
+mtcg_status mtcg_fold(mtcg_plan* plan, const void* d_parts, uint64_t n_parts, void* d_acc, int accumulate,
+                      void* stream, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!plan) throw DataError("null plan");
+    const Compiled& c = plan->dp->c;
+    if (n_parts && (!d_parts || !d_acc)) throw DataError("null buffer");
+    fold_slices(plan->dp->engine, c.precision, d_parts, n_parts, c.n_rows * c.row_elems, d_acc, accumulate != 0,
+                stream);
+  });
+}
+
 mtcg_status mtcg_fetch(mtcg_plan* plan, const void* d_acc, void* stream, mtcg_result* res,
                        char* err, size_t errlen) {
   return guarded(err, errlen, nullptr, [&] {
@@ -247,6 +491,12 @@ mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p, const mtcg_options*
     if (!h || !res) throw DataError("null argument");
     check_problem_pointers(p);
     const mtcg_options o = effective_options(h, opt ? *opt : default_options());
+    const int n_dev = static_cast<int>(h->engines.size());
+    const int n_use = o.workers > 0 ? std::min(n_dev, static_cast<int>(o.workers)) : n_dev;
+    if (n_use > 1) {
+      eval_multi(h, p, o, n_use, res);
+      return;
+    }
     Compiled c = compile_problem(*p, o, device_cap(h, o));
     mtcg_plan plan;
     plan.dp = upload_plan(h->engine, std::move(c));

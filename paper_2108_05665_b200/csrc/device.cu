@@ -1432,6 +1432,10 @@ DevicePlan::~DevicePlan() {
   for (void* e : op_events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* e : join_events) cudaEventDestroy(static_cast<cudaEvent_t>(e));
   for (void* s : aux_streams) cudaStreamDestroy(static_cast<cudaStream_t>(s));
+  if (d_stage) {
+    cudaStreamSynchronize(engine ? engine->stream : nullptr);
+    cudaFree(d_stage);
+  }
   if (d_blob) {
     if (engine) {
       engine->blob_pool.emplace_back(d_blob, blob_bytes);
@@ -1563,7 +1567,7 @@ void ensure_arena(DevicePlan& dp) {
 }
 
 void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
-                void* stream) {
+                void* stream, void* d_out_slices) {
   CK(cudaSetDevice(dp.engine->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
   if (s0 >= s1) return;
@@ -1618,16 +1622,60 @@ void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accu
       launch_slice(dp, d_acc, st, nullptr, nullptr, 0, n_pro);
     }
   }
+  // per-slice outputs: every slice overwrites d_acc (staging) and is copied
+  // to its own slot of d_out_slices
+  const uint64_t slice_bytes = dp.c.n_rows * dp.c.row_elems * static_cast<uint64_t>(dp.c.elem_bytes);
   for (uint64_t s = s0; s < s1; ++s) {
-    set_slice(dp, s, accumulate || s > s0, st);
+    set_slice(dp, s, !d_out_slices && (accumulate || s > s0), st);
     if (ge) {
       CK(cudaGraphLaunch(static_cast<cudaGraphExec_t>(ge->exec), st));
       dp.engine->launches += ge->kernels;
     } else {
       launch_slice(dp, d_acc, st, nullptr, nullptr, n_pro);
     }
+    if (d_out_slices && slice_bytes)
+      CK(cudaMemcpyAsync(static_cast<uint8_t*>(d_out_slices) + (s - s0) * slice_bytes, d_acc, slice_bytes,
+                         cudaMemcpyDeviceToDevice, st));
   }
 }
+
+namespace {
+// acc = (accumulate ? acc : parts[0]) + parts[1] + ... + parts[n - 1], one
+// rounded add per part in part order: the reference's slice fold
+// (multieval.cpp:498-513, add_into :369-372), and exactly what the root
+// epilogue's accumulation computes when the slices run on one device.
+template <class T>
+__global__ void fold_kernel(const T* parts, uint64_t n_parts, uint64_t n_elem, T* acc, int accumulate) {
+  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < n_elem;
+       i += uint64_t{gridDim.x} * blockDim.x) {
+    T a = accumulate ? acc[i] : parts[i];
+    for (uint64_t p = accumulate ? 0 : 1; p < n_parts; ++p) {
+      const T b = parts[p * n_elem + i];
+      a.x = a.x + b.x;
+      a.y = a.y + b.y;
+    }
+    acc[i] = a;
+  }
+}
+}  // namespace
+
+void fold_slices(Engine* e, int precision, const void* d_parts, uint64_t n_parts, uint64_t n_elem, void* d_acc,
+                 bool accumulate, void* stream) {
+  CK(cudaSetDevice(e->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : e->stream;
+  if (!n_parts || !n_elem) return;
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n_elem + 255) / 256, kSmSlots * 4));
+  if (precision == MTCG_C64)
+    fold_kernel<<<blocks, 256, 0, st>>>(static_cast<const float2*>(d_parts), n_parts, n_elem,
+                                         static_cast<float2*>(d_acc), accumulate ? 1 : 0);
+  else
+    fold_kernel<<<blocks, 256, 0, st>>>(static_cast<const double2*>(d_parts), n_parts, n_elem,
+                                         static_cast<double2*>(d_acc), accumulate ? 1 : 0);
+  e->launches++;
+  CK(cudaGetLastError());
+}
+
+int engine_device(const Engine* e) { return e->device; }
 
 void time_ops(DevicePlan& dp, uint64_t slice, void* d_acc, bool accumulate, void* stream,
               float* op_ms) {

@@ -51,6 +51,7 @@ struct DevicePlan {
   std::vector<void*> aux_streams;  // cudaStream_t
   std::vector<void*> op_events;    // cudaEvent_t per op
   std::vector<void*> join_events;  // cudaEvent_t per aux stream, + fork
+  void* d_stage = nullptr;         // per-slice output staging (mtcg_run_slices_out)
   ~DevicePlan();
 };
 
@@ -64,8 +65,16 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c);
 
 // Runs slices [s0, s1) accumulating into d_acc (rows x row_elems elements of
 // the plan precision). accumulate=false: the first slice overwrites.
+// d_out_slices != null: no fold — each slice's root values (d_acc is then
+// staging) are copied to d_out_slices + (s - s0) * rows * row_elems.
 void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc,
-                bool accumulate, void* stream);
+                bool accumulate, void* stream, void* d_out_slices = nullptr);
+
+// acc = (accumulate ? acc : parts[0]) + parts[1] + ... in part order (the
+// reference's slice fold); parts: n_parts x n_elem complex of `precision`.
+void fold_slices(Engine* e, int precision, const void* d_parts, uint64_t n_parts, uint64_t n_elem,
+                 void* d_acc, bool accumulate, void* stream);
+int engine_device(const Engine* e);
 
 // Same as run_slices for one slice, with an event pair around each op;
 // op_ms[i] receives op i's device time (ops with batch 0 get 0).

@@ -171,6 +171,34 @@ class CompiledProblem:
             _raise(st, err)
         return _result_from(res, vals, nc[:p.n_nodes], p.n_requests, w)
 
+    def run_slices_out(self, slice_begin: int, slice_end: int, out_ptr: int, stream: int = 0) -> None:
+        """Each slice's root values (no fold) into consecutive blocks of
+        out_ptr (new_accumulator-shaped blocks): the per-rank half of a
+        deterministic multi-GPU evaluation (mtcg_run_slices_out)."""
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_run_slices_out(self.h, slice_begin, slice_end, C.c_void_p(out_ptr),
+                                       C.c_void_p(stream or None), err, 1024)
+        if st:
+            _raise(st, err)
+
+    def fold(self, parts_ptr: int, n_parts: int, acc_ptr: int, accumulate: bool = False,
+             stream: int = 0) -> None:
+        """acc = (acc if accumulate else parts[0]) + parts[1] + ... in order
+        (mtcg_fold: the reference's slice fold)."""
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_fold(self.h, C.c_void_p(parts_ptr), n_parts, C.c_void_p(acc_ptr),
+                             int(accumulate), C.c_void_p(stream or None), err, 1024)
+        if st:
+            _raise(st, err)
+
+    def new_slice_buffer(self, n_slices: int):
+        """Device buffer for n_slices per-slice root tensors."""
+        import torch
+
+        dt = torch.float32 if self.info.precision == A.MTCG_C64 else torch.float64
+        return torch.zeros((max(n_slices, 1), max(int(self.info.n_rows), 1), int(self.info.row_elems), 2),
+                           dtype=dt, device=torch.device("cuda", self.engine.device))
+
     def op_infos(self):
         """Per-op introspection (mtcg_plan_op_info), in launch order."""
         L = lib()
@@ -204,13 +232,19 @@ def _result_from(res: A.mtcg_result, vals: np.ndarray, nc: np.ndarray, n_req: in
 
 
 class Engine:
-    """An mtcg handle bound to one CUDA device."""
+    """An mtcg handle bound to one CUDA device, or to several (``devices``:
+    mtcg_create_multi — eval() then spreads slices over the first
+    min(EvalOptions.workers, len(devices)) of them, bit-identical to one
+    device; repeats share a GPU)."""
 
-    def __init__(self, device: int = 0, hbm_cap_bytes: int = 0):
-        self.device = device
+    def __init__(self, device: int = 0, hbm_cap_bytes: int = 0, devices=None):
+        devs = list(devices) if devices is not None else [device]
+        self.device = devs[0]
+        self.devices = devs
         h = C.c_void_p()
         err = C.create_string_buffer(1024)
-        st = lib().mtcg_create(device, hbm_cap_bytes, C.byref(h), err, 1024)
+        arr = (C.c_int * len(devs))(*devs)
+        st = lib().mtcg_create_multi(arr, len(devs), hbm_cap_bytes, C.byref(h), err, 1024)
         if st:
             _raise(st, err)
         self.h = h
