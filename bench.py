@@ -48,7 +48,7 @@ WORKLOADS = {
 
 
 def load_workload(name: str):
-    from paper_2108_05665_b200 import network as N
+    from workloads import network as N
     from paper_2108_05665_b200.engine import problem_arrays
 
     w = WORKLOADS[name]

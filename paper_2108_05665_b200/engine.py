@@ -22,9 +22,17 @@ import numpy as np
 from . import _abi as A
 from ._lib import lib
 from .errors import DataError, EngineError, MemoryCapError
-from .network import AssignmentSet, NetworkDiagram, Plan, Tensor
 
 PRECISIONS = {"c64": A.MTCG_C64, "c128": A.MTCG_C128}
+
+
+@dataclass
+class Tensor:
+    """A request's result tensor (tensor.hpp:55-87): row-major over `legs`
+    (the batch legs, ascending; none for a single amplitude)."""
+
+    legs: List[int]
+    data: np.ndarray
 
 
 @dataclass
@@ -93,8 +101,10 @@ def _raise(status: int, err: C.Array, cap_node: int = -1):
     raise EngineError(f"mtcg status {status}: {msg}")
 
 
-def problem_arrays(plan: Plan, d: NetworkDiagram, assignments: AssignmentSet) -> A.ProblemArrays:
-    """Pack the reference-shaped inputs into the C ABI's POD arrays."""
+def problem_arrays(plan, d, assignments) -> A.ProblemArrays:
+    """Pack reference-shaped inputs (a Plan, a NetworkDiagram and an
+    AssignmentSet: plan.hpp:33-45, diagram.hpp:32-68 — e.g. workloads.network's
+    restatements) into the C ABI's POD arrays."""
     vs = [(s[0].legs, np.stack([t.data for t in s])) for s in assignments.value_sets]
     nodes = list(zip(plan.left, plan.right, plan.slot))
     return A.ProblemArrays.build(nodes, plan.root, plan.sliced, d.n_closed, d.leg_dims, vs,

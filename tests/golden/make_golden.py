@@ -19,7 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import refimpl as R  # noqa: E402
-from paper_2108_05665_b200 import network as N  # noqa: E402
+from workloads import network as N  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden", "reference_cases.json")
 

@@ -6,7 +6,7 @@ from typing import List, Optional, Tuple
 
 import numpy as np
 
-from paper_2108_05665_b200 import network as N
+from workloads import network as N
 from paper_2108_05665_b200._abi import ProblemArrays
 from paper_2108_05665_b200.engine import problem_arrays
 

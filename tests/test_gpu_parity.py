@@ -96,7 +96,7 @@ def test_duplicate_requests_evaluated_once(engine):
 
 
 def test_memory_cap_reports_node(engine):
-    from paper_2108_05665_b200 import network as N
+    from workloads import network as N
 
     rng = N.Rng(77)
     c = N.random_circuit(rng, 5, 20)

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import refimpl
-from paper_2108_05665_b200 import network as N
+from workloads import network as N
 from paper_2108_05665_b200.errors import DataError, ParseError
 
 from .helpers import GHZ_CIRCUIT, GHZ_PLAN

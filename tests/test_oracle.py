@@ -12,7 +12,7 @@ import pytest
 from oracle import oracle as O
 from oracle import refimpl
 from paper_2108_05665_b200 import _abi as A
-from paper_2108_05665_b200 import network as N
+from workloads import network as N
 from paper_2108_05665_b200.engine import problem_arrays
 
 from .helpers import GHZ_CIRCUIT, GHZ_PLAN, GOLDEN_AMP, ROOT, random_instance

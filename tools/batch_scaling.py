@@ -19,7 +19,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2108_05665_b200 import network as N  # noqa: E402
+from workloads import network as N  # noqa: E402
 from paper_2108_05665_b200.engine import Engine, EvalOptions, problem_arrays  # noqa: E402
 
 

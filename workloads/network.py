@@ -16,7 +16,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .errors import DataError, ParseError
+from paper_2108_05665_b200.errors import DataError, ParseError
 
 INV_SQRT2 = 0.70710678118654752440
 
