@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define MTCG_ABI_VERSION 1
+#define MTCG_ABI_VERSION 2
 
 typedef enum mtcg_status {
   MTCG_OK = 0,
@@ -116,10 +116,19 @@ typedef struct mtcg_options {
   int32_t eval_mode;          /* mtcg_eval_mode */
   int32_t precision;          /* mtcg_precision */
   uint64_t memory_cap_bytes;  /* device arena cap; 0 = the handle's cap */
-  int32_t workers;            /* EvalOptions.workers (accepted; the device
-                                 runs slices itself — results never depend on
-                                 it, multieval.hpp:66-68) */
+  int32_t workers;            /* EvalOptions.workers: on a multi-device
+                                 handle, the GPUs mtcg_eval uses (0 = all);
+                                 results never depend on it,
+                                 multieval.hpp:66-68 */
   int32_t flags;              /* MTCG_FLAG_* */
+  uint64_t row_chunk;         /* memo streaming (the reference's bounded
+                                 left/right caches, multieval.cpp:213-274):
+                                 mtcg_eval takes the requests, in
+                                 lexicographic tuple order, in chunks of this
+                                 many; the request-independent subtrees run
+                                 once per slice for all chunks and the memo
+                                 tables hold one chunk's distinct tuples.
+                                 0 = all requests at once */
 } mtcg_options;
 
 /* mtcg_options.flags */

@@ -63,6 +63,7 @@ class mtcg_options(C.Structure):
         ("memory_cap_bytes", C.c_uint64),
         ("workers", C.c_int32),
         ("flags", C.c_int32),
+        ("row_chunk", C.c_uint64),
     ]
 
 

@@ -335,6 +335,88 @@ void eval_multi(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, in
   cleanup();
 }
 
+// mtcg_eval with options.row_chunk: memo streaming. The requests, in
+// lexicographic tuple order (the reference walks rows in lexicographic order
+// with a one-entry left cache and per-node right dictionaries dropped at last
+// use, multieval.cpp:199-274), are cut into chunks of row_chunk; each chunk is
+// compiled as its own schedule whose request-independent subtrees form a
+// prologue laid out identically in every chunk (planner: request_dependent_
+// slots). Per slice the first chunk runs the prologue, then every chunk runs
+// its own ops against the resident prologue tables: the memo tables hold one
+// chunk's distinct tuples, the request-independent work is not repeated.
+// Values are each row's own slice sums, folded in slice order as without
+// chunking; counters and node_contractions are the whole evaluation's.
+void eval_chunked(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, mtcg_result* res) {
+  const uint64_t K = p->n_requests, B = o.row_chunk;
+  const int ns = p->n_slots;
+  std::vector<char> dep(ns, 0);
+  for (int j = 0; j < ns; ++j) dep[j] = p->slot_n_values[j] > 1;
+  mtcg_options oc = o;
+  oc.row_chunk = 0;
+  oc.flags &= ~MTCG_FLAG_SLICE_REUSE;
+  // the whole evaluation's exact counts (host only; no device schedule kept)
+  const Compiled whole = compile_problem(*p, oc, 0);
+  std::vector<uint64_t> order(K);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+    return std::lexicographical_compare(p->tuples + a * ns, p->tuples + (a + 1) * ns, p->tuples + b * ns,
+                                        p->tuples + (b + 1) * ns);
+  });
+  const uint64_t n_chunks = (K + B - 1) / B;
+  std::vector<std::vector<uint32_t>> tuples(n_chunks);
+  std::vector<std::unique_ptr<DevicePlan>> plans;
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    const uint64_t r0 = c * B, r1 = std::min(K, r0 + B);
+    tuples[c].resize((r1 - r0) * ns);
+    for (uint64_t r = r0; r < r1; ++r)
+      std::memcpy(tuples[c].data() + (r - r0) * ns, p->tuples + order[r] * ns, sizeof(uint32_t) * ns);
+    mtcg_problem q = *p;
+    q.n_requests = r1 - r0;
+    q.tuples = tuples[c].data();
+    plans.push_back(upload_plan(h->engine, compile_problem(q, oc, device_cap(h, oc), &dep)));
+  }
+  for (auto& dp : plans) ensure_arena(*dp);  // the shared arena at its largest before any run
+  std::vector<std::unique_ptr<DevBuf>> accs;
+  for (auto& dp : plans)
+    accs.push_back(std::make_unique<DevBuf>(h->engine, dp->c.n_rows * dp->c.row_elems * dp->c.elem_bytes));
+  for (auto& dp : plans) ensure_arena(*dp);
+  const uint64_t S = whole.n_slices;
+  for (uint64_t s = 0; s < S; ++s)
+    for (uint64_t c = 0; c < n_chunks; ++c) run_slice_chunk(*plans[c], s, accs[c]->p, s > 0, c == 0, nullptr);
+  // fetch every chunk and scatter its requests back to the caller's order
+  const uint64_t w = whole.row_elems;
+  if (res->values && res->values_capacity < K * w)
+    throw DataError("values buffer too small: need " + std::to_string(K * w) + " complex");
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    const uint64_t r0 = c * B, cnt = plans[c]->c.n_requests;
+    std::vector<double> vals(2 * cnt * w);
+    mtcg_result sub{};
+    sub.values = vals.data();
+    sub.values_capacity = cnt * w;
+    mtcg_plan plan;
+    plan.dp = std::move(plans[c]);
+    fetch_into(&plan, accs[c]->p, nullptr, &sub);
+    plans[c] = std::move(plan.dp);
+    if (res->values)
+      for (uint64_t i = 0; i < cnt; ++i)
+        std::memcpy(res->values + 2 * order[r0 + i] * w, vals.data() + 2 * i * w, sizeof(double) * 2 * w);
+    if (c == 0) {
+      res->n_out_legs = sub.n_out_legs;
+      std::memcpy(res->out_legs, sub.out_legs, sizeof(res->out_legs));
+    }
+  }
+  if (res->node_contractions)
+    std::memcpy(res->node_contractions, whole.node_contractions.data(),
+                sizeof(uint64_t) * whole.node_contractions.size());
+  res->mults = whole.mults;
+  res->adds = whole.adds;
+  res->rw = whole.rw;
+  uint64_t peak = 0;
+  for (auto& dp : plans) peak = std::max(peak, dp->c.arena_bytes() + dp->c.resident_bytes());
+  res->hbm_peak_bytes = peak;
+  res->cap_node = -1;
+}
+
 }  // namespace
 
 extern "C" {
@@ -494,7 +576,12 @@ mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p, const mtcg_options*
     const int n_dev = static_cast<int>(h->engines.size());
     const int n_use = o.workers > 0 ? std::min(n_dev, static_cast<int>(o.workers)) : n_dev;
     if (n_use > 1) {
+      if (o.row_chunk) throw DataError("row_chunk with several devices is not supported");
       eval_multi(h, p, o, n_use, res);
+      return;
+    }
+    if (o.row_chunk && o.row_chunk < p->n_requests) {
+      eval_chunked(h, p, o, res);
       return;
     }
     Compiled c = compile_problem(*p, o, device_cap(h, o));

@@ -913,6 +913,14 @@ double finish_partials(const std::vector<double>& part) {
 
 constexpr int kSmSlots = 148 * 8;
 constexpr int kXebBlocks = 592;  // 4 x 148 SMs
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  if (d < 0 || d >= kMaxDevices) throw CudaError("device ordinal out of range");
+  return d;
+}
 
 template <class R, int TM, int TN, int RM, int RN>
 void launch_tile(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
@@ -922,11 +930,12 @@ void launch_tile(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
   const size_t smem = sizeof(T) * (TK * (TM + 1) + TK * (TN + 1)) +
                       sizeof(uint32_t) * (2 * TM + 2 * TN + 2 * TK);
   auto kern = contract_tile<R, TM, TN, RM, RN, TK>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};  // per instantiation and device
+  const int dev = current_device();
+  if (!attr_set[dev]) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)));
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const uint64_t M = uint64_t{1} << op.fa, N = uint64_t{1} << op.fb;
   const uint64_t tiles = ((M + TM - 1) / TM) * ((N + TN - 1) / TN) * op.nb;
@@ -981,11 +990,12 @@ void launch_rows_grouped_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st)
   constexpr int RPT = RPT0 < 1 ? 1 : (RPT0 > 8 ? 8 : RPT0);
   const size_t smem = sizeof(T) * op.grp_max * K * N + sizeof(uint32_t) * (K + N + op.grp_max);
   auto kern = contract_rows_grouped<R, K, N, RPT>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};  // per instantiation and device
+  const int dev = current_device();
+  if (!attr_set[dev]) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             kGroupSmemBytes + 48 * 1024));
-    attr_set = true;
+    attr_set[dev] = true;
   }
   const uint64_t M = uint64_t{1} << op.fa;
   const uint64_t n_chunks = (M + 256 * RPT - 1) / (256 * RPT);
@@ -1179,10 +1189,11 @@ void launch_chain(DevicePlan& dp, const Chain& ch, cudaStream_t st) {
   d.tbl_words = static_cast<int>(ch.steps.back().tbl_off + ch.steps.back().tbl.size() - ch.steps[0].tbl_off);
   const size_t smem = (2 * ((size_t{1} << d.q) + 1 << d.inner_bits) + 64 * ch.steps.size()) * sizeof(T) +
                       4 * static_cast<size_t>(d.tbl_words);
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
+  static size_t smem_set[kMaxDevices] = {};  // function attributes are per device
+  const int dev = current_device();
+  if (smem > 48 * 1024 && smem > smem_set[dev]) {
     CK(cudaFuncSetAttribute(chain_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    smem_set = smem;
+    smem_set[dev] = smem;
   }
   // chunks per block: up to 8, keeping >= 4 blocks per SM's worth of work
   d.cpb_bits = 0;
@@ -1566,21 +1577,12 @@ void ensure_arena(DevicePlan& dp) {
   }
 }
 
-void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
-                void* stream, void* d_out_slices) {
-  CK(cudaSetDevice(dp.engine->device));
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
-  if (s0 >= s1) return;
-  ensure_arena(dp);
-  // One slice's launches are captured as a CUDA graph on first use (per
-  // accumulator) and replayed for every slice after a set-slice kernel: the
-  // host issues 2 launches per slice. MTCG_NO_GRAPHS=1 launches directly.
-  // With slice reuse the invariant ops (ops [0, n_pro)) form a second graph
-  // run once per call, before the first slice: the arena is shared by the
-  // handle's plans, so their resident tables are rebuilt on every run.
-  const bool graphs = !std::getenv("MTCG_NO_GRAPHS");
+// The captured graphs of a plan for accumulator d_acc (slice body, and the
+// prologue when the plan has one), created on first use; null when graphs
+// are disabled (MTCG_NO_GRAPHS=1).
+DevicePlan::GraphEntry* plan_graphs(DevicePlan& dp, void* d_acc, cudaStream_t st) {
+  if (std::getenv("MTCG_NO_GRAPHS")) return nullptr;
   const size_t n_pro = dp.c.n_prologue_ops;
-  DevicePlan::GraphEntry* ge = nullptr;
   auto capture = [&](size_t op0, size_t op1, void*& exec_out, uint64_t& kernels_out) {
     const uint64_t before = dp.engine->launches;
     cudaGraph_t graph = nullptr;
@@ -1602,17 +1604,68 @@ void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accu
     kernels_out = dp.engine->launches - before;
     dp.engine->launches = before;  // counted when replayed
   };
-  if (graphs) {
-    auto it = dp.graphs.find(d_acc);
-    if (it == dp.graphs.end()) {
-      ensure_dag_resources(dp);
-      DevicePlan::GraphEntry e;
-      capture(n_pro, ~size_t{0}, e.exec, e.kernels);
-      if (n_pro) capture(0, n_pro, e.exec_pro, e.kernels_pro);
-      it = dp.graphs.emplace(d_acc, e).first;
-    }
-    ge = &it->second;
+  auto it = dp.graphs.find(d_acc);
+  if (it == dp.graphs.end()) {
+    ensure_dag_resources(dp);
+    DevicePlan::GraphEntry e;
+    capture(n_pro, ~size_t{0}, e.exec, e.kernels);
+    if (n_pro) capture(0, n_pro, e.exec_pro, e.kernels_pro);
+    it = dp.graphs.emplace(d_acc, e).first;
   }
+  return &it->second;
+}
+
+// One slice of a row-chunked evaluation: the request-independent prologue
+// (when with_prologue: the first chunk of the slice) and the chunk's body.
+void run_slice_chunk(DevicePlan& dp, uint64_t s, void* d_acc, bool accumulate, bool with_prologue,
+                     void* stream) {
+  CK(cudaSetDevice(dp.engine->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
+  ensure_arena(dp);
+  const size_t n_pro = dp.c.n_prologue_ops;
+  DevicePlan::GraphEntry* ge = plan_graphs(dp, d_acc, st);
+  set_slice(dp, s, accumulate, st);
+  if (with_prologue && n_pro) {
+    if (ge) {
+      CK(cudaGraphLaunch(static_cast<cudaGraphExec_t>(ge->exec_pro), st));
+      dp.engine->launches += ge->kernels_pro;
+    } else {
+      launch_slice(dp, d_acc, st, nullptr, nullptr, 0, n_pro);
+    }
+  }
+  if (ge) {
+    CK(cudaGraphLaunch(static_cast<cudaGraphExec_t>(ge->exec), st));
+    dp.engine->launches += ge->kernels;
+  } else {
+    launch_slice(dp, d_acc, st, nullptr, nullptr, n_pro);
+  }
+}
+
+void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate,
+                void* stream, void* d_out_slices) {
+  CK(cudaSetDevice(dp.engine->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : dp.engine->stream;
+  if (s0 >= s1) return;
+  ensure_arena(dp);
+  // One slice's launches are captured as a CUDA graph on first use (per
+  // accumulator) and replayed for every slice after a set-slice kernel: the
+  // host issues 2 launches per slice. MTCG_NO_GRAPHS=1 launches directly.
+  // With slice reuse the invariant ops (ops [0, n_pro)) form a second graph
+  // run once per call, before the first slice: the arena is shared by the
+  // handle's plans, so their resident tables are rebuilt on every run. A
+  // row-chunked plan's prologue runs every slice (run_slice_chunk).
+  const size_t n_pro = dp.c.row_prologue ? 0 : dp.c.n_prologue_ops;
+  if (dp.c.row_prologue && dp.c.n_prologue_ops) {
+    const uint64_t slice_bytes = dp.c.n_rows * dp.c.row_elems * static_cast<uint64_t>(dp.c.elem_bytes);
+    for (uint64_t s = s0; s < s1; ++s) {
+      run_slice_chunk(dp, s, d_acc, !d_out_slices && (accumulate || s > s0), true, stream);
+      if (d_out_slices && slice_bytes)
+        CK(cudaMemcpyAsync(static_cast<uint8_t*>(d_out_slices) + (s - s0) * slice_bytes, d_acc, slice_bytes,
+                           cudaMemcpyDeviceToDevice, st));
+    }
+    return;
+  }
+  DevicePlan::GraphEntry* ge = plan_graphs(dp, d_acc, st);
   if (n_pro) {
     set_slice(dp, s0, accumulate, st);
     if (ge) {

@@ -70,6 +70,15 @@ std::unique_ptr<DevicePlan> upload_plan(Engine* e, Compiled&& c);
 void run_slices(DevicePlan& dp, uint64_t s0, uint64_t s1, void* d_acc,
                 bool accumulate, void* stream, void* d_out_slices = nullptr);
 
+// One slice of a row-chunked plan (Compiled::row_prologue): the request-
+// independent prologue when with_prologue (the slice's first chunk), then the
+// chunk's own ops; accumulates into d_acc like run_slices.
+void run_slice_chunk(DevicePlan& dp, uint64_t s, void* d_acc, bool accumulate, bool with_prologue,
+                     void* stream);
+// Sizes the handle's shared arena for this plan (all chunk plans of one
+// evaluation share it: resolve every plan before the first run).
+void ensure_arena(DevicePlan& dp);
+
 // acc = (accumulate ? acc : parts[0]) + parts[1] + ... in part order (the
 // reference's slice fold); parts: n_parts x n_elem complex of `precision`.
 void fold_slices(Engine* e, int precision, const void* d_parts, uint64_t n_parts, uint64_t n_elem,

@@ -335,7 +335,7 @@ struct SectionTimer {
 }  // namespace
 
 Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
-                         uint64_t cap_bytes) {
+                         uint64_t cap_bytes, const std::vector<char>* request_dependent_slots) {
   PhaseTimer timer;
   Compiled c;
   c.precision = opt.precision;
@@ -438,7 +438,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     for (uint32_t l : R)
       if (!contains(L, l)) out.push_back(l);
     std::sort(out.begin(), out.end());
-    if (out.size() > 40) throw DataError("intermediate tensor of order above 40");
+    // element offsets inside one table entry are 32-bit (SplitTable)
+    if (out.size() > 32) throw DataError("intermediate tensor of order above 32 is not supported");
     legs[node] = std::move(out);
   }
   c.out_legs = legs[p.root];
@@ -536,6 +537,27 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     }
     std::stable_partition(sched.begin(), sched.end(), [&](int node) { return invariant[node] != 0; });
     for (int node : sched) c.n_prologue_ops += invariant[node] ? 1 : 0;
+  } else if (request_dependent_slots) {
+    // row-chunked evaluation: request-independent nodes first, in the plan's
+    // own post-order (independent of this chunk's tuple counts, so every
+    // chunk lays the prologue out identically in the first-fit arena)
+    if (static_cast<int>(request_dependent_slots->size()) != p.n_slots)
+      throw InternalError("request_dependent_slots size");
+    for (int node : ix.postorder) {
+      if (p.node_slot[node] >= 0)
+        invariant[node] = !(*request_dependent_slots)[p.node_slot[node]];
+      else
+        invariant[node] = invariant[p.node_left[node]] && invariant[p.node_right[node]];
+    }
+    std::vector<int> pro, body;
+    for (int node : ix.postorder)
+      if (p.node_slot[node] < 0 && invariant[node]) pro.push_back(node);
+    for (int node : sched)
+      if (!invariant[node]) body.push_back(node);
+    sched = pro;
+    sched.insert(sched.end(), body.begin(), body.end());
+    c.n_prologue_ops = pro.size();
+    c.row_prologue = true;
   }
 
   // --- static arena: first-fit over the schedule ---------------------------
@@ -543,6 +565,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
   std::map<uint64_t, uint64_t> free_blocks;  // offset -> length
   uint64_t arena_top = 0;
   std::vector<uint64_t> arena_off(n, 0);
+  std::vector<uint64_t> frontier_row_exp(n, ~uint64_t{0});
   const uint64_t fixed_bytes =
       leaf_elems * c.elem_bytes + 2 * c.n_rows * c.row_elems * c.elem_bytes;
   auto alloc = [&](uint64_t elems, int node) -> uint64_t {
@@ -897,6 +920,18 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         arena_off[node] = alloc(table_elems[node], node);
       }
       op.out_base = arena_off[node];
+      // A frontier table (invariant, read by a dependent parent every slice /
+      // chunk) may be a tensor-core A operand quantized once in place after
+      // the prologue: its row exponents (one byte per row of the parent's
+      // view) get a resident slot here, in the prologue's allocation sequence
+      const int par = ix.parent[node];
+      if (invariant[node] && par >= 0 && !invariant[par]) {
+        const int sib = p.node_left[par] == node ? p.node_right[par] : p.node_left[par];
+        int kc = 0;
+        for (uint32_t x : legs[node]) kc += contains(legs[sib], x) ? 1 : 0;
+        const uint64_t rows = table_elems[node] >> kc;
+        frontier_row_exp[node] = alloc((rows + c.elem_bytes - 1) / c.elem_bytes, node);
+      }
     }
     if (op.config == kTcConfig && op.nb > 0) {
       // scratch: B̂ hi/lo (2N x 2K floats per item each)
@@ -912,11 +947,11 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       op.a_prequant = invariant[op.child_a] && !invariant[node] && op.kc > 5;
       op.scratch_elems = 2 * bhat + 4096 / c.elem_bytes +
                          (col_exps + (op.a_prequant ? 0 : row_exps) + c.elem_bytes) / c.elem_bytes + 1;
-      // (prologue-written, read by every slice: a private region above the
-      // first-fit arena, which earlier slice ops reuse)
+      // (prologue-written, read by every slice: the slot reserved when the
+      // frontier table was allocated)
       if (op.a_prequant) {
-        op.row_exp_off = private_top;
-        private_top += ((row_exps + c.elem_bytes - 1) / c.elem_bytes + align - 1) / align * align;
+        if (frontier_row_exp[op.child_a] == ~uint64_t{0}) throw InternalError("frontier row exponents");
+        op.row_exp_off = frontier_row_exp[op.child_a];
       }
       if (op.scratch_elems <= private_elems) {
         scratch_private.push_back(c.ops.size());
@@ -948,8 +983,6 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     if (!op.root && node_private[op.node]) op.out_base += arena_top;
   }
   for (size_t i : scratch_private) c.ops[i].scratch_off += arena_top;
-  for (Op& op : c.ops)
-    if (op.a_prequant) op.row_exp_off += arena_top;
   c.arena_elems = arena_top + private_top;
   c.private_elems = private_top;
   // --- fused operand chains ---------------------------------------------------------
@@ -977,7 +1010,12 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     auto linked = [&](size_t i) {  // op i+1 continues op i
       const Op& a = c.ops[i];
       const Op& b = c.ops[i + 1];
-      const bool seg = (i < c.n_prologue_ops) == (i + 1 < c.n_prologue_ops);
+      const bool seg = (i < c.n_prologue_ops) == (i + 1 < c.n_prologue_ops) &&
+                       // row-chunked plans: a chain's tail table lives in a
+                       // region placed after the plan's own arena, which
+                       // differs between chunk plans, so the shared prologue
+                       // has no chains
+                       !(c.row_prologue && i < c.n_prologue_ops);
       return seg && eligible(a) && eligible(b) && !b.a_leaf && op_of[b.child_a] == static_cast<int>(i) &&
              a.nb == b.nb && bijective(b);
     };

@@ -185,6 +185,9 @@ struct Compiled {
   // nodes, run once per run range; their tables feeding slice-dependent
   // parents stay resident in the arena across slices
   size_t n_prologue_ops = 0;
+  // row-chunked evaluation: the prologue is the request-independent part,
+  // run once per slice (by the first chunk) rather than once per run range
+  bool row_prologue = false;
   uint64_t executed_contractions = 0;  // per run range of S slices: see slice_contractions()
   uint64_t arena_bytes() const { return arena_elems * elem_bytes; }
   uint64_t resident_bytes() const {
@@ -195,7 +198,14 @@ struct Compiled {
 // Validates `p` with the reference's checks and messages, builds the tuple
 // index and the schedule. cap_bytes = 0: no cap. Throws DataError /
 // MemoryCapError.
+// request_dependent_slots (row-chunked evaluation): the slots whose value
+// varies over the requests of the WHOLE problem (this `p` holds one chunk of
+// them). Nodes over request-independent slots only form a prologue, scheduled
+// first in a canonical order and run once per slice for all chunks; the
+// tables they hand to request-dependent parents stay resident at offsets that
+// are the same in every chunk's schedule.
 Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
-                         uint64_t cap_bytes);
+                         uint64_t cap_bytes,
+                         const std::vector<char>* request_dependent_slots = nullptr);
 
 }  // namespace mtcg

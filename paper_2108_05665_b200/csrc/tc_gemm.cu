@@ -2322,12 +2322,8 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   // Short output rows (<= 32 complex per tile row) that are strided in memory
   // are transposed through smem in the epilogue; longer rows are written per
   // lane with vector stores.
-  static int n_sms = 0;
-  if (!n_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  DevAttr& da = dev_attr();  // per device: SM count, smem opt-ins
+  const int n_sms = da.n_sms;
   // (narrower n tiles for ops with fewer tiles than SMs were measured slower:
   // every tile still walks the whole K, now with smem-bound small MMAs)
   const int bn = tc_tile_n(static_cast<int>(Nr));
@@ -2381,20 +2377,17 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   p.m_contig = op.m_contig;
   p.transpose = transpose ? 1 : 0;
   p.partials = op.partials;
+  p.sa = p.sb = nullptr;
+  p.tom_cache = 0;
   // 8 converter warps + 1 epilogue group once the main loop per tile (>= 32
   // stages) outlasts a tile's epilogue (MTCG_TC_CONV=4|8 overrides)
   static const int conv_env = std::getenv("MTCG_TC_CONV") ? std::atoi(std::getenv("MTCG_TC_CONV")) : 0;
   p.n_conv = conv_env == 4 || conv_env == 8 ? conv_env : (Kr / bk >= 32 ? 8 : 4);
-  static size_t smem_set[4] = {0, 0, 0, 0};
   const int kv = pair ? 3 : f16 ? 2 : bk == 32 ? 1 : 0;
   auto kern = pair  ? tc_gemm_persistent<32, true, true>
               : f16 ? tc_gemm_persistent<32, true>
               : bk == 32 ? tc_gemm_persistent<32, false> : tc_gemm_persistent<16, false>;
-  if (smem > smem_set[kv]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (pair) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    smem_set[kv] = smem;
-  }
+  ensure_smem(da, kv, kern, smem, pair);
   const uint64_t tile_m = pair ? 2 * kBM : kBM;
   const uint64_t tiles = ga ? uint64_t{op.n_ga_tiles} * ((Nr + bn - 1) / bn)
                             : ((M + tile_m - 1) / tile_m) * ((Nr + bn - 1) / bn) * units;
@@ -2421,9 +2414,10 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, ma, mbhi, mblo, p, n_stages);
+    TCK(cudaLaunchKernelEx(&cfg, kern, ma, mbhi, mblo, p, n_stages));
   } else {
     kern<<<grid, kPThreads, smem, st>>>(ma, mbhi, mblo, p, n_stages);
+    TCK(cudaGetLastError());
   }
   if (tracing) {
     std::vector<unsigned long long> h(kTraceTiles * 8);

@@ -42,10 +42,13 @@ class EvalOptions:
     memory_cap_bytes: int = 0
     workers: int = 1
     precision: str = "c64"
-    tensor_cores: bool = True  # dense complex64 ops on tcgen05 (3xFP16 / 3xTF32)
+    tensor_cores: bool = True  # dense complex64 ops on tcgen05 (split-integer GEMM)
     # evaluate slice-invariant subtrees once per run instead of once per slice
     # (MTCG_FLAG_SLICE_REUSE; same values, reference counters)
     slice_reuse: bool = False
+    # memo streaming: requests in lexicographic chunks of this many (one-shot
+    # eval; 0 = all at once)
+    row_chunk: int = 0
 
 
 @dataclass
@@ -121,6 +124,7 @@ def _options(mode: int, opts: Optional[EvalOptions]) -> A.mtcg_options:
     o.memory_cap_bytes = int(opts.memory_cap_bytes)
     o.workers = int(opts.workers)
     o.flags = (0 if opts.tensor_cores else 1) | (2 if opts.slice_reuse else 0)  # MTCG_FLAG_*
+    o.row_chunk = int(opts.row_chunk)
     return o
 
 

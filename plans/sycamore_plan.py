@@ -1,0 +1,156 @@
+"""Contraction-plan supply for the 53-qubit Sycamore workloads (BASELINE
+configs 3-5; SURVEY §7 hard part 5, §8(f) rank 3).
+
+The reference's annealer starts from its left-deep plan (optimizer.cpp:82)
+and keeps its best plan by an incrementally drifting objective
+(plan.hpp:213, plan.cpp:492), which at 53 qubits leaves it near a plan with a
+2^53-element node. This is a plan PRODUCER — the caller's side of
+the hot path's boundary (plans are inputs, `Plan` plan.hpp:33-45) — written
+here for the multi-amplitude objective the engine executes:
+
+  cost(T)  = Σ_nodes k_T · 2^(|legs L ∪ legs R|) · S      (complex MACs)
+  table(T) = k_T · 2^|legs T|                              (memo entries)
+
+with k_T the number of distinct output-bit tuples of the node's subtree over
+the request batch (the exact `distinct[node]` of build_tuple_index,
+plan.cpp:292-333; estimated here as 2^q (1 - e^(-k/2^q)) for q output qubits,
+then counted exactly by the reference's CostedPlan), S = 2^(sliced legs).
+
+Search: randomised recursive bisection of the tensor graph (plans/
+treeopt.py) as the start, then simulated annealing over the paper's subtree
+rotations with slicing moves (plans/treesa.cpp, exact O(1) move deltas),
+several independent runs in parallel, the cheapest kept; the winner is
+checked by the reference's exact CostedPlan totals (oracle/_ref) and by the
+engine's emulate (the HBM arena of the device schedule).
+
+    python plans/sycamore_plan.py --cycles 12 --seed 2024 --k 10000 \\
+        --runs 8 --steps 300000000 --log2-max-table 31 --max-slices 14 \\
+        --out plans/cfg3.plan
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import random
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def network(cycles: int, seed: int):
+    from workloads import network as N
+
+    c = N.sycamore_circuit(cycles, seed)
+    d = N.to_diagram(c, True)
+    legs, qs = [], []
+    for j, t in enumerate(d.slot_tensors):
+        closed = 0
+        for leg in t.legs:
+            if not d.is_open(leg):
+                closed |= 1 << leg
+        legs.append(closed)
+        qs.append(len(d.slot_open_legs[j]))
+    return c, d, legs, qs
+
+
+def treesa_binary() -> str:
+    out = os.path.join(ROOT, "plans", "_build", "treesa")
+    src = os.path.join(ROOT, "plans", "treesa.cpp")
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        subprocess.run(["g++", "-O3", "-march=native", "-std=c++17", "-o", out, src], check=True)
+    return out
+
+
+def treesa(net, n_legs, merges, sliced, steps, seed, beta0, beta1, log2_max_table, beta_mem,
+           slice_every, max_slices):
+    lines = [f"{net.n} {n_legs} {net.k}"]
+    for i in range(net.n):
+        ls = [j for j in range(n_legs) if net.legs[i] >> j & 1]
+        lines.append(f"{net.q[i]} {len(ls)} " + " ".join(map(str, ls)))
+    lines.append(str(len(merges)))
+    lines += [f"{a} {b}" for a, b in merges]
+    lines.append(f"{steps} {beta0} {beta1} {log2_max_table} {beta_mem} {slice_every} {max_slices} {seed}")
+    sl = [j for j in range(n_legs) if sliced >> j & 1]
+    lines.append(f"{len(sl)} " + " ".join(map(str, sl)))
+    r = subprocess.run([treesa_binary()], input="\n".join(lines) + "\n", capture_output=True, text=True,
+                       check=True)
+    print(r.stderr.strip(), file=sys.stderr)
+    out = r.stdout.strip().splitlines()
+    mm = [tuple(map(int, l.split())) for l in out[:-1]]
+    sliced = 0
+    for x in out[-1].split()[1:]:
+        sliced |= 1 << int(x)
+    return mm, sliced
+
+
+def plan_text(n_slots: int, merges, sliced: int) -> str:
+    expr = {i: str(i) for i in range(n_slots)}
+    n = n_slots
+    for a, b in merges:
+        expr[n] = f"({expr.pop(a)} {expr.pop(b)})"
+        n += 1
+    root = expr[n - 1]
+    legs = [str(i) for i in range(sliced.bit_length()) if sliced >> i & 1]
+    return root + "\nslice: " + " ".join(legs) + "\n"
+
+
+def search_one(args):
+    (legs, qs, k, n_legs, seed, steps, beta0, beta1, log2_max_table, beta_mem, max_slices) = args
+    import treeopt as T
+
+    net = T.Network(legs, qs, k)
+    rng = random.Random(seed)
+    merges = T.bisection_tree(net, rng, cutoff=8, imbalance=0.2, noise=0.5)
+    merges, sliced = treesa(net, n_legs, merges, 0, steps, seed, beta0, beta1, log2_max_table, beta_mem,
+                            max(1, steps // 400), max_slices)
+    cost, big, order = T.evaluate(net, merges, sliced)
+    return cost, big, order, merges, sliced, seed
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cycles", type=int, default=12)
+    ap.add_argument("--seed", type=int, default=2024, help="circuit seed")
+    ap.add_argument("--k", type=int, default=10000)
+    ap.add_argument("--runs", type=int, default=8)
+    ap.add_argument("--jobs", type=int, default=os.cpu_count() or 1)
+    ap.add_argument("--steps", type=int, default=200_000_000)
+    ap.add_argument("--beta0", type=float, default=0.5)
+    ap.add_argument("--beta1", type=float, default=200.0)
+    ap.add_argument("--log2-max-table", type=float, default=31.0)
+    ap.add_argument("--beta-mem", type=float, default=4.0)
+    ap.add_argument("--max-slices", type=int, default=16)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    sys.path.insert(0, os.path.join(ROOT, "plans"))
+    _, d, legs, qs = network(a.cycles, a.seed)
+    n_legs = d.n_closed
+    from multiprocessing import Pool
+
+    treesa_binary()  # build once, before the workers
+    jobs = [(legs, qs, a.k, n_legs, 1000 + r, a.steps, a.beta0, a.beta1, a.log2_max_table, a.beta_mem,
+             a.max_slices) for r in range(a.runs)]
+    t0 = time.time()
+    with Pool(min(a.jobs, a.runs)) as pool:
+        results = pool.map(search_one, jobs)
+    results.sort(key=lambda r: r[0])
+    for cost, big, order, merges, sliced, seed in results:
+        print(f"run {seed}: cost {cost:.3e} MACs, largest table {big:.3e}, max order {order}, "
+              f"{sliced.bit_count()} sliced legs", file=sys.stderr)
+    cost, big, order, merges, sliced, seed = results[0]
+    print(f"best: {cost:.3e} ({time.time() - t0:.0f}s)", file=sys.stderr)
+    text = plan_text(len(legs), merges, sliced)
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(text)
+        print(a.out)
+    else:
+        print(text)
+
+
+if __name__ == "__main__":
+    main()

@@ -26,7 +26,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for sym in sorted(declared):
         assert hasattr(L, sym), sym
     assert set(EXPORTS) <= declared | {"mtcg_version"}
-    assert L.mtcg_version() == 1
+    assert L.mtcg_version() == 2
 
 
 def test_library_is_an_in_tree_sm100a_build():
