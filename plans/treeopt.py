@@ -210,18 +210,23 @@ def bisection_tree(net: Network, rng: random.Random, cutoff: int = 8, imbalance:
 # ---- costs -----------------------------------------------------------------------
 
 
-def evaluate(net: Network, merges, sliced: int = 0):
-    """Per-node (k_T, 2^|L ∪ R| MACs, out order) and totals."""
+def evaluate(net: Network, merges, sliced: int = 0, chunk: int = 0):
+    """(total MACs, largest memo table, largest order). chunk > 0: memo
+    streaming — request-dependent nodes evaluated per chunk of `chunk`
+    requests, tables holding one chunk's distinct tuples."""
     legs = [l & ~sliced for l in net.legs]
     qs = list(net.q)
+    b = chunk if 0 < chunk < net.k else net.k
+    n_chunks = math.ceil(net.k / b)
     tot = 0.0
     big = 0.0
     order = 0
-    for a, b in merges:
-        la, lb = legs[a], legs[b]
-        q = qs[a] + qs[b]
-        kt = kappa(q, net.k)
-        tot += kt * (1 << (la | lb).bit_count())
+    for a_, b_ in merges:
+        la, lb = legs[a_], legs[b_]
+        q = qs[a_] + qs[b_]
+        kt = kappa(q, b) if q else 1.0
+        ev = kt * n_chunks if q else 1.0
+        tot += ev * (1 << (la | lb).bit_count())
         out = la ^ lb
         legs.append(out)
         qs.append(q)

@@ -6,14 +6,16 @@
 // with the multi-amplitude cost C = S * Σ_nodes k_T 2^|legs L ∪ legs R| and
 // memo table k_T 2^|legs T| (k_T: distinct output-bit tuples of the
 // subtree over the k requests, estimated as 2^q (1 - e^(-k/2^q)) for q
-// output qubits; S = 2^sliced). A rotation changes one node's legs, so a move
+// output qubits; S = 2^sliced). With memo streaming (requests in chunks of
+// B, mtcg_options.row_chunk) a request-dependent node is evaluated per chunk
+// for that chunk's distinct tuples and its table holds one chunk's. A rotation changes one node's legs, so a move
 // is evaluated in O(1): the two affected nodes' costs are swapped in and the
 // total is recomputed exactly from scratch every few thousand moves (the
 // reference's incremental long-double p-norm drifts). Every
 // `slice_every` moves a slicing move adds (or swaps) a sliced leg chosen
 // among the legs of the largest tables.
 //
-// stdin: n_leaves n_legs k
+// stdin: n_leaves n_legs k chunk (memo streaming chunk; 0: none)
 //        per leaf: q count leg...
 //        n_merges, then n_merges lines "a b" (ids: leaves 0..n-1, merge i -> n+i)
 //        steps beta0 beta1 log2_max_table beta_mem slice_every max_slices seed
@@ -42,22 +44,31 @@ struct Tree {
   std::vector<Node> nodes;  // leaves first
   int n_leaves = 0, root = -1;
   double k = 1;
+  double chunk = 0;  // memo streaming: requests per chunk (0: all at once)
   Legs sliced;
 
-  double kappa(int q) const {
-    if (k <= 1) return 1.0;
-    if (q >= 62) return k;
+  static double distinct(int q, double n) {
+    if (n <= 1 || q == 0) return 1.0;
+    if (q >= 62) return n;
     const double m = std::ldexp(1.0, q);
-    return k < 40 * m ? m * -std::expm1(-k / m) : m;
+    return n < 40 * m ? m * -std::expm1(-n / m) : m;
   }
-  // cost of internal node v (per slice), and its table
+  double chunk_size() const { return chunk > 0 && chunk < k ? chunk : k; }
+  // evaluations of a node with q output qubits: once when request-
+  // independent, else per chunk the chunk's distinct tuples
+  double evals(int q) const {
+    if (q == 0) return 1.0;
+    const double b = chunk_size();
+    return std::ceil(k / b) * distinct(q, b);
+  }
+  // cost of internal node v (per slice), and its memo table (one chunk)
   double node_cost(int v) const {
     const Node& n = nodes[v];
     const Legs u = (nodes[n.left].legs | nodes[n.right].legs) & ~sliced;
-    return kappa(n.q) * std::ldexp(1.0, static_cast<int>(u.count()));
+    return evals(n.q) * std::ldexp(1.0, static_cast<int>(u.count()));
   }
   double node_table(int v) const {
-    return kappa(nodes[v].q) * std::ldexp(1.0, static_cast<int>((nodes[v].legs & ~sliced).count()));
+    return distinct(nodes[v].q, chunk_size()) * std::ldexp(1.0, static_cast<int>((nodes[v].legs & ~sliced).count()));
   }
   void refresh(int v) {
     Node& n = nodes[v];
@@ -87,8 +98,10 @@ int main() {
   Tree T;
   int n_legs;
   double k;
-  std::cin >> T.n_leaves >> n_legs >> k;
+  double chunk;
+  std::cin >> T.n_leaves >> n_legs >> k >> chunk;
   T.k = k;
+  T.chunk = chunk;
   T.nodes.resize(T.n_leaves);
   for (int i = 0; i < T.n_leaves; ++i) {
     int q, c;
