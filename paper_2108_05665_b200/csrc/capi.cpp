@@ -31,7 +31,21 @@ struct mtcg_handle {
 };
 
 struct mtcg_plan {
-  std::unique_ptr<DevicePlan> dp;
+  std::unique_ptr<DevicePlan> dp;  // the schedule; chunk 0 of a chunked plan
+  // memo streaming (mtcg_options.row_chunk): one schedule per request chunk
+  // sharing the request-independent prologue; the caller's accumulator holds
+  // the chunks' rows back to back
+  struct Chunked {
+    std::vector<std::unique_ptr<DevicePlan>> rest;  // chunks 1..
+    std::vector<uint64_t> row_off;                  // first accumulator row per chunk
+    std::vector<uint64_t> req_off;                  // first request (in `order`) per chunk
+    std::vector<uint64_t> order;                    // requests in lexicographic tuple order
+    uint64_t rows = 0;                              // accumulator rows, all chunks
+    std::unique_ptr<Compiled> whole;                // the whole evaluation's counts
+    DevicePlan& chunk(size_t c, mtcg_plan& pl) { return c == 0 ? *pl.dp : *rest[c - 1]; }
+    size_t n() const { return rest.size() + 1; }
+  };
+  std::unique_ptr<Chunked> chunked;
 };
 
 namespace {
@@ -346,7 +360,7 @@ void eval_multi(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, in
 // chunk's distinct tuples, the request-independent work is not repeated.
 // Values are each row's own slice sums, folded in slice order as without
 // chunking; counters and node_contractions are the whole evaluation's.
-void eval_chunked(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, mtcg_result* res) {
+std::unique_ptr<mtcg_plan> compile_chunked(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o) {
   const uint64_t K = p->n_requests, B = o.row_chunk;
   const int ns = p->n_slots;
   std::vector<char> dep(ns, 0);
@@ -354,52 +368,79 @@ void eval_chunked(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, 
   mtcg_options oc = o;
   oc.row_chunk = 0;
   oc.flags &= ~MTCG_FLAG_SLICE_REUSE;
+  auto plan = std::make_unique<mtcg_plan>();
+  plan->chunked = std::make_unique<mtcg_plan::Chunked>();
+  auto& ch = *plan->chunked;
   // the whole evaluation's exact counts (host only; no device schedule kept)
-  const Compiled whole = compile_problem(*p, oc, 0);
-  std::vector<uint64_t> order(K);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+  ch.whole = std::make_unique<Compiled>(compile_problem(*p, oc, 0));
+  ch.order.resize(K);
+  std::iota(ch.order.begin(), ch.order.end(), 0);
+  std::stable_sort(ch.order.begin(), ch.order.end(), [&](uint64_t a, uint64_t b) {
     return std::lexicographical_compare(p->tuples + a * ns, p->tuples + (a + 1) * ns, p->tuples + b * ns,
                                         p->tuples + (b + 1) * ns);
   });
   const uint64_t n_chunks = (K + B - 1) / B;
-  std::vector<std::vector<uint32_t>> tuples(n_chunks);
-  std::vector<std::unique_ptr<DevicePlan>> plans;
+  std::vector<uint32_t> tuples;
   for (uint64_t c = 0; c < n_chunks; ++c) {
     const uint64_t r0 = c * B, r1 = std::min(K, r0 + B);
-    tuples[c].resize((r1 - r0) * ns);
+    tuples.resize((r1 - r0) * ns);
     for (uint64_t r = r0; r < r1; ++r)
-      std::memcpy(tuples[c].data() + (r - r0) * ns, p->tuples + order[r] * ns, sizeof(uint32_t) * ns);
+      std::memcpy(tuples.data() + (r - r0) * ns, p->tuples + ch.order[r] * ns, sizeof(uint32_t) * ns);
     mtcg_problem q = *p;
     q.n_requests = r1 - r0;
-    q.tuples = tuples[c].data();
-    plans.push_back(upload_plan(h->engine, compile_problem(q, oc, device_cap(h, oc), &dep)));
+    q.tuples = tuples.data();
+    auto dp = upload_plan(h->engine, compile_problem(q, oc, device_cap(h, oc), &dep));
+    ch.req_off.push_back(r0);
+    ch.row_off.push_back(ch.rows);
+    ch.rows += dp->c.n_rows;
+    if (c == 0)
+      plan->dp = std::move(dp);
+    else
+      ch.rest.push_back(std::move(dp));
   }
-  for (auto& dp : plans) ensure_arena(*dp);  // the shared arena at its largest before any run
-  std::vector<std::unique_ptr<DevBuf>> accs;
-  for (auto& dp : plans)
-    accs.push_back(std::make_unique<DevBuf>(h->engine, dp->c.n_rows * dp->c.row_elems * dp->c.elem_bytes));
-  for (auto& dp : plans) ensure_arena(*dp);
-  const uint64_t S = whole.n_slices;
-  for (uint64_t s = 0; s < S; ++s)
-    for (uint64_t c = 0; c < n_chunks; ++c) run_slice_chunk(*plans[c], s, accs[c]->p, s > 0, c == 0, nullptr);
-  // fetch every chunk and scatter its requests back to the caller's order
-  const uint64_t w = whole.row_elems;
+  // the shared arena at its largest before any run
+  for (size_t c = 0; c < ch.n(); ++c) ensure_arena(ch.chunk(c, *plan));
+  return plan;
+}
+
+void run_chunked(mtcg_plan& plan, uint64_t s0, uint64_t s1, void* d_acc, bool accumulate, void* stream) {
+  auto& ch = *plan.chunked;
+  for (size_t c = 0; c < ch.n(); ++c) ensure_arena(ch.chunk(c, plan));
+  const Compiled& c0 = plan.dp->c;
+  const uint64_t row_bytes = c0.row_elems * static_cast<uint64_t>(c0.elem_bytes);
+  for (uint64_t s = s0; s < s1; ++s)
+    for (size_t c = 0; c < ch.n(); ++c)
+      run_slice_chunk(ch.chunk(c, plan), s, static_cast<uint8_t*>(d_acc) + ch.row_off[c] * row_bytes,
+                      accumulate || s > s0, c == 0, stream);
+}
+
+void fetch_chunked(mtcg_plan& plan, const void* d_acc, void* stream, mtcg_result* res) {
+  auto& ch = *plan.chunked;
+  const Compiled& whole = *ch.whole;
+  const uint64_t K = whole.n_requests, w = whole.row_elems;
   if (res->values && res->values_capacity < K * w)
     throw DataError("values buffer too small: need " + std::to_string(K * w) + " complex");
-  for (uint64_t c = 0; c < n_chunks; ++c) {
-    const uint64_t r0 = c * B, cnt = plans[c]->c.n_requests;
+  const uint64_t row_bytes = w * static_cast<uint64_t>(whole.elem_bytes);
+  for (size_t c = 0; c < ch.n(); ++c) {
+    DevicePlan& dp = ch.chunk(c, plan);
+    const uint64_t cnt = dp.c.n_requests;
     std::vector<double> vals(2 * cnt * w);
     mtcg_result sub{};
     sub.values = vals.data();
     sub.values_capacity = cnt * w;
-    mtcg_plan plan;
-    plan.dp = std::move(plans[c]);
-    fetch_into(&plan, accs[c]->p, nullptr, &sub);
-    plans[c] = std::move(plan.dp);
+    mtcg_plan one;
+    one.dp.reset(&dp);  // borrowed for fetch_into
+    try {
+      fetch_into(&one, static_cast<const uint8_t*>(d_acc) + ch.row_off[c] * row_bytes, stream, &sub);
+    } catch (...) {
+      one.dp.release();
+      throw;
+    }
+    one.dp.release();
     if (res->values)
       for (uint64_t i = 0; i < cnt; ++i)
-        std::memcpy(res->values + 2 * order[r0 + i] * w, vals.data() + 2 * i * w, sizeof(double) * 2 * w);
+        std::memcpy(res->values + 2 * ch.order[ch.req_off[c] + i] * w, vals.data() + 2 * i * w,
+                    sizeof(double) * 2 * w);
     if (c == 0) {
       res->n_out_legs = sub.n_out_legs;
       std::memcpy(res->out_legs, sub.out_legs, sizeof(res->out_legs));
@@ -412,9 +453,18 @@ void eval_chunked(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, 
   res->adds = whole.adds;
   res->rw = whole.rw;
   uint64_t peak = 0;
-  for (auto& dp : plans) peak = std::max(peak, dp->c.arena_bytes() + dp->c.resident_bytes());
-  res->hbm_peak_bytes = peak;
+  for (size_t c = 0; c < ch.n(); ++c)
+    peak = std::max(peak, ch.chunk(c, plan).c.arena_bytes() + ch.chunk(c, plan).c.resident_bytes());
+  res->hbm_peak_bytes = peak + ch.rows * row_bytes;
   res->cap_node = -1;
+}
+
+void eval_chunked(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, mtcg_result* res) {
+  std::unique_ptr<mtcg_plan> plan = compile_chunked(h, p, o);
+  const uint64_t row_bytes = plan->dp->c.row_elems * static_cast<uint64_t>(plan->dp->c.elem_bytes);
+  DevBuf acc(h->engine, plan->chunked->rows * row_bytes);
+  run_chunked(*plan, 0, plan->chunked->whole->n_slices, acc.p, false, nullptr);
+  fetch_chunked(*plan, acc.p, nullptr, res);
 }
 
 }  // namespace
@@ -495,6 +545,10 @@ mtcg_status mtcg_compile(mtcg_handle* h, const mtcg_problem* p, const mtcg_optio
     if (!h || !out) throw DataError("null handle");
     check_problem_pointers(p);
     const mtcg_options o = effective_options(h, opt ? *opt : default_options());
+    if (o.row_chunk && o.row_chunk < p->n_requests) {
+      *out = compile_chunked(h, p, o).release();
+      return;
+    }
     Compiled c = compile_problem(*p, o, device_cap(h, o));
     auto plan = std::make_unique<mtcg_plan>();
     plan->dp = upload_plan(h->engine, std::move(c));
@@ -506,6 +560,20 @@ void mtcg_plan_destroy(mtcg_plan* plan) { delete plan; }
 
 mtcg_status mtcg_plan_get_info(const mtcg_plan* plan, mtcg_plan_info* info) {
   if (!plan || !info) return MTCG_ERR_ARGUMENT;
+  if (plan->chunked) {
+    fill_info(*plan->chunked->whole, info);
+    info->n_rows = plan->chunked->rows;  // the accumulator: every chunk's rows
+    uint64_t arena = 0, resident = 0;
+    for (size_t c = 0; c < plan->chunked->n(); ++c) {
+      const Compiled& cc = plan->chunked->chunk(c, *const_cast<mtcg_plan*>(plan)).c;
+      arena = std::max(arena, cc.arena_bytes());
+      resident += cc.resident_bytes();
+    }
+    info->hbm_arena_bytes = arena;
+    info->hbm_resident_bytes = resident;
+    info->prologue_ops = plan->dp->c.n_prologue_ops;
+    return MTCG_OK;
+  }
   fill_info(plan->dp->c, info);
   return MTCG_OK;
 }
@@ -518,6 +586,10 @@ mtcg_status mtcg_run(mtcg_plan* plan, uint64_t slice_begin, uint64_t slice_end, 
     if (slice_begin > slice_end || slice_end > c.n_slices)
       throw DataError("slice range outside [0, " + std::to_string(c.n_slices) + ")");
     if (!d_acc && c.n_rows) throw DataError("null accumulator");
+    if (plan->chunked) {
+      run_chunked(*plan, slice_begin, slice_end, d_acc, accumulate != 0, stream);
+      return;
+    }
     run_slices(*plan->dp, slice_begin, slice_end, d_acc, accumulate != 0, stream);
   });
 }
@@ -531,6 +603,7 @@ mtcg_status mtcg_run_slices_out(mtcg_plan* plan, uint64_t slice_begin, uint64_t 
     if (slice_begin > slice_end || slice_end > c.n_slices)
       throw DataError("slice range outside [0, " + std::to_string(c.n_slices) + ")");
     if (!d_out && c.n_rows && slice_end > slice_begin) throw DataError("null output buffer");
+    if (plan->chunked) throw DataError("per-slice outputs of a row-chunked plan are not supported");
     if (!dp.d_stage) dp.d_stage = device_alloc(dp.engine, c.n_rows * c.row_elems * c.elem_bytes);
     run_slices(dp, slice_begin, slice_end, dp.d_stage, false, stream, d_out);
   });
@@ -542,7 +615,8 @@ mtcg_status mtcg_fold(mtcg_plan* plan, const void* d_parts, uint64_t n_parts, vo
     if (!plan) throw DataError("null plan");
     const Compiled& c = plan->dp->c;
     if (n_parts && (!d_parts || !d_acc)) throw DataError("null buffer");
-    fold_slices(plan->dp->engine, c.precision, d_parts, n_parts, c.n_rows * c.row_elems, d_acc, accumulate != 0,
+    const uint64_t rows = plan->chunked ? plan->chunked->rows : c.n_rows;
+    fold_slices(plan->dp->engine, c.precision, d_parts, n_parts, rows * c.row_elems, d_acc, accumulate != 0,
                 stream);
   });
 }
@@ -551,6 +625,10 @@ mtcg_status mtcg_fetch(mtcg_plan* plan, const void* d_acc, void* stream, mtcg_re
                        char* err, size_t errlen) {
   return guarded(err, errlen, nullptr, [&] {
     if (!plan || !res) throw DataError("null argument");
+    if (plan->chunked) {
+      fetch_chunked(*plan, d_acc, stream, res);
+      return;
+    }
     fetch_into(plan, d_acc, stream, res);
   });
 }
@@ -562,6 +640,16 @@ mtcg_status mtcg_xeb_device(mtcg_plan* plan, const void* d_acc, int n_qubits, vo
     const Compiled& c = plan->dp->c;
     if (c.n_requests == 0) throw DataError("linear_xeb needs at least one sample");
     if (n_qubits < 0 || n_qubits > 1022) throw DataError("qubit count out of range");
+    if (plan->chunked) {  // over the fetched amplitudes (compensated device reduction)
+      const Compiled& w = *plan->chunked->whole;
+      std::vector<double> vals(2 * w.n_requests * w.row_elems);
+      mtcg_result r{};
+      r.values = vals.data();
+      r.values_capacity = w.n_requests * w.row_elems;
+      fetch_chunked(*plan, d_acc, stream, &r);
+      *out = xeb_probs(plan->dp->engine, vals.data(), w.n_requests * w.row_elems, n_qubits, true);
+      return;
+    }
     *out = xeb_device(*plan->dp, d_acc, n_qubits, stream);
   });
 }

@@ -67,3 +67,23 @@ def test_chunking_runs_under_a_cap_the_whole_schedule_exceeds(engine):
     want, _, _, _ = O.eval_problem(p)
     got = engine.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", memory_cap_bytes=cap, row_chunk=10))
     assert bits_equal(got.amplitudes, want)
+
+
+@pytest.mark.parametrize("seed", [3, 6, 15])
+def test_chunked_staged_api(engine, seed):
+    """mtcg_compile with row_chunk: run slice ranges into one accumulator
+    (chunks back to back), fetch, fused XEB — as the unchunked plan."""
+    p, c, _ = random_instance(seed)
+    want, want_nc, _, _ = O.eval_problem(p)
+    cp = engine.compile(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", row_chunk=2))
+    S = cp.n_slices
+    acc = cp.new_accumulator()
+    cp.run(0, S // 2 if S > 1 else S, acc.data_ptr())
+    if S > 1:
+        cp.run(S // 2, S, acc.data_ptr(), accumulate=True)
+    r = cp.fetch(acc.data_ptr())
+    assert bits_equal(r.amplitudes, want)
+    assert np.array_equal(r.node_contractions, want_nc)
+    f = cp.xeb(acc.data_ptr(), c.n_qubits)
+    f_ref = O.linear_xeb(c.n_qubits, (np.abs(want) ** 2).ravel())
+    assert abs(f - f_ref) <= 1e-12 * max(1.0, abs(f_ref))
