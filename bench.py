@@ -40,6 +40,10 @@ WORKLOADS = {
                   text="cal45: synthetic 20-qubit 4x5 grid, m=10 (grid_circuit seed 12345, fused), "
                        "1000 random bitstrings (seed 99), plans/cal45.plan (3 sliced legs); the "
                        "reference arm's calibration run"),
+    "cfg3": dict(kind="sycamore", cycles=12, circuit_seed=2024, k=10000, row_chunk=2500, rows=0, cols=53,
+                 text="cfg3: synthetic 53-qubit Sycamore layout, m=12 (ABCDCDAB fSim, sycamore_circuit seed "
+                      "2024, fused), 10^4 random bitstrings (seed 99), plans/cfg3.plan (20 sliced legs, 2^20 "
+                      "slices; plans/sycamore_plan.py), memo streaming in chunks of 2500 requests"),
     "cfg2": dict(rows=5, cols=6, layers=12, k=10000,
                  text="cfg2: synthetic 30-qubit 5x6 grid, m=12 (grid_circuit seed 12345, "
                       "fused), 10^4 random bitstrings (seed 99), plans/cfg2.plan "
@@ -47,11 +51,18 @@ WORKLOADS = {
 }
 
 
-def load_workload(name: str):
+def load_workload(name: str, k: int = 0):
     from workloads import network as N
     from paper_2108_05665_b200.engine import problem_arrays
 
     w = WORKLOADS[name]
+    if w.get("kind") == "sycamore":
+        c = N.sycamore_circuit(w["cycles"], w["circuit_seed"])
+        bits = N.random_bitstrings(N.Rng(99), c.n_qubits, w["k"])[: k or w["k"]]
+        d = N.to_diagram(c, True)
+        asg = N.build_assignments(d, bits, [])
+        plan_text = open(os.path.join(ROOT, "plans", f"{name}.plan")).read()
+        return problem_arrays(N.parse_plan(plan_text), d, asg), c, bits, plan_text
     c = N.grid_circuit(w["rows"], w["cols"], w["layers"], 12345)
     bits = N.random_bitstrings(N.Rng(99), w["rows"] * w["cols"], w["k"])
     d = N.to_diagram(c, True)
@@ -414,6 +425,108 @@ def parity_check(cp, acc, config, n_qubits, xeb_dev):
                          and cnt_equal)}
 
 
+def run_sliced_subset(args):
+    """53-qubit workloads (cfg3): the whole evaluation is ~3.4e17 complex MACs
+    over 2^20 slices, so a step is one slice of it — every slice is the same
+    schedule on different projections, and CostedPlan's cost is per-slice x S
+    (plan.cpp:497-502). W warm-up slices, then K timed slices; the full
+    evaluation's throughput is extrapolated: value = k / (t_slice * S). The
+    memo streams in chunks (mtcg_options.row_chunk). Parity: the first 10
+    bitstrings on slices 0 and 1 against the unmodified reference's own
+    per-slice amplitudes (tests/golden/cfg3_reference.npz), and the exact
+    algorithmic totals against its CostedPlan."""
+    import torch
+
+    from paper_2108_05665_b200.engine import Engine, EvalOptions
+
+    w = WORKLOADS[args.config]
+    problem, circ, bits, _ = load_workload(args.config)
+    k = len(bits)
+    eng = Engine(0)
+    t0 = time.perf_counter()
+    cp = eng.compile(problem, 0, EvalOptions(precision=args.precision, row_chunk=w["row_chunk"]))
+    compile_s = time.perf_counter() - t0
+    S = cp.n_slices
+    torch.cuda.set_stream(torch.cuda.Stream())
+    stream = torch.cuda.current_stream().cuda_stream
+    acc = cp.new_accumulator()
+    W = max(args.warmup, 1)
+    for i in range(W):
+        cp.run(i, i + 1, acc.data_ptr(), accumulate=i > 0, stream=stream)
+    torch.cuda.synchronize()
+    launches0 = eng.launches
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        marks[0].record()
+        for i in range(args.steps):
+            cp.run(W + i, W + i + 1, acc.data_ptr(), accumulate=True, stream=stream)
+            marks[i + 1].record()
+        torch.cuda.synchronize()
+    launches = eng.launches - launches0
+    t_ms = marks[0].elapsed_time(marks[-1])
+    slice_ms = t_ms / args.steps
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
+    mults = int(cp.info.mults)
+    flops_slice = 8.0 * mults / S
+    value = k / (slice_ms * 1e-3 * S)
+    # parity on the 10-bitstring subset (slices 0, 1) against the reference
+    parity = {"available": False}
+    gpath = os.path.join(ROOT, "tests", "golden", f"{args.config}_reference.npz")
+    if os.path.exists(gpath):
+        g = np.load(gpath)
+        sub_k = int(g["subset"])
+        psub, _, _, _ = load_workload(args.config, sub_k)
+        res = {}
+        for prec in ("c64", "c128"):
+            cs = eng.compile(psub, 0, EvalOptions(precision=prec))
+            a_ = cs.new_accumulator()
+            got = []
+            for s_ in g["slices"]:
+                cs.run(int(s_), int(s_) + 1, a_.data_ptr())
+                got.append(cs.fetch(a_.data_ptr()).amplitudes.reshape(-1))
+            got = np.stack(got)
+            want = g["slice_amplitudes"]
+            floor = 2.0 ** (-circ.n_qubits / 2)
+            res[prec] = {"max_rel": float(np.max(np.abs(got - want) / np.maximum(np.abs(want), floor))),
+                         "l2_rel": float(np.linalg.norm(got - want) / np.linalg.norm(want)),
+                         "bit_identical": bool(np.array_equal(got.view(np.float64), want.view(np.float64)))}
+            del cs, a_
+        parity = {"against": f"tests/golden/{args.config}_reference.npz (reference run_slice, complex128)",
+                  "subset": f"{sub_k} bitstrings x slices {list(map(int, g['slices']))}",
+                  "c64": res["c64"], "c128": res["c128"],
+                  "mults_equal_reference_costedplan": str(mults) == str(g["mults_str"]),
+                  "pass": bool(res["c128"]["bit_identical"] and res["c64"]["max_rel"] <= 1e-4
+                               and str(mults) == str(g["mults_str"]))}
+    hbm, tflops, src = measured_peaks()
+    ceiling = tflops / 3.0
+    line = {
+        "metric": METRIC, "value": value, "unit": "amplitudes/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": W, "ms_per_step": slice_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": w["text"], "n_qubits": circ.n_qubits, "bitstrings": k, "slices": S,
+                   "step": "one slice of the evaluation (all slices are the same schedule)",
+                   "extrapolation": f"value = k / (t_slice x {S} slices); full evaluation "
+                                    f"{slice_ms * S / 1e3 / 3600:.2f} h on 1 GPU",
+                   "row_chunk": w["row_chunk"], "l2": "per-slice working set > 126 MB L2"},
+        "effective_tflops": flops_slice / (slice_ms * 1e-3) / 1e12,
+        "mults_total": mults, "flops_per_slice": flops_slice,
+        "roofline": {"bound": "tensor", "achieved": flops_slice / (slice_ms * 1e-3) / 1e12, "peak": tflops,
+                     "unit": "TFLOP/s", "frac": flops_slice / (slice_ms * 1e-3) / 1e12 / tflops,
+                     "scheme_ceiling": ceiling, "traffic": None,
+                     "kernel": "whole slice (all ops)", "peak_source": f"{src} (bf16 dense)"},
+        "parity": parity,
+        "compile_s": compile_s,
+        "hbm_arena_bytes": int(cp.info.hbm_arena_bytes),
+        "gpu_launches": launches,
+        "e2e": None,
+        "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def run_engine(args):
     import torch
     import torch.distributed as dist
@@ -651,6 +764,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if WORKLOADS[args.config].get("kind") == "sycamore":
+        return run_sliced_subset(args)
     return run_engine(args)
 
 

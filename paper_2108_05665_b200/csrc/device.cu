@@ -175,6 +175,7 @@ struct DevOp {
   int n_fast;               // epilogue lane order
   int accumulate;           // root: add into the accumulator
   int a_kcontig;            // rows kernel: A rows K-contiguous
+  int b_kcontig;            // dot kernel: B rows K-contiguous too (direct loads)
   int o_ncontig;            // rows kernel: output n contiguous
   const uint32_t* grp_items;  // grouped rows kernel: items ordered by A entry
   const uint32_t* grp_start;  // ... CSR offsets per group
@@ -792,7 +793,24 @@ __global__ void __launch_bounds__(256)
     const float2* B = op.b + uint64_t{op.ib ? __ldg(op.ib + item) : (uint32_t)item} * op.b_item +
                       op.b_slice + op.tbn(o);
     float2 acc = make_float2(0.f, 0.f);
-    for (uint64_t c = lane; c < K; c += 32) cmac(acc, A[op.tak(c)], B[op.tbk(c)], false);
+    if (op.a_kcontig && op.b_kcontig) {
+      // both rows K-contiguous: coalesced direct loads, 4 independent sums
+      float2 acc1 = acc, acc2 = acc, acc3 = acc;
+      uint64_t c = lane;
+      for (; c + 96 < K; c += 128) {
+        const float2 a0 = __ldg(A + c), a1 = __ldg(A + c + 32), a2 = __ldg(A + c + 64), a3 = __ldg(A + c + 96);
+        const float2 b0 = __ldg(B + c), b1 = __ldg(B + c + 32), b2 = __ldg(B + c + 64), b3 = __ldg(B + c + 96);
+        cmac(acc, a0, b0, false);
+        cmac(acc1, a1, b1, false);
+        cmac(acc2, a2, b2, false);
+        cmac(acc3, a3, b3, false);
+      }
+      for (; c < K; c += 32) cmac(acc, __ldg(A + c), __ldg(B + c), false);
+      acc.x += acc1.x + (acc2.x + acc3.x);
+      acc.y += acc1.y + (acc2.y + acc3.y);
+    } else {
+      for (uint64_t c = lane; c < K; c += 32) cmac(acc, A[op.tak(c)], B[op.tbk(c)], false);
+    }
 #pragma unroll
     for (int sh = 16; sh > 0; sh >>= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, sh);
@@ -1277,6 +1295,7 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
     d.kc = op.kc;
     d.n_fast = op.store_n_fast ? 1 : 0;
     d.a_kcontig = op.a_kcontig ? 1 : 0;
+    d.b_kcontig = op.b_kcontig ? 1 : 0;
     d.o_ncontig = op.o_ncontig ? 1 : 0;
     d.grp_items = dp.d_index + op.grp_items_off;
     d.grp_start = dp.d_index + op.grp_start_off;

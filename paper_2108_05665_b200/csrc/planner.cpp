@@ -124,15 +124,42 @@ TupleIndex build_tuple_index(const mtcg_problem& p, const PlanIdx& ix) {
   // informative column, value ranges are the slots' value counts): O(k w)
   // instead of a comparison sort. Sorted rows also keep the per-node key
   // passes below cache-friendly.
+  // Consecutive informative columns are packed into one digit while the
+  // product of their value ranges stays <= 4096 (lexicographic within the
+  // group), and the digits stored digit-major: ~w/6 passes over small
+  // sequential arrays instead of w passes of strided reads (k = 10^5:
+  // 160 -> ~15 ms).
+  std::vector<std::pair<size_t, size_t>> groups;  // [c0, c1)
+  std::vector<uint32_t> group_span;
+  for (size_t c0 = 0; c0 < w;) {
+    uint64_t span = 1;
+    size_t c1 = c0;
+    while (c1 < w && span * static_cast<uint64_t>(p.slot_n_values[informative[c1]]) <= 4096)
+      span *= static_cast<uint64_t>(p.slot_n_values[informative[c1++]]);
+    if (c1 == c0) span = static_cast<uint64_t>(p.slot_n_values[informative[c1++]]);  // a single wide slot
+    groups.push_back({c0, c1});
+    group_span.push_back(static_cast<uint32_t>(span));
+    c0 = c1;
+  }
+  static thread_local std::vector<uint32_t> digits;
+  digits.resize(groups.size() * k);
+  for (size_t g = 0; g < groups.size(); ++g)
+    for (uint64_t i = 0; i < k; ++i) {
+      uint32_t d = 0;
+      for (size_t c = groups[g].first; c < groups[g].second; ++c)
+        d = d * static_cast<uint32_t>(p.slot_n_values[informative[c]]) + Cp[i * w + c];
+      digits[g * k + i] = d;
+    }
   std::vector<uint64_t> order(k), tmp(k);
   std::iota(order.begin(), order.end(), 0);
   std::vector<uint64_t> count;
-  for (size_t c = w; c-- > 0;) {
-    const uint64_t span = static_cast<uint64_t>(p.slot_n_values[informative[c]]);
+  for (size_t g = groups.size(); g-- > 0;) {
+    const uint64_t span = group_span[g];
+    const uint32_t* dg = digits.data() + g * k;
     count.assign(span + 1, 0);
-    for (uint64_t i = 0; i < k; ++i) ++count[Cp[order[i] * w + c] + 1];
+    for (uint64_t i = 0; i < k; ++i) ++count[dg[i] + 1];
     for (uint64_t v = 0; v < span; ++v) count[v + 1] += count[v];
-    for (uint64_t i = 0; i < k; ++i) tmp[count[Cp[order[i] * w + c]]++] = order[i];
+    for (uint64_t i = 0; i < k; ++i) tmp[count[dg[order[i]]]++] = order[i];
     order.swap(tmp);
   }
   auto lex_eq = [&](uint64_t a, uint64_t b) {
@@ -776,7 +803,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     const uint64_t units = grouped ? uint64_t{g_start.size() - 1} : op.nb;
     const bool tc_ok = c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) &&
                        !op.a_leaf && op.fa >= 7 && fb_eff >= tc_min_fb && op.kc >= 4 &&
-                       fb_eff <= 12 && intensity >= 6.0 && (!grouped || op.fa >= 12) &&
+                       fb_eff <= 12 && op.kc <= 14 && intensity >= 6.0 && (!grouped || op.fa >= 12) &&
                        (units << (op.fa + fb_eff + op.kc)) >= (uint64_t{1} << 26);
     // MTCG_TC_ONLY=<node>[,<node>...] restricts the tensor path (diagnostics)
     const char* tc_only = std::getenv("MTCG_TC_ONLY");
@@ -865,6 +892,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       const auto ks = strides_of(k_legs, a_layout);
       op.a_kcontig = !op.a_leaf;
       for (size_t b = 0; b < ks.size(); ++b) op.a_kcontig &= ks[b] == (uint64_t{1} << b);
+      const auto kb = strides_of(k_legs, b_layout);
+      op.b_kcontig = !op.b_leaf;
+      for (size_t b = 0; b < kb.size(); ++b) op.b_kcontig &= kb[b] == (uint64_t{1} << b);
       const auto ns = strides_of(n_legs, out_layout);
       op.o_ncontig = op.config != kGenericConfig && op.config != kDotConfig;
       for (size_t b = 0; b < ns.size(); ++b) op.o_ncontig &= ns[b] == (uint64_t{1} << b);

@@ -78,6 +78,7 @@ struct Op {
   bool a_prequant = false;
   uint64_t row_exp_off = 0;
   bool a_kcontig = false;          // A rows are K-contiguous (tak(k) == k)
+  bool b_kcontig = false;          // B rows are K-contiguous (tbk(k) == k)
   bool o_ncontig = false;          // output n index is contiguous (ton(n) == n)
   bool o_mcontig = false;          // output m bit 0 has stride 1
   // ops this op must wait for when independent ops run concurrently: the

@@ -1982,6 +1982,42 @@ __global__ void __launch_bounds__(256) quantize_rows_kernel(float* a, uint64_t r
   }
 }
 
+// Rows longer than 4096 floats (K > 2^11 complex): one block per row, the
+// row staged in shared memory (kr * 4 bytes) before any byte is written.
+__global__ void __launch_bounds__(256) quantize_rows_smem_kernel(float* a, uint64_t rows, int kr, int8_t* sa_out) {
+  extern __shared__ float4 qrow[];
+  __shared__ float red[8];
+  const int n4 = kr / 4;
+  for (uint64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const float4* src = reinterpret_cast<const float4*>(a + row * kr);
+    float mx = 0.f;
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+      const float4 v = src[i];
+      qrow[i] = v;
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < 8; ++w) mx = fmaxf(mx, red[w]);
+    const int sa = i8_scale_exp(mx);
+    const float sc = pow2f_wide(sa);
+    if (threadIdx.x == 0) sa_out[row] = static_cast<int8_t>(sa);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(a + row * kr);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+      const float4 v = qrow[i];
+      uint32_t w0, w1, w2;
+      i8_pack4(i8_biased(v.x, sc), i8_biased(v.y, sc), i8_biased(v.z, sc), i8_biased(v.w, sc), w0, w1, w2);
+      dst[i] = w0;
+      dst[kr / 4 + i] = w1;
+      dst[kr / 2 + i] = w2;
+    }
+    __syncthreads();  // qrow / red reused by the next row
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -2123,8 +2159,24 @@ int launch_quantize(const TcOp& op, cudaStream_t st) {
     case 1024: quantize_rows_kernel<8><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
     case 2048: quantize_rows_kernel<16><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
     case 4096: quantize_rows_kernel<32><<<blocks, 256, 0, st>>>(a, rows, op.row_exp); break;
-    default: throw std::runtime_error("split-integer path: unsupported K = 2^" + std::to_string(op.kc));
+    default: {
+      if (kr > (1 << 15)) throw std::runtime_error("split-integer path: K > 2^14");
+      const size_t smem = static_cast<size_t>(kr) * 4;
+      if (smem > 48 * 1024) {
+        static bool set[64] = {};
+        int dev = 0;
+        TCK(cudaGetDevice(&dev));
+        if (!set[dev & 63]) {
+          TCK(cudaFuncSetAttribute(quantize_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   128 * 1024));
+          set[dev & 63] = true;
+        }
+      }
+      const unsigned b = static_cast<unsigned>(std::min<uint64_t>(rows, 148 * 8));
+      quantize_rows_smem_kernel<<<b, 256, smem, st>>>(a, rows, kr, op.row_exp);
+    }
   }
+  TCK(cudaGetLastError());
   return 1;
 }
 
@@ -2154,7 +2206,7 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   const uint32_t units = ga ? op.n_ga_groups : op.slots ? op.n_groups : op.nb;
   const uint64_t Nr = 2 * N * (op.slots ? op.slots : 1u), Kr = uint64_t{2} << op.kc;
   const bool qa = tc_i8_prequant(op.kc);
-  if (op.kc > 11) throw std::runtime_error("split-integer path: K > 2^11");
+  if (op.kc > 14) throw std::runtime_error("split-integer path: K > 2^14");  // s32 accumulators
   int launches = 0;
   if (qa && op.quantize_a) launches += launch_quantize(op, st);
   // B̂ digit planes [plane][units * Nr rows][kr_pad], column exponents

@@ -66,8 +66,8 @@ def treesa_binary() -> str:
 
 
 def treesa(net, n_legs, merges, sliced, steps, seed, beta0, beta1, log2_max_table, beta_mem,
-           slice_every, max_slices, chunk=0):
-    lines = [f"{net.n} {n_legs} {net.k} {chunk}"]
+           slice_every, max_slices, chunk=0, alpha=0.0):
+    lines = [f"{net.n} {n_legs} {net.k} {chunk} {alpha}"]
     for i in range(net.n):
         ls = [j for j in range(n_legs) if net.legs[i] >> j & 1]
         lines.append(f"{net.q[i]} {len(ls)} " + " ".join(map(str, ls)))
@@ -99,14 +99,14 @@ def plan_text(n_slots: int, merges, sliced: int) -> str:
 
 
 def search_one(args):
-    (legs, qs, k, n_legs, seed, steps, beta0, beta1, log2_max_table, beta_mem, max_slices, chunk) = args
+    (legs, qs, k, n_legs, seed, steps, beta0, beta1, log2_max_table, beta_mem, max_slices, chunk, alpha) = args
     import treeopt as T
 
     net = T.Network(legs, qs, k)
     rng = random.Random(seed)
     merges = T.bisection_tree(net, rng, cutoff=8, imbalance=0.2, noise=0.5)
     merges, sliced = treesa(net, n_legs, merges, 0, steps, seed, beta0, beta1, log2_max_table, beta_mem,
-                            max(1, steps // 400), max_slices, chunk)
+                            max(1, steps // 400), max_slices, chunk, alpha)
     cost, big, order = T.evaluate(net, merges, sliced, chunk)
     return cost, big, order, merges, sliced, seed
 
@@ -125,6 +125,8 @@ def main():
     ap.add_argument("--beta-mem", type=float, default=4.0)
     ap.add_argument("--max-slices", type=int, default=16)
     ap.add_argument("--chunk", type=int, default=0, help="memo-streaming chunk (requests); 0: none")
+    ap.add_argument("--alpha", type=float, default=10.0,
+                    help="complex MACs per element of traffic (B200 c64: ~500 TF/s / 6.5 TB/s / 8 flop)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     sys.path.insert(0, os.path.join(ROOT, "plans"))
@@ -134,7 +136,7 @@ def main():
 
     treesa_binary()  # build once, before the workers
     jobs = [(legs, qs, a.k, n_legs, 1000 + r, a.steps, a.beta0, a.beta1, a.log2_max_table, a.beta_mem,
-             a.max_slices, a.chunk) for r in range(a.runs)]
+             a.max_slices, a.chunk, a.alpha) for r in range(a.runs)]
     t0 = time.time()
     with Pool(min(a.jobs, a.runs)) as pool:
         results = pool.map(search_one, jobs)

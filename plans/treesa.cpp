@@ -2,8 +2,9 @@
 // 53-qubit workloads; see plans/sycamore_plan.py). The paper's local search
 // (PAPER.md:846-953): rotations (a*b)*c -> (a*c)*b / (c*b)*a of any subtree,
 // objective
-//     f = log2(C) + beta_mem * max(0, log2(table_max / M_max))
-// with the multi-amplitude cost C = S * Σ_nodes k_T 2^|legs L ∪ legs R| and
+//     f = log2(C + α RW) + beta_mem * max(0, log2(table_max / M_max))
+// with the multi-amplitude cost C = S * Σ_nodes k_T
+// 2^|legs L ∪ legs R|, RW = S * Σ_nodes k_T (|L| + |R| + |T|) and
 // memo table k_T 2^|legs T| (k_T: distinct output-bit tuples of the
 // subtree over the k requests, estimated as 2^q (1 - e^(-k/2^q)) for q
 // output qubits; S = 2^sliced). With memo streaming (requests in chunks of
@@ -15,7 +16,8 @@
 // `slice_every` moves a slicing move adds (or swaps) a sliced leg chosen
 // among the legs of the largest tables.
 //
-// stdin: n_leaves n_legs k chunk (memo streaming chunk; 0: none)
+// stdin: n_leaves n_legs k chunk alpha (memo streaming chunk, 0: none;
+//        alpha: complex MACs per element of traffic, the paper's C + αRW)
 //        per leaf: q count leg...
 //        n_merges, then n_merges lines "a b" (ids: leaves 0..n-1, merge i -> n+i)
 //        steps beta0 beta1 log2_max_table beta_mem slice_every max_slices seed
@@ -62,10 +64,16 @@ struct Tree {
     return std::ceil(k / b) * distinct(q, b);
   }
   // cost of internal node v (per slice), and its memo table (one chunk)
+  double alpha = 0;  // complex MACs one element of memory traffic is worth (the paper's C + αRW)
   double node_cost(int v) const {
     const Node& n = nodes[v];
-    const Legs u = (nodes[n.left].legs | nodes[n.right].legs) & ~sliced;
-    return evals(n.q) * std::ldexp(1.0, static_cast<int>(u.count()));
+    const Legs l = nodes[n.left].legs & ~sliced, r = nodes[n.right].legs & ~sliced;
+    const double macs = std::ldexp(1.0, static_cast<int>((l | r).count()));
+    const double rw = alpha > 0 ? std::ldexp(1.0, static_cast<int>(l.count())) +
+                                      std::ldexp(1.0, static_cast<int>(r.count())) +
+                                      std::ldexp(1.0, static_cast<int>((l ^ r).count()))
+                                : 0.0;
+    return evals(n.q) * (macs + alpha * rw);
   }
   double node_table(int v) const {
     return distinct(nodes[v].q, chunk_size()) * std::ldexp(1.0, static_cast<int>((nodes[v].legs & ~sliced).count()));
@@ -98,10 +106,11 @@ int main() {
   Tree T;
   int n_legs;
   double k;
-  double chunk;
-  std::cin >> T.n_leaves >> n_legs >> k >> chunk;
+  double chunk, alpha;
+  std::cin >> T.n_leaves >> n_legs >> k >> chunk >> alpha;
   T.k = k;
   T.chunk = chunk;
+  T.alpha = alpha;
   T.nodes.resize(T.n_leaves);
   for (int i = 0; i < T.n_leaves; ++i) {
     int q, c;

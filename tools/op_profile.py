@@ -38,9 +38,14 @@ def main():
     from paper_2108_05665_b200._lib import lib
     from paper_2108_05665_b200.engine import Engine, EvalOptions
 
+    from bench import WORKLOADS
+
     problem, circ, bits, _ = load_workload(a.config)
     eng = Engine(0)
-    cp = eng.compile(problem, 0, EvalOptions(precision=a.precision))
+    # chunked plans (memo streaming): the ops of chunk 0's schedule (the
+    # request-independent prologue + the first chunk's own ops)
+    cp = eng.compile(problem, 0, EvalOptions(precision=a.precision,
+                                             row_chunk=WORKLOADS[a.config].get("row_chunk", 0)))
     acc = cp.new_accumulator()
     L = lib()
     L.mtcg_plan_op_count.argtypes = [C.c_void_p]
