@@ -139,6 +139,11 @@ typedef struct mtcg_options {
                                        are unchanged, counters stay the
                                        reference's (per-slice) counts. Ignored
                                        under a memory cap. */
+#define MTCG_FLAG_HOST_INDEX 4      /* build the tuple index (plan.cpp:292-333)
+                                       on the host CPU; default on a handle:
+                                       radix sorts on the handle's GPU (same
+                                       rows, ranks and pairs). mtcg_emulate
+                                       always uses the host builder. */
 
 /* eval outputs. `values` is a caller buffer of values_capacity complex
  * elements receiving, request-major, each request's tensor (order-0, or
@@ -281,6 +286,17 @@ mtcg_status mtcg_emulate(const mtcg_problem* p, const mtcg_options* opt,
                          uint64_t cap_bytes, mtcg_plan_info* info,
                          uint64_t* node_contractions, int32_t* cap_node,
                          char* err, size_t errlen);
+
+/* Tuple index check (build_tuple_index, plan.cpp:292-333): builds the index
+ * of `p` with the host builder and on the handle's GPU, compares rows,
+ * row_of_request, the row representatives, every node's distinct count,
+ * (rank_left, rank_right) pairs, leaf value lists and the root's ranks;
+ * *equal = 1 when all match. *rows = the distinct request tuples, host_ms /
+ * device_ms = the two builders' wall times (either pointer may be NULL). */
+mtcg_status mtcg_tuple_index_check(mtcg_handle* h, const mtcg_problem* p,
+                                   int32_t* equal, uint64_t* rows,
+                                   double* host_ms, double* device_ms,
+                                   char* err, size_t errlen);
 
 /* Per-op introspection of a compiled schedule (one op = one batched launch
  * per slice). */

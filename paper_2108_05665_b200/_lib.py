@@ -79,6 +79,7 @@ def lib():
             L.mtcg_plan_op_count.restype = C.c_int32
             L.mtcg_plan_op_info.argtypes = [vp, C.c_int32, C.POINTER(A.mtcg_op_info)]
             L.mtcg_time_ops.argtypes = [vp, C.c_uint64, vp, C.c_int, vp, C.POINTER(C.c_float), cp, sz]
+            L.mtcg_tuple_index_check.argtypes = [vp, pp, i32p, u64p, dp, dp, cp, sz]
             _lib = L
         return _lib
 
@@ -90,5 +91,5 @@ EXPORTS = (
     "mtcg_plan_get_info", "mtcg_run", "mtcg_fetch", "mtcg_xeb_device",
     "mtcg_emulate", "mtcg_launch_count", "mtcg_plan_op_count", "mtcg_plan_op_info",
     "mtcg_time_ops", "mtcg_create_multi", "mtcg_device_count", "mtcg_visible_devices",
-    "mtcg_run_slices_out", "mtcg_fold",
+    "mtcg_run_slices_out", "mtcg_fold", "mtcg_tuple_index_check",
 )

@@ -5,6 +5,7 @@
 
 #include <cstdio>
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <memory>
 
@@ -113,6 +114,11 @@ void check_problem_pointers(const mtcg_problem* p) {
 mtcg_options effective_options(const mtcg_handle* h, mtcg_options o) {
   if (o.memory_cap_bytes || h->cap) o.flags &= ~MTCG_FLAG_SLICE_REUSE;
   return o;
+}
+
+// GPU the tuple index is built on (-1: the host builder, MTCG_FLAG_HOST_INDEX)
+int index_device(const mtcg_handle* h, const mtcg_options& o) {
+  return (o.flags & MTCG_FLAG_HOST_INDEX) ? -1 : engine_device(h->engine);
 }
 
 uint64_t device_cap(const mtcg_handle* h, const mtcg_options& o) {
@@ -249,7 +255,7 @@ struct DevBuf {
 // copies (repeated devices) carry the values; device streams order reuse of
 // the per-device and root buffers across rounds.
 void eval_multi(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, int n_use, mtcg_result* res) {
-  Compiled c = compile_problem(*p, o, device_cap(h, o));
+  Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, o));
   std::vector<std::unique_ptr<DevicePlan>> plans;
   for (int g = 0; g < n_use; ++g) {
     Compiled cg = c;  // host copy per device
@@ -372,7 +378,7 @@ std::unique_ptr<mtcg_plan> compile_chunked(mtcg_handle* h, const mtcg_problem* p
   plan->chunked = std::make_unique<mtcg_plan::Chunked>();
   auto& ch = *plan->chunked;
   // the whole evaluation's exact counts (host only; no device schedule kept)
-  ch.whole = std::make_unique<Compiled>(compile_problem(*p, oc, 0));
+  ch.whole = std::make_unique<Compiled>(compile_problem(*p, oc, 0, nullptr, index_device(h, oc)));
   ch.order.resize(K);
   std::iota(ch.order.begin(), ch.order.end(), 0);
   std::stable_sort(ch.order.begin(), ch.order.end(), [&](uint64_t a, uint64_t b) {
@@ -389,7 +395,7 @@ std::unique_ptr<mtcg_plan> compile_chunked(mtcg_handle* h, const mtcg_problem* p
     mtcg_problem q = *p;
     q.n_requests = r1 - r0;
     q.tuples = tuples.data();
-    auto dp = upload_plan(h->engine, compile_problem(q, oc, device_cap(h, oc), &dep));
+    auto dp = upload_plan(h->engine, compile_problem(q, oc, device_cap(h, oc), &dep, index_device(h, oc)));
     ch.req_off.push_back(r0);
     ch.row_off.push_back(ch.rows);
     ch.rows += dp->c.n_rows;
@@ -525,6 +531,32 @@ void mtcg_destroy(mtcg_handle* h) {
   delete h;
 }
 
+mtcg_status mtcg_tuple_index_check(mtcg_handle* h, const mtcg_problem* p, int32_t* equal, uint64_t* rows,
+                                   double* host_ms, double* device_ms, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!h) throw DataError("null handle");
+    check_problem_pointers(p);
+    using clk = std::chrono::steady_clock;
+    auto t0 = clk::now();
+    const TupleIndex a = tuple_index(*p, -1);
+    auto t1 = clk::now();
+    const TupleIndex b = tuple_index(*p, engine_device(h->engine));
+    auto t2 = clk::now();
+    bool eq = a.rows == b.rows && a.row_of_request == b.row_of_request &&
+              a.row_tuple_first == b.row_tuple_first && a.distinct == b.distinct &&
+              a.rank_value == b.rank_value && a.pair_l == b.pair_l && a.pair_r == b.pair_r;
+    if (eq && a.rows) {
+      const uint32_t* ra = a.rank[p->root];
+      const uint32_t* rb = b.rank[p->root];
+      eq = ra && rb && std::equal(ra, ra + a.rows, rb);
+    }
+    if (equal) *equal = eq;
+    if (rows) *rows = a.rows;
+    if (host_ms) *host_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (device_ms) *device_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
+  });
+}
+
 mtcg_status mtcg_emulate(const mtcg_problem* p, const mtcg_options* opt, uint64_t cap_bytes,
                          mtcg_plan_info* info, uint64_t* node_contractions, int32_t* cap_node,
                          char* err, size_t errlen) {
@@ -549,7 +581,7 @@ mtcg_status mtcg_compile(mtcg_handle* h, const mtcg_problem* p, const mtcg_optio
       *out = compile_chunked(h, p, o).release();
       return;
     }
-    Compiled c = compile_problem(*p, o, device_cap(h, o));
+    Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, o));
     auto plan = std::make_unique<mtcg_plan>();
     plan->dp = upload_plan(h->engine, std::move(c));
     *out = plan.release();
@@ -672,7 +704,7 @@ mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p, const mtcg_options*
       eval_chunked(h, p, o, res);
       return;
     }
-    Compiled c = compile_problem(*p, o, device_cap(h, o));
+    Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, o));
     mtcg_plan plan;
     plan.dp = upload_plan(h->engine, std::move(c));
     const Compiled& cc = plan.dp->c;

@@ -27,6 +27,7 @@
 #include <cstring>
 #include <map>
 #include <numeric>
+#include <thread>
 
 #include "configs.hpp"
 
@@ -88,16 +89,7 @@ PlanIdx index_plan(const mtcg_problem& p) {
   return ix;
 }
 
-struct TupleIndex {
-  uint64_t rows = 0;
-  std::vector<uint32_t> row_tuple_first;  // request index representing row
-  std::vector<uint64_t> row_of_request;
-  // rank of every row per node: views into one pooled buffer (see below)
-  std::vector<uint32_t*> rank;                    // [node] -> [row]
-  std::vector<std::vector<uint32_t>> rank_value;  // leaves: rank -> value index
-  std::vector<std::vector<uint32_t>> pair_l, pair_r;  // internal: rank -> child ranks
-  std::vector<uint32_t> distinct;
-};
+
 
 // build_tuple_index (plan.cpp:292-333). Rows are the distinct request tuples
 // in lexicographic order; rank[node][row] is the dense rank of the row's
@@ -361,8 +353,67 @@ struct SectionTimer {
 };
 }  // namespace
 
+namespace {
+// check_inputs' tuple range check (multieval.cpp:284-297; the first offending
+// entry in request-major order names the slot), fused with the extraction of
+// the informative columns for the device tuple index (colsT != nullptr);
+// split over host threads for large batches.
+void check_tuples(const mtcg_problem& p, const std::vector<int>& informative, std::vector<uint32_t>* colsT) {
+  const uint64_t k = p.n_requests;
+  const int m = p.n_slots;
+  const size_t w = informative.size();
+  if (colsT) colsT->resize(std::max<size_t>(w, 1) * k);
+  uint32_t* out = colsT ? colsT->data() : nullptr;
+  auto range = [&](uint64_t i0, uint64_t i1) -> uint64_t {  // first bad flat index or ~0
+    for (uint64_t i = i0; i < i1; ++i) {
+      const uint32_t* t = p.tuples + i * m;
+      for (int j = 0; j < m; ++j)
+        if (t[j] >= static_cast<uint32_t>(p.slot_n_values[j])) return i * m + j;
+      if (out)
+        for (size_t c = 0; c < w; ++c) out[c * k + i] = t[informative[c]];
+    }
+    return ~uint64_t{0};
+  };
+  uint64_t bad = ~uint64_t{0};
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const unsigned nt = k * static_cast<uint64_t>(m) >= (uint64_t{1} << 22) ? hw : 1;
+  if (nt == 1) {
+    bad = range(0, k);
+  } else {
+    uint64_t first[16];
+    std::thread th[16];
+    for (unsigned t = 0; t < nt; ++t)
+      th[t] = std::thread([&, t] { first[t] = range(k * t / nt, k * (t + 1) / nt); });
+    for (unsigned t = 0; t < nt; ++t) {
+      th[t].join();
+      bad = std::min(bad, first[t]);
+    }
+  }
+  if (bad != ~uint64_t{0})
+    throw DataError(fmt("request tuple indexes past slot %lld's value set", static_cast<long long>(bad % m)));
+}
+
+std::vector<int> informative_slots(const mtcg_problem& p) {
+  std::vector<int> v;
+  for (int j = 0; j < p.n_slots; ++j)
+    if (p.slot_n_values[j] > 1) v.push_back(j);
+  return v;
+}
+}  // namespace
+
+TupleIndex tuple_index(const mtcg_problem& p, int device) {
+  const PlanIdx ix = index_plan(p);
+  TupleIndex ti;
+  const std::vector<int> inf = informative_slots(p);
+  std::vector<uint32_t> colsT;
+  check_tuples(p, inf, device >= 0 ? &colsT : nullptr);
+  if (device < 0 || !build_tuple_index_device(p, ix.postorder, inf, colsT, device, ti)) ti = build_tuple_index(p, ix);
+  return ti;
+}
+
 Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
-                         uint64_t cap_bytes, const std::vector<char>* request_dependent_slots) {
+                         uint64_t cap_bytes, const std::vector<char>* request_dependent_slots,
+                         int index_device) {
   PhaseTimer timer;
   Compiled c;
   c.precision = opt.precision;
@@ -377,10 +428,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
 
   // --- check_inputs (multieval.cpp:284-297) --------------------------------
   const PlanIdx ix = index_plan(p);
-  for (uint64_t i = 0; i < p.n_requests; ++i)
-    for (int j = 0; j < p.n_slots; ++j)
-      if (p.tuples[i * p.n_slots + j] >= static_cast<uint32_t>(p.slot_n_values[j]))
-        throw DataError(fmt("request tuple indexes past slot %lld's value set", j));
+  const std::vector<int> informative = informative_slots(p);
+  static thread_local std::vector<uint32_t> colsT;  // informative columns for the device index
+  check_tuples(p, informative, index_device >= 0 ? &colsT : nullptr);
   for (int j = 0; j < p.n_slots; ++j)
     if (p.slot_n_values[j] < 1)
       throw DataError(fmt("slot %lld has an empty value set", j));
@@ -440,7 +490,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
 
   timer.mark("validate+leaves");
   // --- tuple index ----------------------------------------------------------
-  TupleIndex ti = build_tuple_index(p, ix);
+  TupleIndex ti;
+  if (index_device < 0 || !build_tuple_index_device(p, ix.postorder, informative, colsT, index_device, ti))
+    ti = build_tuple_index(p, ix);
   c.n_requests = p.n_requests;
   c.n_rows = ti.rows;
   c.row_of_request = ti.row_of_request;

@@ -196,6 +196,35 @@ struct Compiled {
   }
 };
 
+// build_tuple_index (plan.cpp:292-333) output. Rows are the distinct request
+// tuples in lexicographic order; a node's dense ranks order its distinct
+// restrictions by (rank_left, rank_right).
+struct TupleIndex {
+  uint64_t rows = 0;
+  std::vector<uint32_t> row_tuple_first;  // request index representing row
+  std::vector<uint64_t> row_of_request;
+  // rank of every row per node (host builder: every node; device builder:
+  // the root only, in root_rank)
+  std::vector<uint32_t*> rank;                    // [node] -> [row]
+  std::vector<uint32_t> root_rank;
+  std::vector<std::vector<uint32_t>> rank_value;  // leaves: rank -> value index
+  std::vector<std::vector<uint32_t>> pair_l, pair_r;  // internal: rank -> child ranks
+  std::vector<uint32_t> distinct;
+};
+
+// Device builder (index.cu): radix sorts on GPU `device`, same TupleIndex as
+// the host builder. `postorder` lists children before parents; colsT holds
+// the informative slots' columns (slots with more than one value, ascending),
+// column-major [informative.size()][n_requests]. Returns false when it does
+// not apply (no requests).
+bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& postorder,
+                              const std::vector<int>& informative, const std::vector<uint32_t>& colsT, int device,
+                              TupleIndex& ti);
+
+// The tuple index alone (index_plan's checks, then the device builder on
+// `device` >= 0 or the host builder): diagnostics / tests.
+TupleIndex tuple_index(const mtcg_problem& p, int device);
+
 // Validates `p` with the reference's checks and messages, builds the tuple
 // index and the schedule. cap_bytes = 0: no cap. Throws DataError /
 // MemoryCapError.
@@ -207,6 +236,8 @@ struct Compiled {
 // are the same in every chunk's schedule.
 Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
                          uint64_t cap_bytes,
-                         const std::vector<char>* request_dependent_slots = nullptr);
+                         const std::vector<char>* request_dependent_slots = nullptr,
+                         int index_device = -1);
+// index_device >= 0: build the tuple index on that GPU (build_tuple_index_device)
 
 }  // namespace mtcg

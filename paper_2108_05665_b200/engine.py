@@ -49,6 +49,9 @@ class EvalOptions:
     # memo streaming: requests in lexicographic chunks of this many (one-shot
     # eval; 0 = all at once)
     row_chunk: int = 0
+    # tuple index (plan.cpp:292-333) on the GPU (default) or the host CPU
+    # (MTCG_FLAG_HOST_INDEX); same rows, ranks and pairs either way
+    device_index: bool = True
 
 
 @dataclass
@@ -123,7 +126,8 @@ def _options(mode: int, opts: Optional[EvalOptions]) -> A.mtcg_options:
     o.precision = PRECISIONS[opts.precision]
     o.memory_cap_bytes = int(opts.memory_cap_bytes)
     o.workers = int(opts.workers)
-    o.flags = (0 if opts.tensor_cores else 1) | (2 if opts.slice_reuse else 0)  # MTCG_FLAG_*
+    o.flags = ((0 if opts.tensor_cores else 1) | (2 if opts.slice_reuse else 0)
+               | (0 if opts.device_index else 4))  # MTCG_FLAG_*
     o.row_chunk = int(opts.row_chunk)
     return o
 
@@ -300,6 +304,18 @@ class Engine:
         if st:
             _raise(st, err, cap_node.value)
         return CompiledProblem(self, h, problem)
+
+    def tuple_index_check(self, problem: A.ProblemArrays):
+        """Build the tuple index on the host and on this GPU and compare them
+        (mtcg_tuple_index_check). Returns (equal, rows, host_ms, device_ms)."""
+        eq, rows = C.c_int32(0), C.c_uint64(0)
+        hm, dm = C.c_double(0), C.c_double(0)
+        err = C.create_string_buffer(1024)
+        st = lib().mtcg_tuple_index_check(self.h, C.byref(problem.struct()), C.byref(eq), C.byref(rows),
+                                          C.byref(hm), C.byref(dm), err, 1024)
+        if st:
+            _raise(st, err)
+        return bool(eq.value), int(rows.value), hm.value, dm.value
 
     def linear_xeb(self, n: int, probs) -> float:
         p = np.ascontiguousarray(probs, dtype=np.float64)
