@@ -140,10 +140,12 @@ typedef struct mtcg_options {
                                        reference's (per-slice) counts. Ignored
                                        under a memory cap. */
 #define MTCG_FLAG_HOST_INDEX 4      /* build the tuple index (plan.cpp:292-333)
-                                       on the host CPU; default on a handle:
-                                       radix sorts on the handle's GPU (same
-                                       rows, ranks and pairs). mtcg_emulate
-                                       always uses the host builder. */
+                                       on the host CPU */
+#define MTCG_FLAG_DEVICE_INDEX 8    /* build it with radix sorts on the
+                                       handle's GPU (same rows, ranks and
+                                       pairs). Neither flag: the GPU from
+                                       2^15 requests up, else the host.
+                                       mtcg_emulate always uses the host. */
 
 /* eval outputs. `values` is a caller buffer of values_capacity complex
  * elements receiving, request-major, each request's tensor (order-0, or

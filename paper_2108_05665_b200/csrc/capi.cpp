@@ -116,9 +116,13 @@ mtcg_options effective_options(const mtcg_handle* h, mtcg_options o) {
   return o;
 }
 
-// GPU the tuple index is built on (-1: the host builder, MTCG_FLAG_HOST_INDEX)
-int index_device(const mtcg_handle* h, const mtcg_options& o) {
-  return (o.flags & MTCG_FLAG_HOST_INDEX) ? -1 : engine_device(h->engine);
+// GPU the tuple index is built on (-1: the host builder). Below 2^15
+// requests the host builder is as fast (k = 10^4: 4.9 vs 4.3 ms) and leaves
+// the GPU to the previous evaluation's kernels.
+int index_device(const mtcg_handle* h, const mtcg_problem& p, const mtcg_options& o) {
+  if (o.flags & MTCG_FLAG_HOST_INDEX) return -1;
+  if (!(o.flags & MTCG_FLAG_DEVICE_INDEX) && p.n_requests < (uint64_t{1} << 15)) return -1;
+  return engine_device(h->engine);
 }
 
 uint64_t device_cap(const mtcg_handle* h, const mtcg_options& o) {
@@ -255,7 +259,7 @@ struct DevBuf {
 // copies (repeated devices) carry the values; device streams order reuse of
 // the per-device and root buffers across rounds.
 void eval_multi(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, int n_use, mtcg_result* res) {
-  Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, o));
+  Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, *p, o));
   std::vector<std::unique_ptr<DevicePlan>> plans;
   for (int g = 0; g < n_use; ++g) {
     Compiled cg = c;  // host copy per device
@@ -378,7 +382,7 @@ std::unique_ptr<mtcg_plan> compile_chunked(mtcg_handle* h, const mtcg_problem* p
   plan->chunked = std::make_unique<mtcg_plan::Chunked>();
   auto& ch = *plan->chunked;
   // the whole evaluation's exact counts (host only; no device schedule kept)
-  ch.whole = std::make_unique<Compiled>(compile_problem(*p, oc, 0, nullptr, index_device(h, oc)));
+  ch.whole = std::make_unique<Compiled>(compile_problem(*p, oc, 0, nullptr, index_device(h, *p, oc)));
   ch.order.resize(K);
   std::iota(ch.order.begin(), ch.order.end(), 0);
   std::stable_sort(ch.order.begin(), ch.order.end(), [&](uint64_t a, uint64_t b) {
@@ -395,7 +399,7 @@ std::unique_ptr<mtcg_plan> compile_chunked(mtcg_handle* h, const mtcg_problem* p
     mtcg_problem q = *p;
     q.n_requests = r1 - r0;
     q.tuples = tuples.data();
-    auto dp = upload_plan(h->engine, compile_problem(q, oc, device_cap(h, oc), &dep, index_device(h, oc)));
+    auto dp = upload_plan(h->engine, compile_problem(q, oc, device_cap(h, oc), &dep, index_device(h, q, oc)));
     ch.req_off.push_back(r0);
     ch.row_off.push_back(ch.rows);
     ch.rows += dp->c.n_rows;
@@ -581,7 +585,7 @@ mtcg_status mtcg_compile(mtcg_handle* h, const mtcg_problem* p, const mtcg_optio
       *out = compile_chunked(h, p, o).release();
       return;
     }
-    Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, o));
+    Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, *p, o));
     auto plan = std::make_unique<mtcg_plan>();
     plan->dp = upload_plan(h->engine, std::move(c));
     *out = plan.release();
@@ -704,7 +708,7 @@ mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p, const mtcg_options*
       eval_chunked(h, p, o, res);
       return;
     }
-    Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, o));
+    Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, *p, o));
     mtcg_plan plan;
     plan.dp = upload_plan(h->engine, std::move(c));
     const Compiled& cc = plan.dp->c;

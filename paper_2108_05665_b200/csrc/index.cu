@@ -343,7 +343,11 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
     ~Restore() { cudaSetDevice(d); }
   } restore{prev};
   cudaStream_t st;
-  IK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  // highest priority: the index usually runs while the previous
+  // evaluation's kernels still occupy the GPU
+  int prio_lo = 0, prio_hi = 0;
+  IK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  IK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio_hi));
   struct StreamGuard {
     cudaStream_t s;
     ~StreamGuard() { cudaStreamDestroy(s); }

@@ -833,13 +833,36 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         g_max = 0;
       }
     }
-    const bool grouped = g_max > 0;
-    // tensor-path slots per group: 2 N x slots a multiple of 32 real columns
-    uint32_t tc_slots = g_max;
-    if (grouped && op.fb < 4) {
-      const uint32_t q = 16u >> op.fb;  // slots per 32 real columns
-      tc_slots = (g_max + q - 1) / q * q;
+    // Tensor-path groups: every unit is padded to `tc_slots` item blocks, and
+    // the epilogue drains the padding too, so large groups are cut into
+    // sub-groups of S items with S minimising units x (K + S N) — one A row
+    // read per unit plus S item blocks drained per row (S = 1: no grouping).
+    // 2 N S must be a multiple of 32 real columns.
+    std::vector<uint32_t> tg_start;
+    uint32_t tc_slots = 0;
+    if (g_max > 0) {
+      const uint32_t q = op.fb < 4 ? 16u >> op.fb : 1u;  // slots per 32 real columns
+      const double Kd = std::ldexp(1.0, op.kc), Nd = std::ldexp(1.0, op.fb);
+      double best = 0;
+      for (uint32_t S = q; S < 2 * std::max(g_max, q); S *= 2) {
+        uint64_t units_s = 0;
+        for (size_t g = 0; g + 1 < g_start.size(); ++g) units_s += (g_start[g + 1] - g_start[g] + S - 1) / S;
+        const double cost = double(units_s) * (Kd + S * Nd);
+        if (tc_slots == 0 || cost < best) {
+          best = cost;
+          tc_slots = S;
+        }
+      }
+      if (tc_slots > 1) {
+        tg_start.push_back(0);
+        for (size_t g = 0; g + 1 < g_start.size(); ++g)
+          for (uint32_t i = g_start[g] + tc_slots; i < g_start[g + 1] + tc_slots; i += tc_slots)
+            tg_start.push_back(std::min(i, g_start[g + 1]));
+      } else {
+        tc_slots = 0;
+      }
     }
+    const bool grouped = tc_slots > 0;
     // Tensor-core path (complex64 only): dense, K-contiguous intermediate A,
     // shapes the 128 x (2N) x (2K) real tiles cover exactly.
     // Ops with intensity MNK / (MK + NK + MN) >= 6 complex MACs per element
@@ -852,7 +875,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     const double Md = std::ldexp(1.0, op.fa), Nd = std::ldexp(1.0, fb_eff),
                  Kd = std::ldexp(1.0, op.kc);
     const double intensity = Md * Nd * Kd / (Md * Kd + Nd * Kd + Md * Nd);
-    const uint64_t units = grouped ? uint64_t{g_start.size() - 1} : op.nb;
+    const uint64_t units = grouped ? uint64_t{tg_start.size() - 1} : op.nb;
     const bool tc_ok = c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) &&
                        !op.a_leaf && op.fa >= 7 && fb_eff >= tc_min_fb && op.kc >= 4 &&
                        fb_eff <= 12 && op.kc <= 14 && intensity >= 6.0 && (!grouped || op.fa >= 12) &&
@@ -896,14 +919,14 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         }
         s0 = s1;
       }
-    } else if (grouped && op.fb <= 4 && op.kc <= 5 && op.fa >= 8 &&
+    } else if (g_max > 0 && op.fb <= 4 && op.kc <= 5 && op.fa >= 8 &&
                ((uint64_t{g_max} << (op.fb + op.kc)) * c.elem_bytes) <= kGroupSmemBytes) {
       op.config = kRowsGroupedConfig;
       op.grp_max = g_max;
     }
     if (op.grp_max) {
       op.grp_items = std::move(g_order);
-      op.grp_start = std::move(g_start);
+      op.grp_start = op.config == kTcConfig ? std::move(tg_start) : std::move(g_start);
     }
     sec.lap(1);
     // m / n bit orders: free legs by increasing address in the output layout;
@@ -1492,6 +1515,21 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       std::fprintf(stderr, "[mtcg]   deps");
       for (int d : op.deps) std::fprintf(stderr, " %d", c.ops[d].node);
       std::fprintf(stderr, "\n");
+      // per-bit strides (elements) of the op's index spaces
+      auto bit_strides = [](const char* name, const SplitTable& t) {
+        std::fprintf(stderr, "[mtcg]   %s:", name);
+        for (int b = 0; b < t.bits; ++b) {
+          const uint64_t v = b < t.lo_bits ? t.lo[uint64_t{1} << b] : t.hi[uint64_t{1} << (b - t.lo_bits)];
+          std::fprintf(stderr, " %llu", static_cast<unsigned long long>(v));
+        }
+        std::fprintf(stderr, "\n");
+      };
+      bit_strides("A m", op.tam);
+      bit_strides("A k", op.tak);
+      bit_strides("B n", op.tbn);
+      bit_strides("B k", op.tbk);
+      bit_strides("out m", op.tom);
+      bit_strides("out n", op.ton);
     }
   }
   return c;

@@ -49,9 +49,10 @@ class EvalOptions:
     # memo streaming: requests in lexicographic chunks of this many (one-shot
     # eval; 0 = all at once)
     row_chunk: int = 0
-    # tuple index (plan.cpp:292-333) on the GPU (default) or the host CPU
-    # (MTCG_FLAG_HOST_INDEX); same rows, ranks and pairs either way
-    device_index: bool = True
+    # tuple index (plan.cpp:292-333): None = the GPU from 2^15 requests up,
+    # else the host; True / False force the GPU (MTCG_FLAG_DEVICE_INDEX) / the
+    # host (MTCG_FLAG_HOST_INDEX). Same rows, ranks and pairs either way.
+    device_index: Optional[bool] = None
 
 
 @dataclass
@@ -127,7 +128,7 @@ def _options(mode: int, opts: Optional[EvalOptions]) -> A.mtcg_options:
     o.memory_cap_bytes = int(opts.memory_cap_bytes)
     o.workers = int(opts.workers)
     o.flags = ((0 if opts.tensor_cores else 1) | (2 if opts.slice_reuse else 0)
-               | (0 if opts.device_index else 4))  # MTCG_FLAG_*
+               | {None: 0, True: 8, False: 4}[opts.device_index])  # MTCG_FLAG_*
     o.row_chunk = int(opts.row_chunk)
     return o
 

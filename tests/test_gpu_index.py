@@ -79,6 +79,6 @@ def test_device_index_chunked(engine):
     """Memo streaming compiles every chunk with the device index."""
     p, c, _ = workload("cfg1")
     want, want_nc, _, _ = O.eval_problem(p)
-    got = engine.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", row_chunk=300))
+    got = engine.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", row_chunk=300, device_index=True))
     assert bits_equal(got.amplitudes, want)
     assert np.array_equal(got.node_contractions, want_nc)
