@@ -45,6 +45,10 @@ constexpr int kDotConfig = 15;
 // Member of a fused operand chain (planner.hpp Chain; reported by op_info —
 // the chain's last op launches the chain kernel, the others nothing).
 constexpr int kChainConfig = 16;
+// Small M x N (M <= 16, 8 <= N <= 16) with a long K (>= 512), both operands
+// K-contiguous intermediates, complex64: one CTA per item streams A and B
+// through a cp.async ring, warps own 4 x 8 output blocks, lanes split K.
+constexpr int kLongKConfig = 17;
 // shared-memory budget for one group's B blocks (bytes)
 constexpr int kGroupSmemBytes = 48 * 1024;
 

@@ -823,6 +823,119 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---- small M x N, long K (complex64) ---------------------------------------------
+// One CTA per item (grid-stride): A (M x K) and B (N x K), both K-contiguous,
+// stream through a kLkStages-deep cp.async ring of kLkKT-wide K tiles (each
+// operand element read from HBM once); warp w owns the 4 x 8 output block at
+// m0 = 4 (w & 3), n0 = 8 (w >> 2); its lanes split each tile's K (lane,
+// lane + 32) and a butterfly reduction combines them. Bound: HBM (16 x 16 x
+// 16384 per item: 4 MB read for 16.8 M FMA).
+constexpr int kLkKT = 64;      // complex K per stage
+constexpr int kLkStages = 6;   // 6 x 16 KB ring
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(256, 1)
+    contract_longk(const DevOp<float2> op_in) {
+  DevOp<float2> op = op_in;
+  resolve_slice(op);
+  extern __shared__ float4 lk_smem[];
+  float2* ring = reinterpret_cast<float2*>(lk_smem);  // [stage][A 16 rows | B 16 rows][kLkKT]
+  const int M = 1 << op.fa, N = 1 << op.fb;
+  const int n_tiles = 1 << (op.kc - 6);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m0 = 4 * (warp & 3), n0 = 8 * (warp >> 2);
+  const bool active = m0 < M && n0 < N;
+  // loader: thread t copies 16 B (2 complex) at row t >> 4 (of 16), column
+  // 2 (t & 15) and + 32 complex, for A then B
+  const int lrow = tid >> 4, lcol = 2 * (tid & 15);
+  for (uint64_t item = blockIdx.x; item < op.nb; item += gridDim.x) {
+    const float2* A = op.a + uint64_t{op.ia ? __ldg(op.ia + item) : static_cast<uint32_t>(item)} * op.a_item + op.a_slice;
+    const float2* B = op.b + uint64_t{op.ib ? __ldg(op.ib + item) : static_cast<uint32_t>(item)} * op.b_item + op.b_slice;
+    const float2* arow = lrow < M ? A + op.tam(lrow) : nullptr;
+    const float2* brow = lrow < N ? B + op.tbn(lrow) : nullptr;
+    auto issue = [&](int t) {
+      if (t < n_tiles) {
+        float2* st = ring + (t % kLkStages) * (32 * kLkKT);
+        const uint64_t k0 = uint64_t(t) * kLkKT;
+        if (arow) {
+          cp_async16(st + lrow * kLkKT + lcol, arow + k0 + lcol);
+          cp_async16(st + lrow * kLkKT + lcol + 32, arow + k0 + lcol + 32);
+        }
+        if (brow) {
+          cp_async16(st + (16 + lrow) * kLkKT + lcol, brow + k0 + lcol);
+          cp_async16(st + (16 + lrow) * kLkKT + lcol + 32, brow + k0 + lcol + 32);
+        }
+      }
+      cp_async_commit();
+    };
+    float2 acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t < kLkStages - 1; ++t) issue(t);
+    for (int t = 0; t < n_tiles; ++t) {
+      cp_async_wait<kLkStages - 2>();
+      __syncthreads();  // tile t visible to all; tile t - 1's slot free
+      issue(t + kLkStages - 1);
+      if (active) {
+        const float2* st = ring + (t % kLkStages) * (32 * kLkKT);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = lane + 32 * h;
+          float2 a[4], b[8];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = st[(m0 + i) * kLkKT + k];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) b[j] = st[(16 + n0 + j) * kLkKT + k];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              acc[i][j].x = fmaf(a[i].x, b[j].x, fmaf(-a[i].y, b[j].y, acc[i][j].x));
+              acc[i][j].y = fmaf(a[i].x, b[j].y, fmaf(a[i].y, b[j].x, acc[i][j].y));
+            }
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // the ring is reused by the next item
+    if (active) {
+      // butterfly over the lanes: every lane ends with the block's sums
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int sh = 16; sh > 0; sh >>= 1) {
+            acc[i][j].x += __shfl_xor_sync(0xffffffffu, acc[i][j].x, sh);
+            acc[i][j].y += __shfl_xor_sync(0xffffffffu, acc[i][j].y, sh);
+          }
+      // lane l stores element (l >> 3, l & 7) of the block
+      const int i = lane >> 3, j = lane & 7;
+      float2 v = acc[0][0];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y)
+          if (x == i && y == j) v = acc[x][y];
+      if (m0 + i < M && n0 + j < N) {
+        float2* dst = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + item)} : item) * op.out_item +
+                      op.tom(m0 + i) + op.ton(n0 + j);
+        *dst = op.accumulate ? cadd(*dst, v) : v;
+      }
+    }
+  }
+}
+
 // ---- single-slot network: every row's value is the projected leaf ----------------
 
 template <class T>
@@ -1059,6 +1172,21 @@ void launch_op(const DevOp<typename V2<R>::T>& op, int config, cudaStream_t st) 
   switch (config) {
     case kRowsConfig: return launch_rows<R>(op, st);
     case kRowsGroupedConfig: return launch_rows_grouped<R>(op, st);
+    case kLongKConfig:
+      if constexpr (sizeof(R) == 4) {
+        const size_t smem = sizeof(float2) * kLkStages * 32 * kLkKT;
+        static bool attr_set[kMaxDevices] = {};
+        const int dev = current_device();
+        if (!attr_set[dev]) {
+          CK(cudaFuncSetAttribute(contract_longk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+          attr_set[dev] = true;
+        }
+        const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>(op.nb, kSmSlots * 2));
+        contract_longk<<<blocks, 256, smem, st>>>(op);
+        return;
+      }
+      throw CudaError("long-K kernel: complex64 only");
     case kDotConfig:
       if constexpr (sizeof(R) == 4) {
         const uint64_t warps = uint64_t{op.nb} << (op.fa + op.fb);

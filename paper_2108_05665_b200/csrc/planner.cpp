@@ -976,6 +976,11 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       const auto ms = strides_of(m_legs, out_layout);
       op.o_mcontig = !ms.empty() && ms[0] == 1;
     }
+    // long-K small tiles (cfg3 node 619: 16 x 16 x 16384 per item) stream
+    // both operands once instead of through 16 x 16 smem k-steps
+    if (c.precision == MTCG_C64 && op.config != kTcConfig && op.grp_max == 0 && op.fa >= 2 && op.fa <= 4 &&
+        op.fb >= 3 && op.fb <= 4 && op.kc >= 9 && op.a_kcontig && op.b_kcontig && !std::getenv("MTCG_NO_LONGK"))
+      op.config = kLongKConfig;
 
     sec.lap(2);
     // sliced legs carried by leaf operands: offsets per set bit of the slice

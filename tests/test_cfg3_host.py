@@ -1,0 +1,21 @@
+"""cfg3's exact algorithmic totals: the engine's shape replay (mtcg_emulate)
+of the whole 10^4-bitstring evaluation equals the unmodified reference's
+CostedPlan totals recorded with the golden amplitudes
+(tests/golden/make_cfg3_reference.py; plan.cpp:497-502)."""
+import os
+
+import numpy as np
+
+from paper_2108_05665_b200.engine import EvalOptions, emulate_arrays
+
+from .helpers import ROOT
+
+
+def test_cfg3_counts_equal_reference():
+    import bench
+    g = np.load(os.path.join(ROOT, "tests", "golden", "cfg3_reference.npz"))
+    p, _, _, _ = bench.load_workload("cfg3")
+    r = emulate_arrays(p, EvalOptions(precision="c128"))
+    assert str(r.counters.mults) == str(g["mults_str"])
+    assert str(r.counters.adds) == str(g["adds_str"])
+    assert str(r.counters.rw) == str(g["rw_str"])
