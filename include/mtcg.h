@@ -59,7 +59,8 @@ typedef enum mtcg_status {
   MTCG_ERR_MEMORY_CAP = 3,
   MTCG_ERR_CUDA = 5,
   MTCG_ERR_ARGUMENT = 6,
-  MTCG_ERR_NCCL = 7
+  MTCG_ERR_NCCL = 7,
+  MTCG_ERR_PARSE = 8
 } mtcg_status;
 
 /* Arithmetic of the device path.
@@ -299,6 +300,48 @@ mtcg_status mtcg_tuple_index_check(mtcg_handle* h, const mtcg_problem* p,
                                    int32_t* equal, uint64_t* rows,
                                    double* host_ms, double* device_ms,
                                    char* err, size_t errlen);
+
+/* ---- paper-scale request ingestion (host, multithreaded) -------------------
+ * read_samples (formats.cpp:42-69): parses a samples text of `len` bytes —
+ * one string over {0,1,*} per line, '#' comments, blank lines skipped, one
+ * length and one '*' pattern — into `out` [n_rows][n_qubits] canonical
+ * characters (qubit 0 first; bit_order 1 = the text has qubit 0 last).
+ * out_capacity >= len always suffices. MTCG_ERR_PARSE carries the
+ * reference's message ("line N: ..."). */
+mtcg_status mtcg_read_samples(const char* text, uint64_t len, int32_t bit_order,
+                              char* out, uint64_t out_capacity,
+                              uint64_t* n_rows, int32_t* n_qubits,
+                              char* err, size_t errlen);
+
+/* build_assignments' ranking (diagram.cpp:229-297): slot j's fixed bits are
+ * the sample characters at qubits slot_qubits[slot_qubit_begin[j] ..
+ * slot_qubit_begin[j+1]) (its open legs in slot_open_legs order) that are not
+ * batch positions (the '*' columns of sample 0; every sample must agree).
+ * Outputs: tuples [n_rows][n_slots] (mtcg_problem.tuples), slot_n_values
+ * [n_slots], and the distinct fixed-bit tuples of every slot ascending —
+ * packed with the first fixed bit most significant — in value_keys
+ * [value_key_begin[j] .. value_key_begin[j+1]) (value_key_begin [n_slots+1];
+ * a slot without fixed bits has the one key 0: its unprojected tensor).
+ * keys_capacity >= n_slots * min(n_rows, 2^max fixed bits) suffices. The
+ * value tensors are the slot tensors projected on those bits (project_leg,
+ * tensor.cpp:255-282). */
+mtcg_status mtcg_assign(const char* samples, uint64_t n_rows, int32_t n_qubits,
+                        int32_t n_slots, const int32_t* slot_qubit_begin,
+                        const int32_t* slot_qubits, uint32_t* tuples,
+                        int32_t* slot_n_values, uint64_t* value_key_begin,
+                        uint32_t* value_keys, uint64_t keys_capacity,
+                        char* err, size_t errlen);
+
+/* Amplitude TSV (format_amplitude_row, formats.cpp:78-83): one row
+ * "bits<TAB>%.16e<TAB>%.16e" per request and batch value, '*' positions
+ * expanded in row-major order of the batch legs (tools/main.cpp:161-179);
+ * values [n_rows][2^w] complex doubles (mtcg_result.values). Writes `path`;
+ * *written = bytes. */
+mtcg_status mtcg_write_amplitudes(const char* path, const char* samples,
+                                  uint64_t n_rows, int32_t n_qubits,
+                                  int32_t bit_order, const double* values,
+                                  int32_t w, uint64_t* written, char* err,
+                                  size_t errlen);
 
 /* Per-op introspection of a compiled schedule (one op = one batched launch
  * per slice). */

@@ -32,6 +32,7 @@
 #include "mtc/circuit.hpp"
 #include "mtc/diagram.hpp"
 #include "mtc/errors.hpp"
+#include "mtc/formats.hpp"
 #include "mtc/multieval.hpp"
 #include "mtc/optimizer.hpp"
 #include "mtc/plan.hpp"
@@ -588,6 +589,36 @@ int ref_statevector(const char* circuit_text, const char* bitstrings_nl,
   } catch (...) {
     return classify(std::current_exception(), nullptr);
   }
+}
+
+// ---- request ingestion (formats.cpp:42-83) ---------------------------------
+
+int ref_read_samples(const char* text, std::uint64_t len, int order, char* out, std::uint64_t cap,
+                     std::uint64_t* n_rows, int* n_qubits) {
+  try {
+    std::istringstream in(std::string(text, len));
+    const std::vector<std::string> v =
+        read_samples(in, order ? BitOrder::kQubit0Last : BitOrder::kQubit0First);
+    std::uint64_t o = 0;
+    for (const std::string& r : v) {
+      if (o + r.size() > cap) throw std::runtime_error("capacity");
+      std::memcpy(out + o, r.data(), r.size());
+      o += r.size();
+    }
+    *n_rows = v.size();
+    *n_qubits = v.empty() ? 0 : static_cast<int>(v.front().size());
+    return 0;
+  } catch (...) {
+    return classify(std::current_exception(), nullptr);
+  }
+}
+
+int ref_format_amplitude_row(const char* bits, double re, double im, int order, char* out, std::uint64_t cap) {
+  const std::string r = format_amplitude_row(std::string(bits), {re, im},
+                                             order ? BitOrder::kQubit0Last : BitOrder::kQubit0First);
+  if (r.size() + 1 > cap) return 1;
+  std::memcpy(out, r.c_str(), r.size() + 1);
+  return 0;
 }
 
 int ref_linear_xeb(int n, const double* probs, std::uint64_t count,

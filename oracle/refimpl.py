@@ -40,6 +40,8 @@ def lib():
         L.ref_problem_new.restype = vp
         L.ref_problem_new.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_char_p]
         L.ref_problem_free.argtypes = [vp]
+        L.ref_read_samples.argtypes = [C.c_char_p, C.c_uint64, C.c_int, vp, C.c_uint64, u64p, ip]
+        L.ref_format_amplitude_row.argtypes = [C.c_char_p, C.c_double, C.c_double, C.c_int, vp, C.c_uint64]
         L.ref_set_plan.argtypes = [vp, C.c_char_p]
         L.ref_plan_text.restype = vp
         L.ref_plan_text.argtypes = [vp]
@@ -135,6 +137,24 @@ def linear_xeb(n: int, probs: np.ndarray) -> float:
     if rc:
         raise RefError(rc, lib().ref_last_error().decode())
     return out.value
+
+
+def read_samples(text: bytes, order: int = 0) -> List[str]:
+    """The reference's read_samples (formats.cpp:42-69); RefError(code 4 =
+    ParseError) with its message on failure."""
+    buf = C.create_string_buffer(max(len(text), 1))
+    n, nq = C.c_uint64(0), C.c_int(0)
+    rc = lib().ref_read_samples(text, len(text), order, buf, len(buf), C.byref(n), C.byref(nq))
+    if rc:
+        raise RefError(rc, lib().ref_last_error().decode())
+    raw = buf.raw[: n.value * nq.value].decode()
+    return [raw[i * nq.value:(i + 1) * nq.value] for i in range(n.value)]
+
+
+def format_amplitude_row(bits: str, amp: complex, order: int = 0) -> str:
+    out = C.create_string_buffer(len(bits) + 128)
+    lib().ref_format_amplitude_row(bits.encode(), amp.real, amp.imag, order, out, len(out))
+    return out.value.decode()
 
 
 class RefProblem:

@@ -18,6 +18,7 @@ MTCG_ERR_MEMORY_CAP = 3
 MTCG_ERR_CUDA = 5
 MTCG_ERR_ARGUMENT = 6
 MTCG_ERR_NCCL = 7
+MTCG_ERR_PARSE = 8
 
 MTCG_C64 = 0
 MTCG_C128 = 1

@@ -80,6 +80,11 @@ def lib():
             L.mtcg_plan_op_info.argtypes = [vp, C.c_int32, C.POINTER(A.mtcg_op_info)]
             L.mtcg_time_ops.argtypes = [vp, C.c_uint64, vp, C.c_int, vp, C.POINTER(C.c_float), cp, sz]
             L.mtcg_tuple_index_check.argtypes = [vp, pp, i32p, u64p, dp, dp, cp, sz]
+            L.mtcg_read_samples.argtypes = [vp, C.c_uint64, C.c_int32, vp, C.c_uint64, u64p, i32p, cp, sz]
+            L.mtcg_assign.argtypes = [vp, C.c_uint64, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp,
+                                      C.c_uint64, cp, sz]
+            L.mtcg_write_amplitudes.argtypes = [cp, vp, C.c_uint64, C.c_int32, C.c_int32, vp, C.c_int32,
+                                                u64p, cp, sz]
             _lib = L
         return _lib
 
@@ -92,4 +97,5 @@ EXPORTS = (
     "mtcg_emulate", "mtcg_launch_count", "mtcg_plan_op_count", "mtcg_plan_op_info",
     "mtcg_time_ops", "mtcg_create_multi", "mtcg_device_count", "mtcg_visible_devices",
     "mtcg_run_slices_out", "mtcg_fold", "mtcg_tuple_index_check",
+    "mtcg_read_samples", "mtcg_assign", "mtcg_write_amplitudes",
 )

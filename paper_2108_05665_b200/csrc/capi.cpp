@@ -20,6 +20,7 @@
 #include "device.hpp"
 #include "configs.hpp"
 #include "planner.hpp"
+#include "ingest.hpp"
 
 using namespace mtcg;
 
@@ -74,6 +75,9 @@ mtcg_status guarded(char* err, size_t errlen, int32_t* cap_node, F&& f) {
   } catch (const DataError& e) {
     set_err(err, errlen, e.what());
     return MTCG_ERR_DATA;
+  } catch (const ParseError& e) {
+    set_err(err, errlen, e.what());
+    return MTCG_ERR_PARSE;
   } catch (const CudaError& e) {
     set_err(err, errlen, e.what());
     return MTCG_ERR_CUDA;
@@ -533,6 +537,51 @@ void mtcg_destroy(mtcg_handle* h) {
     if (c) nccl().destroy(c);
   for (Engine* e : h->engines) engine_destroy(e);
   delete h;
+}
+
+mtcg_status mtcg_read_samples(const char* text, uint64_t len, int32_t bit_order, char* out,
+                              uint64_t out_capacity, uint64_t* n_rows, int32_t* n_qubits, char* err,
+                              size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if ((!text && len) || !n_rows || !n_qubits) throw DataError("null argument");
+    SampleMatrix m = read_samples(text, len, bit_order);
+    if (m.chars.size() > out_capacity || (!out && !m.chars.empty())) throw DataError("sample output capacity");
+    if (!m.chars.empty()) std::memcpy(out, m.chars.data(), m.chars.size());
+    *n_rows = m.n_rows;
+    *n_qubits = m.n_qubits;
+  });
+}
+
+mtcg_status mtcg_assign(const char* samples, uint64_t n_rows, int32_t n_qubits, int32_t n_slots,
+                        const int32_t* slot_qubit_begin, const int32_t* slot_qubits, uint32_t* tuples,
+                        int32_t* slot_n_values, uint64_t* value_key_begin, uint32_t* value_keys,
+                        uint64_t keys_capacity, char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if ((!samples && n_rows) || n_slots < 0 || n_qubits < 0 || !slot_qubit_begin ||
+        (!slot_qubits && slot_qubit_begin[n_slots] > 0) || (!tuples && n_rows && n_slots) || !slot_n_values ||
+        !value_key_begin)
+      throw DataError("null argument");
+    Assignment a = assign(samples, n_rows, n_qubits, n_slots, slot_qubit_begin, slot_qubits, tuples);
+    if (a.value_keys.size() > keys_capacity || !value_keys) throw DataError("value key capacity");
+    std::memcpy(slot_n_values, a.slot_n_values.data(), a.slot_n_values.size() * 4);
+    std::memcpy(value_key_begin, a.value_key_begin.data(), a.value_key_begin.size() * 8);
+    std::memcpy(value_keys, a.value_keys.data(), a.value_keys.size() * 4);
+  });
+}
+
+mtcg_status mtcg_write_amplitudes(const char* path, const char* samples, uint64_t n_rows, int32_t n_qubits,
+                                  int32_t bit_order, const double* values, int32_t w, uint64_t* written,
+                                  char* err, size_t errlen) {
+  return guarded(err, errlen, nullptr, [&] {
+    if (!path || (!samples && n_rows) || (!values && n_rows) || w < 0 || w > 30) throw DataError("bad argument");
+    const std::string text = format_amplitudes(samples, n_rows, n_qubits, bit_order, values, w);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw DataError(std::string("cannot open output file: ") + path);
+    const size_t put = text.empty() ? 0 : std::fwrite(text.data(), 1, text.size(), f);
+    const bool ok = std::fclose(f) == 0 && put == text.size();
+    if (!ok) throw DataError(std::string("cannot write output file: ") + path);
+    if (written) *written = text.size();
+  });
 }
 
 mtcg_status mtcg_tuple_index_check(mtcg_handle* h, const mtcg_problem* p, int32_t* equal, uint64_t* rows,

@@ -725,25 +725,27 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
       so += d.st_o[i];
     }
   }
-  auto hi = [&](const uint32_t* tab, int bits, int u) {
+  // the per-u parts of the maps (bits 8-10, the same for every thread) live
+  // in shared memory: [ld_o | ld_p | st_o | st_p][u] (registers for them
+  // capped the kernel at 3 blocks per SM)
+  uint32_t* hmap = tb + d.tbl_words;
+  if (threadIdx.x < 4 * kU) {
+    const int t = threadIdx.x / kU, u = threadIdx.x % kU;
+    const uint32_t* tab = t == 0 ? d.ld_o : t == 1 ? d.ld_p : t == 2 ? d.st_o : d.st_p;
+    const int bits = t < 2 ? d.ld_bits : d.st_bits;
     uint32_t x = 0;
-#pragma unroll
     for (int i = 0; i < 3; ++i)
       if (8 + i < bits && (u >> i & 1)) x += tab[8 + i];
-    return x;
-  };
-  // the per-u parts of the maps are the same for every chunk: once
-  uint32_t hlo[kU], hlp[kU], hso[kU], hsp[kU];
-#pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    hlo[u] = lo + hi(d.ld_o, d.ld_bits, u);
-    hlp[u] = lp + hi(d.ld_p, d.ld_bits, u);
-    hso[u] = so + hi(d.st_o, d.st_bits, u);
-    hsp[u] = sp + hi(d.st_p, d.st_bits, u);
+    hmap[threadIdx.x] = x;
   }
+  __syncthreads();
+  const uint32_t* hlo = hmap;
+  const uint32_t* hlp = hmap + kU;
+  const uint32_t* hso = hmap + 2 * kU;
+  const uint32_t* hsp = hmap + 3 * kU;
   T v[kU];
   auto fetch = [&](uint64_t outer) {
-    const T* A = Aitem + d.tu_in(outer);
+    const T* A = Aitem + d.tu_in(outer) + lo;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
       if (threadIdx.x + 256 * u < d.n_ld) v[u] = A[hlo[u]];
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
     __syncthreads();  // the previous chunk's results are stored
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_ld) X0[hlp[u]] = v[u];
+      if (threadIdx.x + 256 * u < d.n_ld) X0[lp + hlp[u]] = v[u];
     if (k + 1 < n_chunks) fetch(outer0 + k + 1);  // in flight during the steps
     T* X = X0;
     T* Y = Y0;
@@ -767,10 +769,10 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
       Y = t;
     }
     __syncthreads();
-    T* O = Oitem + d.tu_out(outer0 + k);
+    T* O = Oitem + d.tu_out(outer0 + k) + so;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_st) O[hso[u]] = X[hsp[u]];
+      if (threadIdx.x + 256 * u < d.n_st) O[hso[u]] = X[sp + hsp[u]];
   }
 }
 
@@ -1334,7 +1336,7 @@ void launch_chain(DevicePlan& dp, const Chain& ch, cudaStream_t st) {
   }
   d.tbl_words = static_cast<int>(ch.steps.back().tbl_off + ch.steps.back().tbl.size() - ch.steps[0].tbl_off);
   const size_t smem = (2 * ((size_t{1} << d.q) + 1 << d.inner_bits) + 64 * ch.steps.size()) * sizeof(T) +
-                      4 * static_cast<size_t>(d.tbl_words);
+                      4 * static_cast<size_t>(d.tbl_words) + 4 * 32;  // + the per-u map parts
   static size_t smem_set[kMaxDevices] = {};  // function attributes are per device
   const int dev = current_device();
   if (smem > 48 * 1024 && smem > smem_set[dev]) {

@@ -18,6 +18,11 @@ namespace mtcg {
 struct DataError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// ParseError (errors.hpp:26-36): "line N: what" when the line is known
+struct ParseError : std::runtime_error {
+  ParseError(const std::string& what, uint64_t line)
+      : std::runtime_error(line ? "line " + std::to_string(line) + ": " + what : what) {}
+};
 struct MemoryCapError : std::runtime_error {
   MemoryCapError(const std::string& w, int node) : std::runtime_error(w), node(node) {}
   int node;

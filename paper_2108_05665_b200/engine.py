@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _abi as A
 from ._lib import lib
-from .errors import DataError, EngineError, MemoryCapError
+from .errors import DataError, EngineError, MemoryCapError, ParseError
 
 PRECISIONS = {"c64": A.MTCG_C64, "c128": A.MTCG_C128}
 
@@ -105,6 +105,8 @@ def _raise(status: int, err: C.Array, cap_node: int = -1):
         raise DataError(msg)
     if status == A.MTCG_ERR_MEMORY_CAP:
         raise MemoryCapError(msg, cap_node)
+    if status == A.MTCG_ERR_PARSE:
+        raise ParseError(msg)
     raise EngineError(f"mtcg status {status}: {msg}")
 
 

@@ -437,6 +437,32 @@ def build_assignments(d: NetworkDiagram, bitstrings: Sequence[str],
     return AssignmentSet(value_sets, tuples, list(bitstrings), batch)
 
 
+def assignments_from_keys(d: NetworkDiagram, samples: Sequence[str], tuples: np.ndarray,
+                          value_keys: Sequence[np.ndarray]) -> AssignmentSet:
+    """AssignmentSet from the native ranking (paper_2108_05665_b200.ingest
+    .assign / mtcg_assign): slot j's value v is its tensor projected on the
+    fixed (non-batch) open legs at the bits of value_keys[j][v], first fixed
+    leg = most significant bit (diagram.cpp:286-292)."""
+    batch = batch_legs_of(d, samples)
+    is_batch = [False] * d.n_qubits
+    for l in batch:
+        is_batch[d.qubit_of(l)] = True
+    value_sets: List[List[Tensor]] = []
+    for j in range(d.slot_count):
+        fixed = [l for l in d.slot_open_legs[j] if not is_batch[d.qubit_of(l)]]
+        if not fixed or not len(samples):
+            value_sets.append([d.slot_tensors[j]])
+            continue
+        vs = []
+        for key in value_keys[j]:
+            t = d.slot_tensors[j]
+            for f, leg in enumerate(fixed):
+                t = project_leg(t, leg, (int(key) >> (len(fixed) - 1 - f)) & 1)
+            vs.append(t)
+        value_sets.append(vs)
+    return AssignmentSet(value_sets, np.ascontiguousarray(tuples, dtype=np.uint32), list(samples), sorted(batch))
+
+
 def batch_legs_of(d: NetworkDiagram, samples: Sequence[str]) -> List[int]:
     """'*' columns of the samples (tools/main.cpp:99-111)."""
     if not samples:
