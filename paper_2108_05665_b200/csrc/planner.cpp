@@ -947,6 +947,17 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       for (uint32_t x : space) s.push_back(contains(lay, x) ? stride_in(lay, x) : 0);
       return s;
     };
+    // long-K small tiles (cfg3 node 619: 16 x 16 x 16384 per item) stream
+    // both operands once instead of through 16 x 16 smem k-steps (decided
+    // before the tables: per-element kernels index them by output position)
+    if (c.precision == MTCG_C64 && op.config != kTcConfig && op.grp_max == 0 && op.fa >= 2 && op.fa <= 4 &&
+        op.fb >= 3 && op.fb <= 4 && op.kc >= 9 && !op.a_leaf && !op.b_leaf && !std::getenv("MTCG_NO_LONGK")) {
+      bool kc_a = true, kc_b = true;
+      const auto ka = strides_of(k_legs, a_layout), kb = strides_of(k_legs, b_layout);
+      for (size_t b = 0; b < ka.size(); ++b) kc_a &= ka[b] == (uint64_t{1} << b);
+      for (size_t b = 0; b < kb.size(); ++b) kc_b &= kb[b] == (uint64_t{1} << b);
+      if (kc_a && kc_b) op.config = kLongKConfig;
+    }
     if (op.config == kGenericConfig || op.config == kDotConfig) {
       // per-output-element kernels: index the stored output directly
       std::vector<uint32_t> o_legs(out_layout.rbegin(), out_layout.rend());
@@ -976,11 +987,6 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
       const auto ms = strides_of(m_legs, out_layout);
       op.o_mcontig = !ms.empty() && ms[0] == 1;
     }
-    // long-K small tiles (cfg3 node 619: 16 x 16 x 16384 per item) stream
-    // both operands once instead of through 16 x 16 smem k-steps
-    if (c.precision == MTCG_C64 && op.config != kTcConfig && op.grp_max == 0 && op.fa >= 2 && op.fa <= 4 &&
-        op.fb >= 3 && op.fb <= 4 && op.kc >= 9 && op.a_kcontig && op.b_kcontig && !std::getenv("MTCG_NO_LONGK"))
-      op.config = kLongKConfig;
 
     sec.lap(2);
     // sliced legs carried by leaf operands: offsets per set bit of the slice
