@@ -298,11 +298,7 @@ def roofline_for(cp, acc, stream, step_ms, hbm_gbs, tensor_tflops, peak_src):
     if rc:
         raise RuntimeError(err.value.decode())
 
-    class OpInfo(C.Structure):
-        _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
-                    ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
-                    ("mults", C.c_uint64), ("bytes", C.c_uint64),
-                    ("compulsory_bytes", C.c_uint64)]
+    from paper_2108_05665_b200._abi import mtcg_op_info as OpInfo  # the one ABI struct
 
     L.mtcg_plan_op_info.argtypes = [C.c_void_p, C.c_int32, C.POINTER(OpInfo)]
     ops = []

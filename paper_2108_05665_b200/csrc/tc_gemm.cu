@@ -350,6 +350,7 @@ struct TcParams {
   const int8_t* sa;
   const int8_t* sb;
   int tom_cache;  // > 0: words of the tom table (lo, then hi) staged in shared memory
+  int blocked;    // split-integer kernel: contiguous tile range per CTA (see t_first)
 };
 
 // Role timestamps of CTA 0's first kTraceTiles tiles (MTCG_TC_TRACE=<node>).
@@ -1216,6 +1217,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint32_t tiles_n = (p.Nr + p.bn - 1) / p.bn;
   const uint32_t tiles_m = p.ga_per ? p.nb_ga_tiles : (p.M + kTM - 1) / kTM;
   const uint64_t tiles = uint64_t{tiles_n} * tiles_m * p.nb;
+  // tile order: strided (CTA c takes c, c + ncta, ...) or blocked (a
+  // contiguous range per CTA: consecutive tiles of one unit, so the
+  // epilogue's column table and the B̂ tile change once per unit instead of
+  // every tile — skinny many-unit ops)
+  const uint64_t t_first = p.blocked ? tiles * cta0 / ncta : cta0;
+  const uint64_t t_last = p.blocked ? tiles * (cta0 + 1) / ncta : tiles;
+  const uint64_t t_stride = p.blocked ? 1 : ncta;
   const int k_stages = QA ? p.Kr / kI8Kb : 1;
   const uint32_t buf_cols = 3 * p.bn;
   const uint32_t n_acc = min(static_cast<uint32_t>(kMaxAcc), 512u / buf_cols);
@@ -1317,11 +1325,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
       uint32_t cached_item = ~0u, a_entry = 0;
       uint64_t pit = 0;
       TileWalk w;
-      w.init(cta0, tiles_n, tiles_m);
-      const Steps ws = make_steps(ncta);
+      w.init(t_first, tiles_n, tiles_m);
+      const Steps ws = make_steps(t_stride);
       const uint32_t a_box_bytes = QA ? kPlaneA : kBM * 128u;
       const int raw_halves = p.Kr > 32 ? 2 : 1;
-      for (uint64_t t = cta0; t < tiles; t += ncta, ++pit, w.advance(ws)) {
+      for (uint64_t t = t_first; t < t_last; t += t_stride, ++pit, w.advance(ws)) {
         const uint32_t item = w.u;
         const int m0 = static_cast<int>(w.m) * kTM + m_off;
         const int n0 = static_cast<int>(w.n) * p.bn + static_cast<int>(rank) * bn_cta;
@@ -1385,7 +1393,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
                            ((kTM >> 4) << 24);
     Ring rg, ra;
     uint64_t it = 0;
-    for (uint64_t t = cta0; t < tiles && (!PAIR || rank == 0); t += ncta, ++it, ra.next(static_cast<int>(n_acc))) {
+    for (uint64_t t = t_first; t < t_last && (!PAIR || rank == 0); t += t_stride, ++it,
+                  ra.next(static_cast<int>(n_acc))) {
       const uint32_t tb = static_cast<uint32_t>(ra.slot);
       uint32_t dacc, d1, d2;
       if (split) {
@@ -1429,7 +1438,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // landed stage is signalled on the leader's conv barrier)
     Ring rg;
     const uint32_t conv_leader = mapa(conv, 0);
-    for (uint64_t t = cta0; t < tiles; t += ncta)
+    for (uint64_t t = t_first; t < t_last; t += t_stride)
       for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
         mbar_wait(&full[rg.slot], rg.round & 1);
         if (lane == 0) mbar_arrive_cluster(conv_leader + 8u * static_cast<uint32_t>(rg.slot));
@@ -1444,7 +1453,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint64_t cit = 0;
     const uint32_t conv_leader = PAIR ? mapa(conv, 0) : 0u;
     const bool two = p.Kr > 32;
-    for (uint64_t t = cta0; t < tiles; t += ncta, ++cit, rg.next(n_stages)) {
+    for (uint64_t t = t_first; t < t_last; t += t_stride, ++cit, rg.next(n_stages)) {
       const int st = rg.slot;
       mbar_wait(&full[st], rg.round & 1);
       if (r == 0) trace(p, cit, 4);
@@ -1517,8 +1526,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const uint64_t entry = p.out_rows ? uint64_t{p.out_rows[item]} : uint64_t{item};
       return static_cast<int64_t>(entry * p.out_item + (ton_cached ? ton_s[n] : p.ton(n)));
     };
-    const uint64_t t_step = split ? uint64_t{ncta} : n_epi * uint64_t{ncta};
-    uint64_t t = cta0 + (split ? 0 : uint64_t{static_cast<uint32_t>(eg)} * ncta);
+    const uint64_t t_step = split ? t_stride : n_epi * t_stride;
+    uint64_t t = t_first + (split ? 0 : uint64_t{static_cast<uint32_t>(eg)} * t_stride);
     uint64_t it = split ? 0 : eg;
     const uint64_t it_step = split ? 1 : n_epi;
     uint32_t nxt_bunit = 0;
@@ -1576,7 +1585,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         nxt_cs = r < p.bn / 2 ? pow2f_wide(-__ldg(p.sb + uint64_t{nxt_bunit} * (p.Nr / 2) + nxt_n0 / 2 + r)) : 0.f;
       }
     };
-    if (t < tiles) fetch();
+    if (t < t_last) fetch();
     const uint32_t acc_empty_leader = PAIR ? mapa(acc_empty, 0) : 0u;
     // ring positions of this group's current tile: accumulator buffer and
     // row-exponent slot (no 64-bit divisions per tile)
@@ -1675,13 +1684,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
     };
     const uint32_t res_free_leader = PAIR ? mapa(res_free, 0) : 0u;
-    for (; t < tiles; t += t_step, it += it_step) {
+    for (; t < t_last; t += t_step, it += it_step) {
       om = nxt_direct || nxt_om == ~uint64_t{0} ? nxt_om : uint64_t{nxt_om_lo + nxt_om_hi};
       key = nxt_key;
       my_coff = nxt_coff;
       my_cs = nxt_cs;
       int sa = nxt_sa;
-      if (t + t_step < tiles) fetch();
+      if (t + t_step < t_last) fetch();
       if (key != table_key) {  // uniform across the group
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));
         if (r < kMaxBn / 2) {
@@ -2274,6 +2283,10 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   p.sa = op.row_exp;
   p.sb = op.col_exp;
   p.tom_cache = tom_cache;
+  // blocked tile order for single-n-tile ops with many units (the strided
+  // order changes unit on almost every tile there); MTCG_TC_BLOCKED=0|1
+  static const char* blk_env = std::getenv("MTCG_TC_BLOCKED");
+  p.blocked = blk_env ? std::atoi(blk_env) : (!ga && Nr <= static_cast<uint64_t>(bn) && units >= 2);
   p.dbg = nullptr;
   const int slot = 4 + (pair ? 2 : 0) + (qa ? 1 : 0);
   auto kern = pair ? (qa ? tc_i8_persistent<true, true> : tc_i8_persistent<true, false>)
@@ -2405,6 +2418,7 @@ int tc_contract(const TcOp& op, cudaStream_t st) {
   const CUtensorMap mbhi = make_map(op.bhat_hi, Kr, uint64_t{units} * Nr, bn_cta, bk, f16);
   const CUtensorMap mblo = make_map(op.bhat_lo, Kr, uint64_t{units} * Nr, bn_cta, bk, f16);
   TcParams p;
+  p.blocked = 0;
   p.M = static_cast<int>(M);
   p.Nr = static_cast<int>(Nr);
   p.Kr = static_cast<int>(Kr);

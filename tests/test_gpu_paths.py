@@ -164,11 +164,7 @@ def _op_kernels(cp):
 
     from paper_2108_05665_b200._lib import lib
 
-    class OpInfo(C.Structure):
-        _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
-                    ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
-                    ("mults", C.c_uint64), ("bytes", C.c_uint64),
-                    ("compulsory_bytes", C.c_uint64)]
+    from paper_2108_05665_b200._abi import mtcg_op_info as OpInfo  # the one ABI struct
 
     L = lib()
     L.mtcg_plan_op_count.restype = C.c_int32

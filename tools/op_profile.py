@@ -18,11 +18,7 @@ sys.path.insert(0, ROOT)
 from bench import load_workload  # noqa: E402
 
 
-class OpInfo(C.Structure):
-    _fields_ = [("node", C.c_int32), ("kernel", C.c_int32), ("fa", C.c_int32),
-                ("fb", C.c_int32), ("kc", C.c_int32), ("batch", C.c_uint32),
-                ("mults", C.c_uint64), ("bytes", C.c_uint64),
-                    ("compulsory_bytes", C.c_uint64)]
+from paper_2108_05665_b200._abi import mtcg_op_info as OpInfo  # the one ABI struct
 
 
 def main():
