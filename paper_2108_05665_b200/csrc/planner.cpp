@@ -893,6 +893,16 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         s = *end ? end + 1 : end;
       }
     }
+    // MTCG_TC_SKIP=<node>[,<node>...] keeps those nodes off the tensor path
+    if (const char* tc_skip = std::getenv("MTCG_TC_SKIP")) {
+      for (const char* s = tc_skip; *s;) {
+        char* end = nullptr;
+        const long v = std::strtol(s, &end, 10);
+        if (end == s) break;
+        if (v == node) tc_listed = false;
+        s = *end ? end + 1 : end;
+      }
+    }
     // Gather mode: M = 32 / 64 rows per item is too short for a 128-row
     // tensor tile, but when many items share few B entries (cfg2 node 349:
     // 9,992 items of 32 x 32 x 128 over 128 B entries) the items of one B
