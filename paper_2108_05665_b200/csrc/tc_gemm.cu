@@ -1176,6 +1176,52 @@ __device__ __forceinline__ float pow2f_wide(int s) { return __int_as_float((max(
 // A rows and half of the B̂ tile. Epilogue: two warpgroups; with a single
 // accumulator buffer (bn = 128: 3 x 128 TMEM columns) both drain every tile
 // (alternate 32-column chunks), otherwise they take alternate tiles.
+// Whole-K stage conversion of row r (converter warps, mode C): 64 raw floats
+// (two SWIZZLE_128B halves; TWO = false: K = 16 complex, the second half is
+// zero and skipped) -> row max -> exponent -> 3 x 64 digit bytes in
+// SWIZZLE_64B rows at plane p * 8 KB, in place (after every converter's raw
+// reads: named barrier 3). Returns the row exponent.
+template <bool TWO>
+__device__ __forceinline__ int convert_row_i8(uint8_t* sp, int r, int n_conv) {
+  constexpr int NC = TWO ? 16 : 8;  // float4s per row
+  constexpr int kPlaneA = kBM * kI8Kb;
+  float4 v[NC];
+  float m[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int h = c >> 3, cc = c & 7;
+    v[c] = reinterpret_cast<const float4*>(sp + h * kBM * 128 + r * 128)[cc ^ (r & 7)];
+    m[c] = fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w)));
+  }
+#pragma unroll
+  for (int w = NC / 2; w > 0; w >>= 1)  // tree: log2(NC) dependent steps
+#pragma unroll
+    for (int c = 0; c < w; ++c) m[c] = fmaxf(m[c], m[c + w]);
+  const int sa = i8_scale_exp(m[0]);
+  const float sc = pow2f_wide(sa);
+  asm volatile("bar.sync 3, %0;" ::"r"(32 * n_conv) : "memory");  // every raw read done (in place)
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {  // 16-byte chunk j of each plane row = elements 16j .. 16j + 15
+    uint32_t w[3][4];
+    if (TWO || j < 2) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 x = v[(4 * j + q) % NC];
+        i8_pack4(i8_biased(x.x, sc), i8_biased(x.y, sc), i8_biased(x.z, sc), i8_biased(x.w, sc), w[0][q], w[1][q],
+                 w[2][q]);
+      }
+    } else {  // zero padding: every digit 0
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[0][q] = w[1][q] = w[2][q] = 0u;
+    }
+    const int off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+#pragma unroll
+    for (int pl = 0; pl < 3; ++pl)
+      *reinterpret_cast<uint4*>(sp + pl * kPlaneA + off) = make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
+  }
+  return sa;
+}
+
 template <bool PAIR, bool QA>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_i8_persistent(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -1458,37 +1504,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       mbar_wait(&full[st], rg.round & 1);
       if (r == 0) trace(p, cit, 4);
       uint8_t* sp = base + st * stage_bytes;
-      float4 v[16];
-      float m[16];
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const int h = c >> 3, cc = c & 7;
-        v[c] = h && !two ? make_float4(0.f, 0.f, 0.f, 0.f)
-                         : reinterpret_cast<const float4*>(sp + h * kBM * 128 + r * 128)[cc ^ (r & 7)];
-        m[c] = fmaxf(fmaxf(fabsf(v[c].x), fabsf(v[c].y)), fmaxf(fabsf(v[c].z), fabsf(v[c].w)));
-      }
-#pragma unroll
-      for (int w = 8; w > 0; w >>= 1)  // tree: 4 dependent steps, not 16
-#pragma unroll
-        for (int c = 0; c < w; ++c) m[c] = fmaxf(m[c], m[c + w]);
-      const float mx = m[0];
-      const int sa = i8_scale_exp(mx);
-      const float sc = pow2f_wide(sa);
-      asm volatile("bar.sync 3, %0;" ::"r"(32 * p.n_conv) : "memory");  // every raw read done (in place)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {  // 16-byte chunk j of each plane row = elements 16j .. 16j + 15
-        uint32_t w[3][4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float4 x = v[4 * j + q];
-          i8_pack4(i8_biased(x.x, sc), i8_biased(x.y, sc), i8_biased(x.z, sc), i8_biased(x.w, sc), w[0][q],
-                   w[1][q], w[2][q]);
-        }
-        const int off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
-#pragma unroll
-        for (int pl = 0; pl < 3; ++pl)
-          *reinterpret_cast<uint4*>(sp + pl * kPlaneA + off) = make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
-      }
+      const int sa = two ? convert_row_i8<true>(sp, r, p.n_conv) : convert_row_i8<false>(sp, r, p.n_conv);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       // row exponent for this tile's epilogue (ring slot released by the
       // pipeline depth: converters run at most n_stages + n_acc tiles ahead)

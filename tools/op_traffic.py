@@ -17,8 +17,8 @@ import csv
 import json
 import sys
 
-PREFIX = ("absmax_kernel", "build_bhat")
-MAIN = ("tc_gemm_persistent", "contract_", "chain_kernel")
+PREFIX = ("absmax_kernel", "build_bhat", "quantize_rows")
+MAIN = ("tc_gemm_persistent", "tc_i8_persistent", "contract_", "chain_kernel")
 
 
 def load_launches(path):
