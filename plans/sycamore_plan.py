@@ -128,6 +128,7 @@ def main():
     ap.add_argument("--alpha", type=float, default=10.0,
                     help="complex MACs per element of traffic (B200 c64: ~500 TF/s / 6.5 TB/s / 8 flop)")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--out-all", default=None, help="directory: every run's plan as run<seed>.plan")
     a = ap.parse_args()
     sys.path.insert(0, os.path.join(ROOT, "plans"))
     _, d, legs, qs = network(a.cycles, a.seed)
@@ -144,6 +145,11 @@ def main():
     for cost, big, order, merges, sliced, seed in results:
         print(f"run {seed}: cost {cost:.3e} MACs, largest table {big:.3e}, max order {order}, "
               f"{sliced.bit_count()} sliced legs", file=sys.stderr)
+    if a.out_all:
+        os.makedirs(a.out_all, exist_ok=True)
+        for _, _, _, merges_r, sliced_r, seed_r in results:
+            with open(os.path.join(a.out_all, f"run{seed_r}.plan"), "w") as f:
+                f.write(plan_text(len(legs), merges_r, sliced_r))
     cost, big, order, merges, sliced, seed = results[0]
     print(f"best: {cost:.3e} ({time.time() - t0:.0f}s)", file=sys.stderr)
     text = plan_text(len(legs), merges, sliced)

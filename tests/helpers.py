@@ -69,3 +69,32 @@ def rel_err(got: np.ndarray, want: np.ndarray, n_qubits: int) -> float:
     """max |a_gpu - a_ref| / max(|a_ref|, 2^(-n/2))."""
     floor = 2.0 ** (-n_qubits / 2)
     return float(np.max(np.abs(got - want) / np.maximum(np.abs(want), floor))) if want.size else 0.0
+
+
+def statevector_samples(name: str, k: int, seed: int):
+    """cfg1-style workload with k bitstrings sampled from the circuit's exact
+    output distribution (the pattern of the reference's XEB
+    criterion, tests/acceptance_main.cpp:400-428: cumulative |amp|^2 over the
+    bitstrings in index order, qubit 0 = most significant bit
+    (support/oracle.cpp:162-167), u = uniform_real01 * total, lower_bound).
+    The distribution is the C oracle's evaluation of all 2^n bitstrings.
+    Returns (problem, circuit, bits, probs_of_bits, target F)."""
+    from oracle import oracle as O
+
+    cfgs = {"cfg1": (3, 4, 8)}
+    r, cc, layers = cfgs[name]
+    n = r * cc
+    c = N.grid_circuit(r, cc, layers, 12345)
+    d = N.to_diagram(c, True)
+    plan = N.parse_plan(open(os.path.join(ROOT, "plans", f"{name}.plan")).read())
+    every = [format(i, f"0{n}b") for i in range(1 << n)]
+    amps, _, _, _ = O.eval_problem(problem_arrays(plan, d, N.build_assignments(d, every, [])))
+    dist = (np.abs(amps.reshape(-1)) ** 2).astype(np.float64)
+    cum = np.cumsum(dist)
+    rng = N.Rng(seed)
+    idx = [min(int(np.searchsorted(cum, rng.uniform_real01() * cum[-1], side="left")), len(dist) - 1)
+           for _ in range(k)]
+    bits = [every[i] for i in idx]
+    target = float((1 << n) * np.sum(dist * dist) - 1.0)
+    p = problem_arrays(plan, d, N.build_assignments(d, bits, []))
+    return p, c, bits, dist[idx], target

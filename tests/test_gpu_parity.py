@@ -205,3 +205,29 @@ def test_cfg2_full_size_against_reference_golden(engine, tensor_cores):
           f"{np.linalg.norm(r.amplitudes - want) / np.linalg.norm(want):.2e}, scale bias {scale:.2e}, "
           f"F {f_dev:.6f} vs {f_ref:.6f} (dF {f_dev - f_ref:.2e})")
     assert abs(f_dev - f_ref) <= TOL * (abs(f_ref) + 1 / math.sqrt(len(bits)))
+
+
+def test_cfg1_statevector_sampled_xeb(engine):
+    """cfg1 with 1,000 bitstrings sampled from the exact output distribution
+    (SURVEY §8(d)): c128 amplitudes bit-identical to the oracle, and the fused
+    device XEB within 5 sigma of the target 2^n sum p^2 - 1 while uniform
+    bitstrings (the cfg1 workload) sit within 5 sigma of 0 — the reference's
+    XEB criterion (tests/acceptance_main.cpp:400-428) on cfg1."""
+    from .helpers import statevector_samples
+
+    p, c, bits, probs, target = statevector_samples("cfg1", 1000, 411)
+    want, _, _, _ = O.eval_problem(p)
+    cp = engine.compile(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128"))
+    acc = cp.new_accumulator()
+    cp.run(0, cp.n_slices, acc.data_ptr())
+    got = cp.fetch(acc.data_ptr())
+    assert bits_equal(got.amplitudes, want)
+    assert np.allclose((np.abs(want.reshape(-1)) ** 2), probs, rtol=1e-12, atol=0)
+    sigma = 1.0 / math.sqrt(len(bits))
+    f = cp.xeb(acc.data_ptr(), c.n_qubits)
+    assert abs(f - target) < 5 * sigma and target > 10 * sigma
+    pu, cu, _ = workload("cfg1")
+    cpu = engine.compile(pu, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128"))
+    accu = cpu.new_accumulator()
+    cpu.run(0, cpu.n_slices, accu.data_ptr())
+    assert abs(cpu.xeb(accu.data_ptr(), cu.n_qubits)) < 5 * sigma
