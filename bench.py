@@ -61,7 +61,8 @@ def load_workload(name: str, k: int = 0):
         bits = N.random_bitstrings(N.Rng(99), c.n_qubits, w["k"])[: k or w["k"]]
         d = N.to_diagram(c, True)
         asg = N.build_assignments(d, bits, [])
-        plan_text = open(os.path.join(ROOT, "plans", f"{name}.plan")).read()
+        # MTCG_PLAN_FILE: a candidate plan instead of the committed one (plan search A/B)
+        plan_text = open(os.environ.get("MTCG_PLAN_FILE") or os.path.join(ROOT, "plans", f"{name}.plan")).read()
         return problem_arrays(N.parse_plan(plan_text), d, asg), c, bits, plan_text
     c = N.grid_circuit(w["rows"], w["cols"], w["layers"], 12345)
     bits = N.random_bitstrings(N.Rng(99), w["rows"] * w["cols"], w["k"])

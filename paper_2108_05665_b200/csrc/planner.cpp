@@ -738,9 +738,12 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     bool ga_mode = false;
     if (c.precision == MTCG_C64 && !(opt.flags & MTCG_FLAG_NO_TENSOR_CORES) && !std::getenv("MTCG_NO_GATHER") &&
         closed.size() >= 4 && ti.distinct[node] >= 1024 && !std::getenv("MTCG_TC_ONLY")) {
+      // ... or a long K (>= 512): even one item per 128-row tile (half or a
+      // quarter of the rows padding) beats the CUDA-core tile kernels there
+      // (cfg3 candidate plans: 2,500 items of 64 x 64 x 4096)
       auto fits = [&](int ca, const std::vector<uint32_t>& fa_, int cb, const std::vector<uint32_t>& fb_) {
         return p.node_slot[ca] < 0 && (fa_.size() == 5 || fa_.size() == 6) && fb_.size() >= 4 && fb_.size() <= 7 &&
-               uint64_t{ti.distinct[cb]} * 8 <= ti.distinct[node];
+               (uint64_t{ti.distinct[cb]} * 8 <= ti.distinct[node] || (closed.size() >= 9 && closed.size() <= 14));
       };
       if (fits(op.a_is_left ? l : r, op.a_is_left ? fl : fr, op.a_is_left ? r : l, op.a_is_left ? fr : fl)) {
         ga_mode = true;
