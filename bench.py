@@ -40,10 +40,14 @@ WORKLOADS = {
                   text="cal45: synthetic 20-qubit 4x5 grid, m=10 (grid_circuit seed 12345, fused), "
                        "1000 random bitstrings (seed 99), plans/cal45.plan (3 sliced legs); the "
                        "reference arm's calibration run"),
-    "cfg3": dict(kind="sycamore", cycles=12, circuit_seed=2024, k=10000, row_chunk=2500, rows=0, cols=53,
+    "cfg3": dict(kind="sycamore", cycles=12, circuit_seed=2024, k=10000, row_chunk=10000, rows=0, cols=53,
                  text="cfg3: synthetic 53-qubit Sycamore layout, m=12 (ABCDCDAB fSim, sycamore_circuit seed "
                       "2024, fused), 10^4 random bitstrings (seed 99), plans/cfg3.plan (20 sliced legs, 2^20 "
-                      "slices; plans/sycamore_plan.py), memo streaming in chunks of 2500 requests"),
+                      "slices; plans/sycamore_plan.py), all requests' memo tables resident (84 GB arena)"),
+    "cfg4": dict(kind="sycamore", cycles=14, circuit_seed=2024, k=100000, row_chunk=25000, rows=0, cols=53,
+                 text="cfg4: synthetic 53-qubit Sycamore layout, m=14 (ABCDCDAB fSim, sycamore_circuit seed "
+                      "2024, fused), 10^5 random bitstrings (seed 99), plans/cfg4.plan (24 sliced legs, 2^24 "
+                      "slices; plans/sycamore_plan.py), memo streaming in chunks of 25,000 requests"),
     "cfg2": dict(rows=5, cols=6, layers=12, k=10000,
                  text="cfg2: synthetic 30-qubit 5x6 grid, m=12 (grid_circuit seed 12345, "
                       "fused), 10^4 random bitstrings (seed 99), plans/cfg2.plan "
@@ -441,7 +445,8 @@ def run_sliced_subset(args):
     k = len(bits)
     eng = Engine(0)
     t0 = time.perf_counter()
-    cp = eng.compile(problem, 0, EvalOptions(precision=args.precision, row_chunk=w["row_chunk"]))
+    row_chunk = int(os.environ.get("MTCG_ROW_CHUNK") or w["row_chunk"])  # chunk-size A/B
+    cp = eng.compile(problem, 0, EvalOptions(precision=args.precision, row_chunk=row_chunk))
     compile_s = time.perf_counter() - t0
     S = cp.n_slices
     torch.cuda.set_stream(torch.cuda.Stream())
@@ -505,7 +510,7 @@ def run_sliced_subset(args):
                    "step": "one slice of the evaluation (all slices are the same schedule)",
                    "extrapolation": f"value = k / (t_slice x {S} slices); full evaluation "
                                     f"{slice_ms * S / 1e3 / 3600:.2f} h on 1 GPU",
-                   "row_chunk": w["row_chunk"], "l2": "per-slice working set > 126 MB L2"},
+                   "row_chunk": row_chunk, "l2": "per-slice working set > 126 MB L2"},
         "effective_tflops": flops_slice / (slice_ms * 1e-3) / 1e12,
         "mults_total": mults, "flops_per_slice": flops_slice,
         "roofline": {"bound": "tensor", "achieved": flops_slice / (slice_ms * 1e-3) / 1e12, "peak": tflops,

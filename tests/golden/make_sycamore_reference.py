@@ -1,22 +1,23 @@
-"""Reference anchors for the 53-qubit workload cfg3 (BASELINE.json configs[2]:
-Sycamore layout, m = 12, ABCDCDAB, 10^4 bitstrings), from the UNMODIFIED
-reference (oracle/_ref):
+"""Reference anchors for the 53-qubit workloads (BASELINE.json configs[2-3]:
+Sycamore layout, ABCDCDAB; cfg3: m = 12, 10^4 bitstrings; cfg4: m = 14, 10^5
+bitstrings), from the UNMODIFIED reference (oracle/_ref):
 
-* the exact algorithmic totals of the whole evaluation with plans/cfg3.plan
+* the exact algorithmic totals of the whole evaluation with plans/<cfg>.plan
   (CostedPlan exact mode, plan.cpp:338-371) — mults, adds, rw;
 * the per-slice amplitudes of slices 0 and 1 for the first 10 bitstrings
   (run_slice, multieval.cpp:465-476: the whole engine on one slice's
   projected leaves), the parity anchor of the device path on the 53-qubit
   network (a full evaluation is ~3.4e17 complex MACs).
 
-The circuit is workloads.network.sycamore_circuit(12, 2024) written in the
+The circuit is workloads.network.sycamore_circuit(m, 2024) written in the
 reference's circuit format (pinned against its parser, tests/test_network.py).
-Writes tests/golden/cfg3_reference.npz.
+Writes tests/golden/<cfg>_reference.npz.
 
-Usage: python tests/golden/make_cfg3_reference.py
+Usage: python tests/golden/make_sycamore_reference.py [--config cfg3|cfg4]
 """
 from __future__ import annotations
 
+import argparse
 import os
 import sys
 import time
@@ -33,10 +34,17 @@ SUBSET = 10
 SLICES = (0, 1)
 
 
+CONFIGS = {"cfg3": (12, 10000), "cfg4": (14, 100000)}  # cycles, bitstrings
+
+
 def main():
-    circ = N.format_circuit(N.sycamore_circuit(12, 2024))
-    bits = N.random_bitstrings(N.Rng(99), 53, 10000)
-    plan = open(os.path.join(ROOT, "plans", "cfg3.plan")).read()
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    a = ap.parse_args()
+    cycles, k = CONFIGS[a.config]
+    circ = N.format_circuit(N.sycamore_circuit(cycles, 2024))
+    bits = N.random_bitstrings(N.Rng(99), 53, k)
+    plan = open(os.path.join(ROOT, "plans", f"{a.config}.plan")).read()
     full = R.RefProblem(circ, bits, plan, fuse=True)
     tot = full.exact_totals()
     sub = R.RefProblem(circ, bits[:SUBSET], plan, fuse=True)
@@ -46,12 +54,12 @@ def main():
         amps.append(sub.eval_slice(s).reshape(-1))
         walls.append(time.time() - t0)
         print(f"slice {s}: {walls[-1]:.1f}s", flush=True)
-    out = os.path.join(ROOT, "tests", "golden", "cfg3_reference.npz")
+    out = os.path.join(ROOT, "tests", "golden", f"{a.config}_reference.npz")
     np.savez_compressed(out, mults=np.array([tot["mults"]], dtype=np.float64),
                         mults_str=str(tot["mults"]), adds_str=str(tot["adds"]), rw_str=str(tot["rw"]),
                         slice_amplitudes=np.stack(amps), slices=np.array(SLICES), subset=SUBSET,
                         wall_s=np.array(walls))
-    print(f"cfg3 reference: mults {tot['mults']:.4e}, slices {SLICES} x {SUBSET} bitstrings -> {out}")
+    print(f"{a.config} reference: mults {tot['mults']:.4e}, slices {SLICES} x {SUBSET} bitstrings -> {out}")
 
 
 if __name__ == "__main__":

@@ -1,7 +1,7 @@
 """cfg3's exact algorithmic totals: the engine's shape replay (mtcg_emulate)
 of the whole 10^4-bitstring evaluation equals the unmodified reference's
 CostedPlan totals recorded with the golden amplitudes
-(tests/golden/make_cfg3_reference.py; plan.cpp:497-502)."""
+(tests/golden/make_sycamore_reference.py; plan.cpp:497-502)."""
 import os
 
 import numpy as np
