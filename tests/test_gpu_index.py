@@ -82,3 +82,41 @@ def test_device_index_chunked(engine):
     got = engine.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", row_chunk=300, device_index=True))
     assert bits_equal(got.amplitudes, want)
     assert np.array_equal(got.node_contractions, want_nc)
+
+
+def test_ingestion_to_amplitude_tsv(engine, tmp_path):
+    """The paper-scale request path end to end on the device: a samples file
+    (comments, '*' column) -> mtcg_read_samples -> mtcg_assign (+ the slot
+    projections) -> mtcg_eval (device tuple index) -> mtcg_write_amplitudes;
+    amplitudes c128 bit-identical to the oracle on the same requests, TSV rows
+    in the reference's format (tools/main.cpp:145-183)."""
+    from paper_2108_05665_b200 import ingest as I
+    from paper_2108_05665_b200.engine import problem_arrays
+
+    c = N.grid_circuit(3, 4, 8, 12345)
+    d = N.to_diagram(c, True)
+    rng = N.Rng(5)
+    raw = N.random_bitstrings(rng, 12, 3000)
+    raw = [b[:7] + "*" + b[8:] for b in raw]
+    text = "# samples\n" + "\n".join(b + (" # x" if i % 97 == 0 else "") for i, b in enumerate(raw)) + "\n"
+    path = tmp_path / "samples.txt"
+    path.write_text(text)
+    m = I.read_samples_file(str(path))
+    bits = I.sample_strings(m)
+    assert bits == raw
+    a = I.assign(m, [[d.qubit_of(l) for l in d.slot_open_legs[j]] for j in range(d.slot_count)])
+    asg = N.assignments_from_keys(d, bits, a.tuples, a.value_keys)
+    plan = N.parse_plan(open(f"{ROOT}/plans/cfg1.plan").read())
+    p = problem_arrays(plan, d, asg)
+    want, _, _, _ = O.eval_problem(p)
+    got = engine.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", device_index=True))
+    assert bits_equal(got.amplitudes, want)
+    out = tmp_path / "amps.tsv"
+    I.write_amplitudes(str(out), m, got.amplitudes)
+    lines = out.read_text().splitlines()
+    assert len(lines) == 2 * len(bits)
+    b0 = bits[0]
+    for v in range(2):
+        s = b0[:7] + str(v) + b0[8:]
+        re_, im_ = got.amplitudes[0, v].real, got.amplitudes[0, v].imag
+        assert lines[v] == f"{s}\t{re_:.16e}\t{im_:.16e}"
