@@ -1491,7 +1491,9 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
         t.ton_lo = d.ton.lo;
         t.ton_hi = d.ton.hi;
         t.ton_bits = d.ton.lo_bits;
-        t.n_contig = op.o_ncontig ? 1 : 0;
+        // vector epilogue stores need adjacent column pairs only (ton(2j + 1)
+        // = ton(2j) + 1), not a contiguous n range
+        t.n_contig = (op.ton.bits >= 1 && (op.ton.lo_bits >= 1 ? op.ton.lo[1] : op.ton.hi[1]) == 1) ? 1 : 0;
         t.m_contig = op.o_mcontig ? 1 : 0;
         dp.engine->launches += tc_contract(t, st);  // [absmax +] B̂ build + GEMM
         if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
