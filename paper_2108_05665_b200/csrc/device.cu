@@ -849,7 +849,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
     contract_longk(const DevOp<float2> op_in) {
   DevOp<float2> op = op_in;
   resolve_slice(op);
@@ -917,24 +917,22 @@ __global__ void __launch_bounds__(256, 1)
     cp_async_wait<0>();
     __syncthreads();  // the ring is reused by the next item
     if (active) {
-      // butterfly over the lanes: every lane ends with the block's sums
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-#pragma unroll
-          for (int sh = 16; sh > 0; sh >>= 1) {
-            acc[i][j].x += __shfl_xor_sync(0xffffffffu, acc[i][j].x, sh);
-            acc[i][j].y += __shfl_xor_sync(0xffffffffu, acc[i][j].y, sh);
-          }
-      // lane l stores element (l >> 3, l & 7) of the block
-      const int i = lane >> 3, j = lane & 7;
-      float2 v = acc[0][0];
+      // butterfly over the lanes per element; lane l keeps element
+      // (l >> 3, l & 7) of the block (no second copy of the sums live)
+      float2 v = make_float2(0.f, 0.f);
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 8; ++y)
-          if (x == i && y == j) v = acc[x][y];
+        for (int y = 0; y < 8; ++y) {
+          float2 t = acc[x][y];
+#pragma unroll
+          for (int sh = 16; sh > 0; sh >>= 1) {
+            t.x += __shfl_xor_sync(0xffffffffu, t.x, sh);
+            t.y += __shfl_xor_sync(0xffffffffu, t.y, sh);
+          }
+          if (lane == x * 8 + y) v = t;
+        }
+      const int i = lane >> 3, j = lane & 7;
       if (m0 + i < M && n0 + j < N) {
         float2* dst = op.out + (op.out_rows ? uint64_t{__ldg(op.out_rows + item)} : item) * op.out_item +
                       op.tom(m0 + i) + op.ton(n0 + j);
