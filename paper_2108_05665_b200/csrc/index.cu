@@ -175,6 +175,8 @@ struct DevScratch {
 };
 DevScratch g_scratch[64];
 
+struct ScratchUnavailable {};
+
 struct Scratch {
   cudaStream_t st;
   DevScratch& d;
@@ -184,7 +186,11 @@ struct Scratch {
       if (d.base) IK(cudaFree(d.base));
       d.base = nullptr;
       d.cap = 0;
-      IK(cudaMalloc(&d.base, need));
+      if (cudaMalloc(&d.base, need) != cudaSuccess) {
+        cudaGetLastError();  // clear: the caller falls back to the host builder
+        d.base = nullptr;
+        throw ScratchUnavailable();
+      }
       d.cap = need;
     }
   }
@@ -353,6 +359,13 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
     ~StreamGuard() { cudaStreamDestroy(s); }
   } sguard{st};
   std::lock_guard<std::mutex> lock(g_scratch[device].mu);
+  // the device's free memory bounds the index: without room for its scratch
+  // (k x live nodes ranks, sort buffers) the host builder takes over
+  try {
+    Scratch probe(st, g_scratch[device], need);
+  } catch (const ScratchUnavailable&) {
+    return false;
+  }
   Scratch S(st, g_scratch[device], need);
   Cub cub{st};
   cub.temp_bytes = Cub::need(max_cnt, max_cnt);
