@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256, (K <= 4 && N <= 4 ? 3 : 2))
 // identical to it (and C128 stays bit-identical to the reference).
 
 template <class R, int K, int N, int RPT>
-__global__ void __launch_bounds__(256, (K <= 4 && sizeof(R) == 4 ? 3 : 2))
+__global__ void __launch_bounds__(256, (K <= 8 && sizeof(R) == 4 ? 3 : 2))
     contract_rows_grouped(const DevOp<typename V2<R>::T> op_in) {
   DevOp<typename V2<R>::T> op = op_in;
   resolve_slice(op);
@@ -1122,7 +1122,9 @@ template <class R, int K, int N>
 void launch_rows_grouped_kn(const DevOp<typename V2<R>::T>& op, cudaStream_t st) {
   using T = typename V2<R>::T;
   // rows per thread: RPT x K complex of A in registers
-  constexpr int RA = sizeof(R) == 8 ? 16 : (K <= 4 || K >= 16 ? 16 : 32);
+  // (K = 8: two rows per thread and three blocks per SM beat four rows at two
+  // blocks — cfg3 node 606 4.97 -> 4.39 ms)
+  constexpr int RA = 16;
   constexpr int RPT0 = RA / K;
   constexpr int RPT = RPT0 < 1 ? 1 : (RPT0 > 8 ? 8 : RPT0);
   const size_t smem = sizeof(T) * op.grp_max * K * N + sizeof(uint32_t) * (K + N + op.grp_max);
