@@ -334,7 +334,7 @@ struct Vec4<double2> {
 };
 
 template <class R, int K, int N, int RPT>
-__global__ void __launch_bounds__(256, (K <= 4 && N <= 4 ? 3 : 2))
+__global__ void __launch_bounds__(256, ((K <= 4 && N <= 4) || (K <= 8 && N <= 8 && sizeof(R) == 4) ? 3 : 2))
     contract_rows(const DevOp<typename V2<R>::T> op_in) {
   DevOp<typename V2<R>::T> op = op_in;
   resolve_slice(op);
