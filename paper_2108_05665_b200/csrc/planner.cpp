@@ -401,6 +401,21 @@ std::vector<int> informative_slots(const mtcg_problem& p) {
 }
 }  // namespace
 
+namespace {
+// Item indices 0..n-1 stably ordered by key[i] (keys < the key range): a
+// counting sort (the grouping / gather orders of every op; comparison sorts
+// were the largest part of host compile at 10^5 requests).
+std::vector<uint32_t> order_by_key(const std::vector<uint32_t>& key) {
+  uint32_t range = 0;
+  for (uint32_t k : key) range = std::max(range, k + 1);
+  std::vector<uint32_t> count(static_cast<size_t>(range) + 1, 0), out(key.size());
+  for (uint32_t k : key) ++count[k + 1];
+  for (uint32_t v = 0; v < range; ++v) count[v + 1] += count[v];
+  for (uint32_t i = 0; i < key.size(); ++i) out[count[key[i]]++] = i;
+  return out;
+}
+}  // namespace
+
 TupleIndex tuple_index(const mtcg_problem& p, int device) {
   const PlanIdx ix = index_plan(p);
   TupleIndex ti;
@@ -820,10 +835,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     std::vector<uint32_t> g_order, g_start;
     uint32_t g_max = 0;
     if (op.nb >= 2 && !std::getenv("MTCG_NO_GROUP")) {
-      g_order.resize(op.nb);
-      std::iota(g_order.begin(), g_order.end(), 0u);
-      std::stable_sort(g_order.begin(), g_order.end(),
-                       [&](uint32_t x, uint32_t y) { return op.ia[x] < op.ia[y]; });
+      g_order = order_by_key(op.ia);
       g_start.push_back(0);
       for (uint32_t i = 1; i <= op.nb; ++i)
         if (i == op.nb || op.ia[g_order[i]] != op.ia[g_order[i - 1]]) {
@@ -917,9 +929,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     } else if (ga_ok) {
       op.config = kTcConfig;
       const uint32_t per = 128u >> op.fa;  // items per tile
-      std::vector<uint32_t> order(op.nb);
-      std::iota(order.begin(), order.end(), 0u);
-      std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return op.ib[x] < op.ib[y]; });
+      const std::vector<uint32_t> order = order_by_key(op.ib);
       for (size_t s0 = 0; s0 < order.size();) {
         size_t s1 = s0;
         while (s1 < order.size() && op.ib[order[s1]] == op.ib[order[s0]]) ++s1;
