@@ -575,12 +575,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-#ifndef MTCG_CHAIN_BLOCKS
-#define MTCG_CHAIN_BLOCKS 3
-#endif
-#ifndef MTCG_CHAIN_BREG
-#define MTCG_CHAIN_BREG 128
-#endif
 // ---- fused operand chains (planner.hpp Chain) --------------------------------------
 //
 // One block = one final item x nu consecutive untouched-leg combinations u.
@@ -626,7 +620,7 @@ __device__ __forceinline__ void chain_step(const T* X, T* Y, const T* Bs, const 
   constexpr int K = 1 << KC, G = 1 << GB;
   // small B tiles in registers (complex64: up to 4 x 4 — else 16 broadcast
   // shared loads in a 4 x 4 work item's ~114 instructions)
-  constexpr bool b_regs = K * G * sizeof(T) <= (sizeof(T) == 8 ? MTCG_CHAIN_BREG : 64);
+  constexpr bool b_regs = K * G * sizeof(T) <= (sizeof(T) == 8 ? 128 : 64);
   const int F = 1 << f_bits;
   // kept legs keep their row positions: in_base[f] is also f's output base
   const uint32_t* in_base = tb;
@@ -688,7 +682,7 @@ __device__ __forceinline__ void chain_step_any(int kc, int gb, const T* X, T* Y,
 // contracted and stored (the load latency is the kernel's critical path; a
 // block per chunk left most blocks outside their load phase).
 template <class R>
-__global__ void __launch_bounds__(256, sizeof(R) == 4 ? MTCG_CHAIN_BLOCKS : 2)
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
     chain_kernel(const __grid_constant__ ChainDev<typename V2<R>::T> d) {
   using T = typename V2<R>::T;
   extern __shared__ __align__(16) uint8_t chain_smem[];
