@@ -120,3 +120,22 @@ def test_ingestion_to_amplitude_tsv(engine, tmp_path):
         s = b0[:7] + str(v) + b0[8:]
         re_, im_ = got.amplitudes[0, v].real, got.amplitudes[0, v].imag
         assert lines[v] == f"{s}\t{re_:.16e}\t{im_:.16e}"
+
+
+def test_auto_device_index_large_batch(engine):
+    """From 2^15 requests mtcg_eval builds the index on the GPU by default:
+    40,000 cfg1 requests (many repeats: 4,096 possible bitstrings) evaluate
+    c128 bit-identical to the oracle, with the same node_contractions."""
+    from paper_2108_05665_b200.engine import problem_arrays
+
+    c = N.grid_circuit(3, 4, 8, 12345)
+    d = N.to_diagram(c, True)
+    bits = N.random_bitstrings(N.Rng(17), 12, 40000)
+    plan = N.parse_plan(open(f"{ROOT}/plans/cfg1.plan").read())
+    p = problem_arrays(plan, d, N.build_assignments(d, bits, []))
+    want, want_nc, _, _ = O.eval_problem(p)
+    got = engine.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128"))
+    assert bits_equal(got.amplitudes, want)
+    assert np.array_equal(got.node_contractions, want_nc)
+    eq, rows, _, _ = engine.tuple_index_check(p)
+    assert eq and rows == len(set(bits))
