@@ -153,3 +153,56 @@ def test_schedule_flags_never_change_counts_on_random_instances(seed):
     assert np.array_equal(a.node_contractions, b.node_contractions)
     assert a.counters == b.counters
     assert b.plan_info.executed_contractions <= b.contractions
+
+
+def test_memory_cap_accounting_differs_from_the_reference_as_documented():
+    """the device arena counts 8 B per complex64 element over
+    its own static schedule (leaves, tables, accumulators), the reference's
+    Session 16 B per scalar over its recursion, so the smallest cap that runs
+    differs between them. Pinned on cfg1: each side's threshold is found by
+    bisection; below both, both raise MemoryCapError; between them, exactly
+    the side with the larger threshold raises; above both, neither does."""
+    from oracle import refimpl as R
+
+    if not R.available():
+        pytest.skip("reference library not built")
+    from workloads import network as N
+    from paper_2108_05665_b200.engine import problem_arrays
+
+    c = N.grid_circuit(3, 4, 8, 12345)
+    bits = N.random_bitstrings(N.Rng(99), 12, 1000)
+    plan_text = open(os.path.join(os.path.dirname(__file__), "..", "plans", "cfg1.plan")).read()
+    d = N.to_diagram(c, True)
+    p = problem_arrays(N.parse_plan(plan_text), d, N.build_assignments(d, bits, []))
+    ref = R.RefProblem(N.format_circuit(c), bits, plan_text, fuse=True)
+
+    def dev_raises(cap):
+        try:
+            emulate_arrays(p, EvalOptions(precision="c64", memory_cap_bytes=cap))
+            return False
+        except MemoryCapError:
+            return True
+
+    def ref_raises(cap):
+        try:
+            ref.emulate(cap)
+            return False
+        except R.RefError as e:
+            assert e.code == 3
+            return True
+
+    def threshold(raises):  # smallest cap that runs
+        lo, hi = 1, 1 << 40
+        assert raises(lo) and not raises(hi)
+        while hi - lo > 1:
+            mid = (lo + hi) // 2
+            lo, hi = (mid, hi) if raises(mid) else (lo, mid)
+        return hi
+
+    t_dev, t_ref = threshold(dev_raises), threshold(ref_raises)
+    assert t_dev != t_ref
+    lo, hi = sorted((t_dev, t_ref))
+    assert dev_raises(lo - 1) and ref_raises(lo - 1)
+    mid = (lo + hi) // 2
+    assert dev_raises(mid) == (t_dev > mid) and ref_raises(mid) == (t_ref > mid)
+    assert not dev_raises(hi) and not ref_raises(hi)
