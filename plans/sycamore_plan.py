@@ -127,9 +127,12 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="memo-streaming chunk (requests); 0: none")
     ap.add_argument("--alpha", type=float, default=10.0,
                     help="complex MACs per element of traffic (B200 c64: ~500 TF/s / 6.5 TB/s / 8 flop)")
+    ap.add_argument("--cc", type=float, default=1.0,
+                    help="cost multiplier for MACs the tensor cores cannot take (CUDA-core rate)")
     ap.add_argument("--out", default=None)
     ap.add_argument("--out-all", default=None, help="directory: every run's plan as run<seed>.plan")
     a = ap.parse_args()
+    os.environ["TREESA_CC"] = str(a.cc)  # read by the treesa binary
     sys.path.insert(0, os.path.join(ROOT, "plans"))
     _, d, legs, qs = network(a.cycles, a.seed)
     n_legs = d.n_closed

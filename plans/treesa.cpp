@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <bitset>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstdio>
 #include <iostream>
@@ -73,8 +74,19 @@ struct Tree {
                                       std::ldexp(1.0, static_cast<int>(r.count())) +
                                       std::ldexp(1.0, static_cast<int>((l ^ r).count()))
                                 : 0.0;
-    return evals(n.q) * (macs + alpha * rw);
+    // cc > 1: MACs of contractions the tensor-core path cannot take (fewer
+    // than 128 free rows on the larger side, fewer than 16 on the other, or
+    // K < 16) cost cc times more (the CUDA-core kernels' rate)
+    double factor = 1.0;
+    if (cc > 1.0) {
+      const int kk = static_cast<int>((l & r).count());
+      const int fl = static_cast<int>(l.count()) - kk, fr = static_cast<int>(r.count()) - kk;
+      const int mm = std::max(fl, fr), nn = std::min(fl, fr);
+      if (mm < 7 || nn < 4 || kk < 4) factor = cc;
+    }
+    return evals(n.q) * (macs * factor + alpha * rw);
   }
+  double cc = 1.0;  // CUDA-core MAC cost multiplier (see node_cost)
   double node_table(int v) const {
     return distinct(nodes[v].q, chunk_size()) * std::ldexp(1.0, static_cast<int>((nodes[v].legs & ~sliced).count()));
   }
@@ -111,6 +123,7 @@ int main() {
   T.k = k;
   T.chunk = chunk;
   T.alpha = alpha;
+  if (const char* e = std::getenv("TREESA_CC")) T.cc = std::atof(e);  // CUDA-core MAC multiplier
   T.nodes.resize(T.n_leaves);
   for (int i = 0; i < T.n_leaves; ++i) {
     int q, c;
