@@ -262,6 +262,87 @@ struct DevBuf {
 // asynchronous work; NCCL send/recv pairs (one group per round) or device
 // copies (repeated devices) carry the values; device streams order reuse of
 // the per-device and root buffers across rounds.
+// Fewer slices than devices (SURVEY §8e fallback): the requests, in
+// lexicographic tuple order, are split into one contiguous block per device;
+// each device evaluates its block over every slice with its own memo (the
+// request-independent subtrees repeat per device) and the rows come back to
+// the host by request — no cross-device sum, so every value is the one the
+// owning device computes alone (complex128: the reference's bits for any
+// device count). Counts and node_contractions are the whole evaluation's.
+void eval_multi_rows(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, int n_use, mtcg_result* res) {
+  const uint64_t K = p->n_requests;
+  const int ns = p->n_slots;
+  mtcg_options oc = o;
+  oc.row_chunk = 0;
+  oc.flags &= ~MTCG_FLAG_SLICE_REUSE;
+  const Compiled whole = compile_problem(*p, oc, 0, nullptr, -1);  // exact counts, validation
+  const uint64_t need = K * whole.row_elems;
+  if (res->values && res->values_capacity < need)
+    throw DataError("values buffer too small: need " + std::to_string(need) + " complex");
+  std::vector<uint64_t> order(K);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+    return std::lexicographical_compare(p->tuples + a * ns, p->tuples + (a + 1) * ns, p->tuples + b * ns,
+                                        p->tuples + (b + 1) * ns);
+  });
+  struct Part {
+    uint64_t r0 = 0, r1 = 0;
+    std::vector<uint32_t> tuples;
+    std::unique_ptr<mtcg_plan> plan;
+    std::unique_ptr<DevBuf> acc;
+  };
+  std::vector<Part> parts(n_use);
+  // compile + enqueue every device's block, then collect
+  for (int g = 0; g < n_use; ++g) {
+    Part& pt = parts[g];
+    pt.r0 = K * g / n_use;
+    pt.r1 = K * (g + 1) / n_use;
+    if (pt.r1 <= pt.r0) continue;
+    pt.tuples.resize((pt.r1 - pt.r0) * ns);
+    for (uint64_t r = pt.r0; r < pt.r1; ++r)
+      std::memcpy(pt.tuples.data() + (r - pt.r0) * ns, p->tuples + order[r] * ns, sizeof(uint32_t) * ns);
+    mtcg_problem q = *p;
+    q.n_requests = pt.r1 - pt.r0;
+    q.tuples = pt.tuples.data();
+    CCK(cudaSetDevice(h->devices[g]));
+    pt.plan = std::make_unique<mtcg_plan>();
+    pt.plan->dp = upload_plan(h->engines[g], compile_problem(q, oc, device_cap(h, oc), nullptr, -1));
+    const Compiled& cg = pt.plan->dp->c;
+    pt.acc = std::make_unique<DevBuf>(h->engines[g], cg.n_rows * cg.row_elems * cg.elem_bytes);
+    run_slices(*pt.plan->dp, 0, cg.n_slices, pt.acc->p, false, nullptr);
+  }
+  std::vector<double> vals;
+  uint64_t peak = 0;
+  for (int g = 0; g < n_use; ++g) {
+    Part& pt = parts[g];
+    if (!pt.plan) continue;
+    CCK(cudaSetDevice(h->devices[g]));
+    const uint64_t n = pt.r1 - pt.r0;
+    vals.assign(2 * n * whole.row_elems, 0.0);
+    mtcg_result sub;
+    std::memset(&sub, 0, sizeof sub);
+    sub.values = vals.data();
+    sub.values_capacity = n * whole.row_elems;
+    fetch_into(pt.plan.get(), pt.acc->p, nullptr, &sub);
+    peak = std::max<uint64_t>(peak, sub.hbm_peak_bytes);
+    if (res->values)
+      for (uint64_t i = 0; i < n; ++i)
+        std::memcpy(res->values + 2 * order[pt.r0 + i] * whole.row_elems, vals.data() + 2 * i * whole.row_elems,
+                    sizeof(double) * 2 * whole.row_elems);
+  }
+  CCK(cudaSetDevice(h->devices[0]));
+  if (res->node_contractions)
+    std::memcpy(res->node_contractions, whole.node_contractions.data(),
+                sizeof(uint64_t) * whole.node_contractions.size());
+  res->mults = whole.mults;
+  res->adds = whole.adds;
+  res->rw = whole.rw;
+  res->hbm_peak_bytes = peak;
+  res->cap_node = -1;
+  res->n_out_legs = static_cast<int32_t>(whole.out_legs.size());
+  for (size_t i = 0; i < whole.out_legs.size() && i < 64; ++i) res->out_legs[i] = whole.out_legs[i];
+}
+
 void eval_multi(mtcg_handle* h, const mtcg_problem* p, const mtcg_options& o, int n_use, mtcg_result* res) {
   Compiled c = compile_problem(*p, o, device_cap(h, o), nullptr, index_device(h, *p, o));
   std::vector<std::unique_ptr<DevicePlan>> plans;
@@ -750,7 +831,11 @@ mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p, const mtcg_options*
     const int n_use = o.workers > 0 ? std::min(n_dev, static_cast<int>(o.workers)) : n_dev;
     if (n_use > 1) {
       if (o.row_chunk) throw DataError("row_chunk with several devices is not supported");
-      eval_multi(h, p, o, n_use, res);
+      const uint64_t S = p->n_sliced >= 0 && p->n_sliced < 63 ? uint64_t{1} << p->n_sliced : ~uint64_t{0};
+      if (S < static_cast<uint64_t>(n_use) && p->n_requests >= static_cast<uint64_t>(n_use))
+        eval_multi_rows(h, p, o, n_use, res);  // fewer slices than GPUs: split the requests
+      else
+        eval_multi(h, p, o, n_use, res);
       return;
     }
     if (o.row_chunk && o.row_chunk < p->n_requests) {

@@ -81,3 +81,22 @@ def test_device_count_and_bad_device():
     assert lib().mtcg_visible_devices() >= 1
     with pytest.raises(DataError, match="not visible"):
         Engine(devices=[0, 999])
+
+
+@pytest.mark.parametrize("n_dev", [2, 4])
+def test_fewer_slices_than_devices_split_requests(engine, n_dev):
+    """S < devices (cfg1: one slice): the requests are split over the devices
+    in lexicographic blocks (SURVEY §8e fallback) — complex128 bit-identical
+    to the oracle, counts and node_contractions the whole evaluation's;
+    complex64 within tolerance of one device."""
+    p, c, _ = workload("cfg1")
+    want, want_nc, want_cnt, _ = O.eval_problem(p)
+    multi = Engine(devices=[0] * n_dev)
+    got = multi.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c128", workers=0))
+    assert bits_equal(got.amplitudes, want)
+    assert np.array_equal(got.node_contractions, want_nc)
+    assert (got.counters.mults, got.counters.adds, got.counters.rw) == tuple(int(x) for x in want_cnt)
+    single = engine.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c64"))
+    g64 = multi.eval(p, A.MTCG_EVAL_AUTO, EvalOptions(precision="c64", workers=0))
+    floor = 2.0 ** (-c.n_qubits / 2)
+    assert np.max(np.abs(g64.amplitudes - single.amplitudes) / np.maximum(np.abs(single.amplitudes), floor)) <= 1e-5
