@@ -406,6 +406,7 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   IK(cudaMemcpyAsync(&rows32, d_scan + (k - 1), 4, cudaMemcpyDeviceToHost, st));
   IK(cudaStreamSynchronize(st));
   const uint64_t rows = rows32;
+  const auto t_rows = std::chrono::steady_clock::now();
 
   // --- per-node ranks: one radix sort per batch of equal-height nodes -------
   uint32_t* d_rank = S.get<uint32_t>(uint64_t(n_rank_slots) * k);
@@ -441,6 +442,7 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   IK(cudaMemcpyAsync(node_off.data(), d_node_off, n * 8, cudaMemcpyDeviceToHost, st));
   IK(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, st));
   IK(cudaStreamSynchronize(st));
+  const auto t_levels = std::chrono::steady_clock::now();
   if (total > pair_bound) throw InternalError("tuple index: pair bound exceeded");
   std::vector<uint32_t> pairs(2 * total), row_of_request(k);
   ti.row_tuple_first.resize(rows);
@@ -477,6 +479,11 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   ti.row_of_request.assign(row_of_request.begin(), row_of_request.end());
   ti.rank.assign(n, nullptr);
   ti.rank[p.root] = ti.root_rank.data();
+  if (tdbg)
+    std::fprintf(stderr, "[mtcg]   device index phases: upload+rows %.3f, levels %.3f, download %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(t_rows - t0).count(),
+                 std::chrono::duration<double, std::milli>(t_levels - t_rows).count(),
+                 std::chrono::duration<double, std::milli>(t1 - t_levels).count());
   if (tdbg)
     std::fprintf(stderr, "[mtcg]   device tuple index %.3f ms (unpack %.3f ms; %d words, %llu rows, %zu batches, %d rank slots)\n",
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
