@@ -260,12 +260,11 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
 
   // --- host schedule: heights, key-width bounds, batches, rank slots --------
   // (rows <= k: bounds use k; the row count only shrinks the launches)
-  std::vector<int> height(n, 0), parent(n, -1);
+  std::vector<int> height(n, 0);
   int max_h = 0;
   for (int node : postorder)
     if (p.node_slot[node] < 0) {
       height[node] = 1 + std::max(height[p.node_left[node]], height[p.node_right[node]]);
-      parent[p.node_left[node]] = parent[p.node_right[node]] = node;
       max_h = std::max(max_h, height[node]);
     }
   std::vector<uint64_t> ub(n, 1), span(n, 1);
