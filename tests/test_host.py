@@ -206,3 +206,33 @@ def test_memory_cap_accounting_differs_from_the_reference_as_documented():
     mid = (lo + hi) // 2
     assert dev_raises(mid) == (t_dev > mid) and ref_raises(mid) == (t_ref > mid)
     assert not dev_raises(hi) and not ref_raises(hi)
+
+
+def test_maximum_sizes_are_rejected_with_the_references_messages():
+    """SURVEY §8(c) edge cases at the size limits: more than 2^24 slices is
+    the reference's own DataError (multieval.cpp:345); an intermediate of
+    order above 32 (the engine's 32-bit table offsets) is rejected up front
+    instead of wrapping; exactly 2^24 slices is accepted."""
+    from workloads import network as N
+    from paper_2108_05665_b200.engine import problem_arrays
+
+    c = N.grid_circuit(5, 6, 12, 12345)
+    d = N.to_diagram(c, True)
+    bits = N.random_bitstrings(N.Rng(99), 30, 4)
+    plan = N.parse_plan(open(os.path.join(os.path.dirname(__file__), "..", "plans", "cfg2.plan")).read())
+    asg = N.build_assignments(d, bits, [])
+    plan.sliced = list(range(25))
+    with pytest.raises(DataError) as e:
+        emulate_arrays(problem_arrays(plan, d, asg), EvalOptions(precision="c64"))
+    assert str(e.value) == "slice list expands to more than 2^24 slices"
+    plan.sliced = list(range(24))
+    info = emulate_arrays(problem_arrays(plan, d, asg), EvalOptions(precision="c64")).plan_info
+    assert info.n_slices == 1 << 24
+    # a left-deep tree over the 53-qubit m=12 network builds order > 32 nodes
+    c53 = N.sycamore_circuit(12, 2024)
+    d53 = N.to_diagram(c53, True)
+    b53 = N.random_bitstrings(N.Rng(1), 53, 2)
+    p53 = problem_arrays(N.left_deep_plan(d53.slot_count), d53, N.build_assignments(d53, b53, []))
+    with pytest.raises(DataError) as e:
+        emulate_arrays(p53, EvalOptions(precision="c64"))
+    assert "order above 32" in str(e.value)
