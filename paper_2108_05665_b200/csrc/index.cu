@@ -5,7 +5,8 @@
 // every distinct rank — computed with radix sorts on the GPU:
 //
 //   rows   the informative tuple columns (slots with more than one value)
-//          are bit-packed into 64-bit words, first column most significant;
+//          come bit-packed into 64-bit words (first column most significant;
+//          packed on the host while the tuples are validated, TupleWords);
 //          a stable LSD radix sort over the words (request index as the
 //          payload) orders the requests lexicographically, ties by request
 //          index — so a row's representative is its first request, as on the
@@ -49,20 +50,6 @@ unsigned blocks_for(uint64_t n) {
   return static_cast<unsigned>(std::min<uint64_t>((n + kThreads - 1) / kThreads, 148ull * 64));
 }
 
-// Word w of request i: the word's columns concatenated, first most significant.
-struct WordSpec {
-  int c0, c1;  // informative columns [c0, c1)
-};
-
-__global__ void pack_word(const uint32_t* __restrict__ cols, uint64_t k, const uint8_t* __restrict__ bits,
-                          int c0, int c1, uint64_t* __restrict__ out) {
-  for (uint64_t i = blockIdx.x * uint64_t{blockDim.x} + threadIdx.x; i < k; i += uint64_t{gridDim.x} * blockDim.x) {
-    uint64_t v = 0;
-    for (int c = c0; c < c1; ++c) v = (v << bits[c]) | cols[uint64_t(c) * k + i];
-    out[i] = v;
-  }
-}
-
 // word values of the requests in the current order (LSD passes after the first)
 __global__ void gather_word(const uint64_t* __restrict__ word, const uint32_t* __restrict__ order, uint64_t k,
                             uint64_t* __restrict__ out) {
@@ -96,13 +83,14 @@ __global__ void row_assign(const uint32_t* __restrict__ scan, const uint32_t* __
 // `col`; 1: single-valued leaf (every key 0); 2: internal node. Rank arrays
 // live in slots (a node's slot is recycled once its parent has run).
 struct Seg {
-  int kind, col;
+  int kind;
+  int wd, sh, nbits;          // kind 0: the column's word, bit offset, width
   int node, right;            // right: internal nodes' right child (pairs)
   int slot, lslot, rslot;     // rank array slots (own, children)
 };
 
 __global__ void level_keys(const Seg* __restrict__ segs, int n_segs, uint64_t rows, int kb,
-                           const uint32_t* __restrict__ cols, uint64_t k, const uint32_t* __restrict__ row_first,
+                           const uint64_t* __restrict__ words, uint64_t k, const uint32_t* __restrict__ row_first,
                            const uint32_t* __restrict__ rank, const uint32_t* __restrict__ distinct,
                            uint64_t* __restrict__ keys, uint32_t* __restrict__ pos) {
   const uint64_t n = uint64_t(n_segs) * rows;
@@ -110,7 +98,8 @@ __global__ void level_keys(const Seg* __restrict__ segs, int n_segs, uint64_t ro
     const uint64_t s = i / rows, r = i - s * rows;
     const Seg g = segs[s];
     uint64_t key = 0;
-    if (g.kind == 0) key = cols[uint64_t(g.col) * k + row_first[r]];
+    if (g.kind == 0)
+      key = (words[uint64_t(g.wd) * k + row_first[r]] >> g.sh) & ((uint64_t{1} << g.nbits) - 1);
     else if (g.kind == 2)
       key = uint64_t(rank[uint64_t(g.lslot) * rows + r]) * distinct[g.right] + rank[uint64_t(g.rslot) * rows + r];
     keys[i] = (kb < 64 ? s << kb : 0) | key;
@@ -235,9 +224,8 @@ __global__ void iota_u32(uint32_t* v, uint64_t n) {
 
 }  // namespace
 
-bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& postorder,
-                              const std::vector<int>& informative, const std::vector<uint32_t>& colsT, int device,
-                              TupleIndex& ti) {
+bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& postorder, const TupleWords& lay,
+                              const std::vector<uint64_t>& tuple_words, int device, TupleIndex& ti) {
   const uint64_t k = p.n_requests;
   if (k == 0 || k >= (uint64_t{1} << 31) || device < 0 || device >= 64) return false;
   const bool tdbg = std::getenv("MTCG_TIMING") != nullptr;
@@ -245,18 +233,9 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   const int m = p.n_slots;
   const int n = p.n_nodes;
   std::vector<int> column_of(m, -1);
-  const int w = static_cast<int>(informative.size());
-  for (int c = 0; c < w; ++c) column_of[informative[c]] = c;
-  std::vector<uint8_t> bits(w);
-  for (int c = 0; c < w; ++c) bits[c] = static_cast<uint8_t>(bits_for(static_cast<uint64_t>(p.slot_n_values[informative[c]])));
-  std::vector<WordSpec> words;
-  for (int c0 = 0; c0 < w;) {
-    int c1 = c0, used = 0;
-    while (c1 < w && used + bits[c1] <= 64) used += bits[c1++];
-    words.push_back({c0, c1});
-    c0 = c1;
-  }
-  const int nw = static_cast<int>(words.size());
+  const int w = static_cast<int>(lay.informative.size());
+  for (int c = 0; c < w; ++c) column_of[lay.informative[c]] = c;
+  const int nw = static_cast<int>(lay.span.size());
 
   // --- host schedule: heights, key-width bounds, batches, rank slots --------
   // (rows <= k: bounds use k; the row count only shrinks the launches)
@@ -274,9 +253,14 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
     g.node = node;
     g.right = -1;
     if (p.node_slot[node] >= 0) {
-      g.col = column_of[p.node_slot[node]];
-      g.kind = g.col >= 0 ? 0 : 1;
-      span[node] = g.col >= 0 ? static_cast<uint64_t>(p.slot_n_values[p.node_slot[node]]) : 1;
+      const int col = column_of[p.node_slot[node]];
+      g.kind = col >= 0 ? 0 : 1;
+      if (col >= 0) {
+        g.wd = lay.word[col];
+        g.sh = lay.shift[col];
+        g.nbits = lay.bits[col];
+      }
+      span[node] = col >= 0 ? static_cast<uint64_t>(p.slot_n_values[p.node_slot[node]]) : 1;
     } else {
       g.kind = 2;
       g.right = p.node_right[node];
@@ -335,7 +319,7 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   uint64_t max_cnt = k;
   for (const Batch& b : batches) max_cnt = std::max<uint64_t>(max_cnt, uint64_t(b.ns) * k);
   auto al = [](uint64_t b) { return (b + 255) & ~uint64_t{255}; };
-  const size_t need = al(uint64_t(std::max(w, 1)) * k * 4) + al(std::max(w, 1)) + al(uint64_t(std::max(nw, 1)) * k * 8) +
+  const size_t need = al(uint64_t(std::max(nw, 1)) * k * 8) +
                       2 * al(k * 8) + 6 * al(k * 4) + al(uint64_t(n_rank_slots) * k * 4) + al(all.size() * sizeof(Seg)) +
                       2 * al(max_cnt * 8) + 4 * al(max_cnt * 4) + al(pair_bound * 8) + al(n * 8) + al(n * 4) + al(8) +
                       al(Cub::need(max_cnt, max_cnt)) + 4096;
@@ -371,13 +355,8 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   cub.temp = S.get<uint8_t>(cub.temp_bytes);
   ti = TupleIndex{};
 
-  uint32_t* d_cols = S.get<uint32_t>(uint64_t(std::max(w, 1)) * k);
-  uint8_t* d_bits = S.get<uint8_t>(std::max(w, 1));
-  if (w) {
-    IK(cudaMemcpyAsync(d_cols, colsT.data(), uint64_t(w) * k * 4, cudaMemcpyHostToDevice, st));
-    IK(cudaMemcpyAsync(d_bits, bits.data(), w, cudaMemcpyHostToDevice, st));
-  }
   uint64_t* d_words = S.get<uint64_t>(uint64_t(std::max(nw, 1)) * k);
+  if (nw) IK(cudaMemcpyAsync(d_words, tuple_words.data(), uint64_t(nw) * k * 8, cudaMemcpyHostToDevice, st));
   uint64_t* d_ka = S.get<uint64_t>(k);
   uint64_t* d_kb = S.get<uint64_t>(k);
   uint32_t* d_order = S.get<uint32_t>(k);
@@ -387,13 +366,9 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   uint32_t* d_row_of_request = S.get<uint32_t>(k);
   uint32_t* d_row_first = S.get<uint32_t>(k);
   iota_u32<<<blocks_for(k), kThreads, 0, st>>>(d_order, k);
-  for (int x = 0; x < nw; ++x)
-    pack_word<<<blocks_for(k), kThreads, 0, st>>>(d_cols, k, d_bits, words[x].c0, words[x].c1,
-                                                  d_words + uint64_t(x) * k);
   // LSD: least significant word first; stable sorts keep the earlier order
   for (int x = nw - 1; x >= 0; --x) {
-    int used = 0;
-    for (int c = words[x].c0; c < words[x].c1; ++c) used += bits[c];
+    const int used = lay.word_bits[x];
     gather_word<<<blocks_for(k), kThreads, 0, st>>>(d_words + uint64_t(x) * k, d_order, k, d_ka);
     cub.sort(d_ka, d_kb, d_order, d_order2, k, used);
     std::swap(d_order, d_order2);
@@ -424,7 +399,7 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   IK(cudaMemcpyAsync(d_all, all.data(), all.size() * sizeof(Seg), cudaMemcpyHostToDevice, st));
   for (const Batch& b : batches) {
     const uint64_t cnt = uint64_t(b.ns) * rows;
-    level_keys<<<blocks_for(cnt), kThreads, 0, st>>>(d_all + b.s0, b.ns, rows, b.kb, d_cols, k, d_row_first, d_rank,
+    level_keys<<<blocks_for(cnt), kThreads, 0, st>>>(d_all + b.s0, b.ns, rows, b.kb, d_words, k, d_row_first, d_rank,
                                                      d_distinct, d_k1, d_p1);
     cub.sort(d_k1, d_k2, d_p1, d_p2, cnt, std::min(64, b.kb + bits_for(b.ns)));
     level_flags<<<blocks_for(cnt), kThreads, 0, st>>>(d_k2, cnt, d_f);
@@ -443,7 +418,10 @@ bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& pos
   IK(cudaStreamSynchronize(st));
   const auto t_levels = std::chrono::steady_clock::now();
   if (total > pair_bound) throw InternalError("tuple index: pair bound exceeded");
-  std::vector<uint32_t> pairs(2 * total), row_of_request(k);
+  // host staging kept across builds (fresh pages cost more than the copies)
+  static thread_local std::vector<uint32_t> pairs, row_of_request;
+  pairs.resize(2 * total);
+  row_of_request.resize(k);
   ti.row_tuple_first.resize(rows);
   ti.root_rank.resize(rows);
   IK(cudaMemcpyAsync(pairs.data(), d_pairs, total * 8, cudaMemcpyDeviceToHost, st));

@@ -355,22 +355,27 @@ struct SectionTimer {
 
 namespace {
 // check_inputs' tuple range check (multieval.cpp:284-297; the first offending
-// entry in request-major order names the slot), fused with the extraction of
-// the informative columns for the device tuple index (colsT != nullptr);
+// entry in request-major order names the slot), fused with the bit-packing of
+// the tuples for the device tuple index (words != nullptr, layout `lay`);
 // split over host threads for large batches.
-void check_tuples(const mtcg_problem& p, const std::vector<int>& informative, std::vector<uint32_t>* colsT) {
+void check_tuples(const mtcg_problem& p, const TupleWords* lay, std::vector<uint64_t>* words) {
   const uint64_t k = p.n_requests;
   const int m = p.n_slots;
-  const size_t w = informative.size();
-  if (colsT) colsT->resize(std::max<size_t>(w, 1) * k);
-  uint32_t* out = colsT ? colsT->data() : nullptr;
+  const size_t nw = lay ? lay->span.size() : 0;
+  if (words) words->resize(std::max<size_t>(nw, 1) * k);
+  uint64_t* out = words ? words->data() : nullptr;
   auto range = [&](uint64_t i0, uint64_t i1) -> uint64_t {  // first bad flat index or ~0
     for (uint64_t i = i0; i < i1; ++i) {
       const uint32_t* t = p.tuples + i * m;
       for (int j = 0; j < m; ++j)
         if (t[j] >= static_cast<uint32_t>(p.slot_n_values[j])) return i * m + j;
       if (out)
-        for (size_t c = 0; c < w; ++c) out[c * k + i] = t[informative[c]];
+        for (size_t x = 0; x < nw; ++x) {
+          uint64_t v = 0;
+          for (int c = lay->span[x].first; c < lay->span[x].second; ++c)
+            v = (v << lay->bits[c]) | t[lay->informative[c]];
+          out[x * k + i] = v;
+        }
     }
     return ~uint64_t{0};
   };
@@ -401,6 +406,35 @@ std::vector<int> informative_slots(const mtcg_problem& p) {
 }
 }  // namespace
 
+TupleWords tuple_word_layout(const mtcg_problem& p) {
+  TupleWords L;
+  L.informative = informative_slots(p);
+  const int w = static_cast<int>(L.informative.size());
+  for (int c = 0; c < w; ++c) {
+    uint64_t nv = static_cast<uint64_t>(p.slot_n_values[L.informative[c]]);
+    int b = 0;
+    while ((uint64_t{1} << b) < nv) ++b;
+    L.bits.push_back(static_cast<uint8_t>(b));
+  }
+  L.word.assign(w, 0);
+  L.shift.assign(w, 0);
+  for (int c0 = 0; c0 < w;) {
+    int c1 = c0, used = 0;
+    while (c1 < w && used + L.bits[c1] <= 64) used += L.bits[c1++];
+    const int x = static_cast<int>(L.span.size());
+    int sh = used;
+    for (int c = c0; c < c1; ++c) {  // first column most significant
+      sh -= L.bits[c];
+      L.word[c] = x;
+      L.shift[c] = sh;
+    }
+    L.span.push_back({c0, c1});
+    L.word_bits.push_back(used);
+    c0 = c1;
+  }
+  return L;
+}
+
 namespace {
 // Item indices 0..n-1 stably ordered by key[i] (keys < the key range): a
 // counting sort (the grouping / gather orders of every op; comparison sorts
@@ -419,10 +453,10 @@ std::vector<uint32_t> order_by_key(const std::vector<uint32_t>& key) {
 TupleIndex tuple_index(const mtcg_problem& p, int device) {
   const PlanIdx ix = index_plan(p);
   TupleIndex ti;
-  const std::vector<int> inf = informative_slots(p);
-  std::vector<uint32_t> colsT;
-  check_tuples(p, inf, device >= 0 ? &colsT : nullptr);
-  if (device < 0 || !build_tuple_index_device(p, ix.postorder, inf, colsT, device, ti)) ti = build_tuple_index(p, ix);
+  const TupleWords lay = tuple_word_layout(p);
+  std::vector<uint64_t> words;
+  check_tuples(p, &lay, device >= 0 ? &words : nullptr);
+  if (device < 0 || !build_tuple_index_device(p, ix.postorder, lay, words, device, ti)) ti = build_tuple_index(p, ix);
   return ti;
 }
 
@@ -443,9 +477,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
 
   // --- check_inputs (multieval.cpp:284-297) --------------------------------
   const PlanIdx ix = index_plan(p);
-  const std::vector<int> informative = informative_slots(p);
-  static thread_local std::vector<uint32_t> colsT;  // informative columns for the device index
-  check_tuples(p, informative, index_device >= 0 ? &colsT : nullptr);
+  const TupleWords tuple_lay = tuple_word_layout(p);
+  static thread_local std::vector<uint64_t> tuple_words;  // packed tuples for the device index
+  check_tuples(p, &tuple_lay, index_device >= 0 ? &tuple_words : nullptr);
   for (int j = 0; j < p.n_slots; ++j)
     if (p.slot_n_values[j] < 1)
       throw DataError(fmt("slot %lld has an empty value set", j));
@@ -506,7 +540,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
   timer.mark("validate+leaves");
   // --- tuple index ----------------------------------------------------------
   TupleIndex ti;
-  if (index_device < 0 || !build_tuple_index_device(p, ix.postorder, informative, colsT, index_device, ti))
+  if (index_device < 0 || !build_tuple_index_device(p, ix.postorder, tuple_lay, tuple_words, index_device, ti))
     ti = build_tuple_index(p, ix);
   c.n_requests = p.n_requests;
   c.n_rows = ti.rows;

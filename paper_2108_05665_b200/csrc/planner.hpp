@@ -217,14 +217,25 @@ struct TupleIndex {
   std::vector<uint32_t> distinct;
 };
 
+// Bit-packed request tuples for the device tuple index: the informative
+// slots (more than one value), ascending, each ceil(log2 n_values) bits,
+// concatenated first-most-significant into 64-bit words (lexicographic
+// tuple order = numeric order of the word sequence).
+struct TupleWords {
+  std::vector<int> informative;         // slot of each informative column
+  std::vector<uint8_t> bits;            // per column
+  std::vector<int> word, shift;         // per column: word index, bit offset in it
+  std::vector<std::pair<int, int>> span;  // per word: columns [c0, c1)
+  std::vector<int> word_bits;           // per word: bits used
+};
+TupleWords tuple_word_layout(const mtcg_problem& p);
+
 // Device builder (index.cu): radix sorts on GPU `device`, same TupleIndex as
-// the host builder. `postorder` lists children before parents; colsT holds
-// the informative slots' columns (slots with more than one value, ascending),
-// column-major [informative.size()][n_requests]. Returns false when it does
-// not apply (no requests).
-bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& postorder,
-                              const std::vector<int>& informative, const std::vector<uint32_t>& colsT, int device,
-                              TupleIndex& ti);
+// the host builder. `postorder` lists children before parents; `words` holds
+// the packed tuples word-major ([word][request], layout `lay`). Returns false
+// when it does not apply (no requests, no room for its scratch).
+bool build_tuple_index_device(const mtcg_problem& p, const std::vector<int>& postorder, const TupleWords& lay,
+                              const std::vector<uint64_t>& words, int device, TupleIndex& ti);
 
 // The tuple index alone (index_plan's checks, then the device builder on
 // `device` >= 0 or the host builder): diagnostics / tests.
