@@ -17,6 +17,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "device.hpp"
 #include "configs.hpp"
 #include "planner.hpp"
@@ -61,6 +63,15 @@ void set_err(char* err, size_t errlen, const char* msg) {
     std::snprintf(err, errlen, "%s", msg);
   }
 }
+
+// NVTX ranges around the ABI entry points (visible in Nsight Systems /
+// Compute timelines; no-ops without a profiler attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <class F>
 mtcg_status guarded(char* err, size_t errlen, int32_t* cap_node, F&& f) {
@@ -707,6 +718,7 @@ mtcg_status mtcg_emulate(const mtcg_problem* p, const mtcg_options* opt, uint64_
 
 mtcg_status mtcg_compile(mtcg_handle* h, const mtcg_problem* p, const mtcg_options* opt,
                          mtcg_plan** out, int32_t* cap_node, char* err, size_t errlen) {
+  NvtxRange nv("mtcg_compile");
   return guarded(err, errlen, cap_node, [&] {
     if (!h || !out) throw DataError("null handle");
     check_problem_pointers(p);
@@ -746,6 +758,7 @@ mtcg_status mtcg_plan_get_info(const mtcg_plan* plan, mtcg_plan_info* info) {
 
 mtcg_status mtcg_run(mtcg_plan* plan, uint64_t slice_begin, uint64_t slice_end, void* d_acc,
                      int accumulate, void* stream, char* err, size_t errlen) {
+  NvtxRange nv("mtcg_run");
   return guarded(err, errlen, nullptr, [&] {
     if (!plan) throw DataError("null plan");
     const Compiled& c = plan->dp->c;
@@ -789,6 +802,7 @@ mtcg_status mtcg_fold(mtcg_plan* plan, const void* d_parts, uint64_t n_parts, vo
 
 mtcg_status mtcg_fetch(mtcg_plan* plan, const void* d_acc, void* stream, mtcg_result* res,
                        char* err, size_t errlen) {
+  NvtxRange nv("mtcg_fetch");
   return guarded(err, errlen, nullptr, [&] {
     if (!plan || !res) throw DataError("null argument");
     if (plan->chunked) {
@@ -822,6 +836,7 @@ mtcg_status mtcg_xeb_device(mtcg_plan* plan, const void* d_acc, int n_qubits, vo
 
 mtcg_status mtcg_eval(mtcg_handle* h, const mtcg_problem* p, const mtcg_options* opt,
                       mtcg_result* res, char* err, size_t errlen) {
+  NvtxRange nv("mtcg_eval");
   int32_t cap_node = -1;
   mtcg_status st = guarded(err, errlen, &cap_node, [&] {
     if (!h || !res) throw DataError("null argument");
