@@ -358,6 +358,10 @@ constexpr int kTraceTiles = 256;
 __device__ __forceinline__ void trace(const TcParams& p, uint64_t it, int slot) {
   if (p.dbg && blockIdx.x == 0 && it < kTraceTiles) p.dbg[it * 8 + slot] = clock64();
 }
+// split-integer kernel: 16 slots per tile (the 8 above + finer marks)
+__device__ __forceinline__ void trace16(const TcParams& p, uint64_t it, int slot) {
+  if (p.dbg && blockIdx.x == 0 && it < kTraceTiles) p.dbg[it * 16 + slot] = clock64();
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -1379,7 +1383,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const uint32_t item = w.u;
         const int m0 = static_cast<int>(w.m) * kTM + m_off;
         const int n0 = static_cast<int>(w.n) * p.bn + static_cast<int>(rank) * bn_cta;
-        trace(p, pit, 0);
+        trace16(p, pit, 0);
         if (item != cached_item) {
           cached_item = item;
           a_entry = unit_a_entry(item);
@@ -1401,6 +1405,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
           const int st = rg.slot;
           if (rg.round > 0) mbar_wait(&empty[st], (rg.round - 1) & 1);
+          if (s == 0) trace16(p, pit, 12);  // stage free
           uint8_t* sp = base + st * stage_bytes;
           const uint32_t a_bytes = QA ? 3 * a_box_bytes : raw_halves * a_box_bytes;
           mbar_expect_tx(&full[st], a_bytes + 3 * plane_b);
@@ -1430,7 +1435,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           }
           tma_load_3d(sp + a_span, &map_b, &full[st], s * kI8Kb, b_row0, 0);
         }
-        trace(p, pit, 1);
+        trace16(p, pit, 1);
       }
     }
   } else if (warp == 1) {  // ---- MMA issuer (converged warp, one elected lane issues) ----
@@ -1456,7 +1461,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         d1 = dacc + p.bn;
         d2 = dacc + 2 * p.bn;
       }
-      if (lane == 0) trace(p, it, 2);
+      if (lane == 0) trace16(p, it, 2);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       for (int s = 0; s < k_stages; ++s, rg.next(n_stages)) {
         const int st = rg.slot;
@@ -1464,6 +1469,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           mbar_wait(&full[st], rg.round & 1);
         else
           mbar_wait(&conv[st], rg.round & 1);
+        if (s == 0 && lane == 0) trace16(p, it, 11);  // stage converted / landed
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sp = smem_u32(base + st * stage_bytes);
         mma_stage_i8<PAIR>(dacc, d1, d2, sw_desc<16>(sp), sw_desc<16>(sp + a_span), kPlaneA,
@@ -1477,7 +1483,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mma_commit_pair_elect(&acc_full[tb]);
       else
         mma_commit_elect(&acc_full[tb]);
-      if (lane == 0) trace(p, it, 3);
+      if (lane == 0) trace16(p, it, 3);
     }
   } else if (QA && PAIR && warp == 2) {  // ---- relay: both CTAs' stages landed ----
     // (the leader's MMA issues over both CTAs' shared memory: each CTA's
@@ -1502,9 +1508,10 @@ __global__ void __launch_bounds__(kPThreads, 1)
     for (uint64_t t = t_first; t < t_last; t += t_stride, ++cit, rg.next(n_stages)) {
       const int st = rg.slot;
       mbar_wait(&full[st], rg.round & 1);
-      if (r == 0) trace(p, cit, 4);
+      if (r == 0) trace16(p, cit, 4);
       uint8_t* sp = base + st * stage_bytes;
       const int sa = two ? convert_row_i8<true>(sp, r, p.n_conv) : convert_row_i8<false>(sp, r, p.n_conv);
+      if (r == 0) trace16(p, cit, 8);  // converted
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       // row exponent for this tile's epilogue (ring slot released by the
       // pipeline depth: converters run at most n_stages + n_acc tiles ahead)
@@ -1716,14 +1723,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
         asm volatile("bar.sync %0, 128;" ::"r"(1 + eg));
         table_key = key;
       }
-      if (warp == e0 && lane == 0) trace(p, it, 7);
+      if (warp == e0 && lane == 0) trace16(p, it, 7);
       mbar_wait(&acc_full[tb], tb_round & 1);
       if constexpr (!QA) {
         mbar_wait(&sa_full[sa_slot], sa_round & 1);
         sa = sa_ring[sa_slot * kBM + r];
       }
       const float rs = pow2f_wide(24 - sa);  // result = 2^(24 - sa - sb) v
-      if (warp == e0 && lane == 0) trace(p, it, 5);
+      if (warp == e0 && lane == 0) trace16(p, it, 5);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (split) {
         const uint32_t i32 = static_cast<uint32_t>(it);
@@ -1751,11 +1758,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
         for (int c0 = 0; c0 < p.bn; c0 += 32) {
           float v[32];
           i8_load_combine(tacc + c0, tacc + p.bn + c0, tacc + 2 * p.bn + c0, wide, v);
+          if (c0 == 0 && warp == e0 && lane == 0) trace16(p, it, 9);  // accumulators combined
           store_chunk(v, c0 / 2, rs);
         }
+        if (warp == e0 && lane == 0) trace16(p, it, 10);  // stores issued
         epi_arrive(&acc_empty[tb], acc_empty_leader + 8u * tb);
       }
-      if (warp == e0 && lane == 0) trace(p, it, 6);
+      if (warp == e0 && lane == 0) trace16(p, it, 6);
       tb += static_cast<uint32_t>(it_step);
       while (tb >= n_acc) {
         tb -= n_acc;
@@ -2317,8 +2326,8 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   const char* tr = std::getenv("MTCG_TC_TRACE");
   const bool tracing = tr && std::atoi(tr) == op.node;
   if (tracing) {
-    TCK(cudaMalloc(&p.dbg, sizeof(unsigned long long) * kTraceTiles * 8));
-    TCK(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * kTraceTiles * 8, st));
+    TCK(cudaMalloc(&p.dbg, sizeof(unsigned long long) * kTraceTiles * 16));
+    TCK(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * kTraceTiles * 16, st));
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -2335,21 +2344,23 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   TCK(cudaLaunchKernelEx(&cfg, kern, ma, mb, p, n_stages));
   ++launches;
   if (tracing) {
-    std::vector<unsigned long long> h(kTraceTiles * 8);
+    std::vector<unsigned long long> h(kTraceTiles * 16);
     TCK(cudaMemcpyAsync(h.data(), p.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st));
     TCK(cudaStreamSynchronize(st));
     TCK(cudaFree(p.dbg));
     const unsigned long long t0 = h[0];
-    std::fprintf(stderr, "[tc trace node %d] i8 pair=%d qa=%d stages=%d bn=%d tiles=%llu grid=%u\n", op.node,
-                 pair ? 1 : 0, qa ? 1 : 0, n_stages, bn, static_cast<unsigned long long>(tiles), grid);
-    std::fprintf(stderr, " tile  prod0  prod1  conv  mma0  mma1  epi-top epi0  epi1   (cycles from tile0 prod0)\n");
+    std::fprintf(stderr, "[tc trace node %d] i8 pair=%d qa=%d stages=%d bn=%d tiles=%llu grid=%u n_conv=%d\n", op.node,
+                 pair ? 1 : 0, qa ? 1 : 0, n_stages, bn, static_cast<unsigned long long>(tiles), grid, n_conv);
+    std::fprintf(stderr,
+                 " tile  prod0 stfree  prod1 landed convd  mma0 mmaC  mma1 epiTop  epi0 comb  strs  epi1"
+                 "   (cycles from tile0 prod0; mmaC = stage ready for the MMA)\n");
+    auto at = [&](int i, int slot) { return h[i * 16 + slot] ? (long long)(h[i * 16 + slot] - t0) : -1LL; };
     for (int i = 0; i < kTraceTiles; ++i) {
-      if (!h[i * 8]) break;
+      if (!h[i * 16]) break;
       if (i < 24 || i % 32 == 0)
-        std::fprintf(stderr, " %4d %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", i, (long long)(h[i * 8] - t0),
-                     (long long)(h[i * 8 + 1] - t0), (long long)(h[i * 8 + 4] - t0), (long long)(h[i * 8 + 2] - t0),
-                     (long long)(h[i * 8 + 3] - t0), (long long)(h[i * 8 + 7] - t0), (long long)(h[i * 8 + 5] - t0),
-                     (long long)(h[i * 8 + 6] - t0));
+        std::fprintf(stderr, " %4d %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", i,
+                     at(i, 0), at(i, 12), at(i, 1), at(i, 4), at(i, 8), at(i, 2), at(i, 11), at(i, 3), at(i, 7),
+                     at(i, 5), at(i, 9), at(i, 10), at(i, 6));
     }
   }
   return launches;
