@@ -20,12 +20,15 @@
 #include "planner.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <thread>
 
@@ -765,20 +768,33 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
   // smallest log2 N sent to the tensor cores (MTCG_TC_MIN_FB overrides; tuning)
   const int tc_min_fb = std::getenv("MTCG_TC_MIN_FB") ? std::atoi(std::getenv("MTCG_TC_MIN_FB")) : 4;
   c.node_contractions.assign(n, 0);
-  SectionTimer sec;
-  for (int node : sched) {
-    sec.start();
+  // Per-op item arrays and grouping: functions of the tuple index and the
+  // plan only, computed for every node up front — over host threads when the
+  // batch is large (10^5 requests: ~3.5 ms single-threaded).
+  struct OpPrep {
+    std::vector<uint32_t> closed, fl, fr, ia, ib, g_order, g_start, tg_start;
+    uint32_t g_max = 0, tc_slots = 0;
+    bool a_is_left = false, ga_mode = false;
+  };
+  std::vector<OpPrep> prep(n);
+  auto prepare = [&](int node) {
+    OpPrep& pr = prep[node];
     const int l = p.node_left[node], r = p.node_right[node];
     const auto& L = legs[l];
     const auto& R = legs[r];
-    std::vector<uint32_t> closed, fl, fr;
+    std::vector<uint32_t>& closed = pr.closed;
+    std::vector<uint32_t>& fl = pr.fl;
+    std::vector<uint32_t>& fr = pr.fr;
     for (uint32_t x : L) (contains(R, x) ? closed : fl).push_back(x);
     for (uint32_t x : R)
       if (!contains(L, x)) fr.push_back(x);
     std::sort(closed.begin(), closed.end());
-
-    Op op;
-    op.node = node;
+    struct {
+      bool a_is_left;
+      int fb, kc;
+      uint32_t nb;
+      std::vector<uint32_t> ia, ib;
+    } op;
     op.a_is_left = fl.size() >= fr.size();
     // Tensor-core gather mode (see below): the gathered A side has M = 32 / 64
     // rows per item and the B side is shared (>= 8 items per B entry); pick
@@ -801,59 +817,26 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         op.a_is_left = !op.a_is_left;
       }
     }
-    op.child_a = op.a_is_left ? l : r;
-    op.child_b = op.a_is_left ? r : l;
-    const auto& fa_legs = op.a_is_left ? fl : fr;
-    const auto& fb_legs = op.a_is_left ? fr : fl;
-    op.fa = static_cast<int>(fa_legs.size());
-    op.fb = static_cast<int>(fb_legs.size());
+    const int child_a = op.a_is_left ? l : r, child_b = op.a_is_left ? r : l;
+    op.fb = static_cast<int>((op.a_is_left ? fr : fl).size());
     op.kc = static_cast<int>(closed.size());
     op.nb = ti.distinct[node];
-    op.root = node == p.root;
-    const auto& out_layout = layout[node];
-
-    // operand sources and per-item entries
-    auto setup_operand = [&](int child, bool& is_leaf, uint64_t& base, uint64_t& item,
-                             std::vector<uint32_t>& idx) {
-      is_leaf = p.node_slot[child] >= 0;
-      idx.resize(op.nb);
-      if (is_leaf) {
-        const int slot = p.node_slot[child];
-        base = c.slot_base[slot];
-        item = c.slot_item[slot];
-      } else {
-        base = arena_off[child];
-        item = uint64_t{1} << legs[child].size();
-      }
-    };
-    setup_operand(op.child_a, op.a_leaf, op.a_base, op.a_item, op.ia);
-    setup_operand(op.child_b, op.b_leaf, op.b_base, op.b_item, op.ib);
     // entry of each child per distinct rank of this node; a leaf's rank is
     // the rank of its value index among the rows (ranks == value indices when
     // every value occurs, which build_assignments guarantees; map explicitly).
     {
       const auto& ra = op.a_is_left ? ti.pair_l[node] : ti.pair_r[node];
       const auto& rb = op.a_is_left ? ti.pair_r[node] : ti.pair_l[node];
-      // a leaf child's rank maps to its value index through rank_value
-      const auto& va = ti.rank_value[op.child_a];
-      const auto& vb = ti.rank_value[op.child_b];
+      const bool a_leaf = p.node_slot[child_a] >= 0, b_leaf = p.node_slot[child_b] >= 0;
+      const auto& va = ti.rank_value[child_a];
+      const auto& vb = ti.rank_value[child_b];
+      op.ia.resize(op.nb);
+      op.ib.resize(op.nb);
       for (uint32_t b = 0; b < op.nb; ++b) {
-        op.ia[b] = op.a_leaf ? va[ra[b]] : ra[b];
-        op.ib[b] = op.b_leaf ? vb[rb[b]] : rb[b];
+        op.ia[b] = a_leaf ? va[ra[b]] : ra[b];
+        op.ib[b] = b_leaf ? vb[rb[b]] : rb[b];
       }
     }
-    sec.lap(0);
-    const auto& a_layout = layout[op.child_a];
-    const auto& b_layout = layout[op.child_b];
-    // m / n bit orders: free legs by increasing address in the output layout
-    auto by_out_addr = [&](std::vector<uint32_t> v) {
-      std::sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) {
-        return stride_in(out_layout, x) < stride_in(out_layout, y);
-      });
-      return v;
-    };
-    op.config = select_config(op.fa, op.fb, op.kc);
-    if (op.config == kGenericConfig && c.precision == MTCG_C64 && op.kc >= 6) op.config = kDotConfig;
     // Tensor-core path (complex64 only): dense, K-contiguous intermediate A,
     // shapes the 128 x (2N) x (2K) real tiles cover exactly.
     // Ops with intensity MNK / (MK + NK + MN) >= 6 complex MACs per element
@@ -866,8 +849,9 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     // concatenation of its items' B blocks (N_eff = slots x N, slots = the
     // largest group, padded so 2 N_eff is a multiple of 32 for the tensor
     // path). MTCG_NO_GROUP=1 disables grouping (A/B tuning).
-    std::vector<uint32_t> g_order, g_start;
-    uint32_t g_max = 0;
+    std::vector<uint32_t>& g_order = pr.g_order;
+    std::vector<uint32_t>& g_start = pr.g_start;
+    uint32_t& g_max = pr.g_max;
     if (op.nb >= 2 && !std::getenv("MTCG_NO_GROUP")) {
       g_order = order_by_key(op.ia);
       g_start.push_back(0);
@@ -887,8 +871,8 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     // sub-groups of S items with S minimising units x (K + S N) — one A row
     // read per unit plus S item blocks drained per row (S = 1: no grouping).
     // 2 N S must be a multiple of 32 real columns.
-    std::vector<uint32_t> tg_start;
-    uint32_t tc_slots = 0;
+    std::vector<uint32_t>& tg_start = pr.tg_start;
+    uint32_t& tc_slots = pr.tc_slots;
     if (g_max > 0) {
       const uint32_t q = op.fb < 4 ? 16u >> op.fb : 1u;  // slots per 32 real columns
       const double Kd = std::ldexp(1.0, op.kc), Nd = std::ldexp(1.0, op.fb);
@@ -911,6 +895,92 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
         tc_slots = 0;
       }
     }
+    pr.a_is_left = op.a_is_left;
+    pr.ga_mode = ga_mode;
+    pr.ia = std::move(op.ia);
+    pr.ib = std::move(op.ib);
+  };
+  {
+    uint64_t items = 0;
+    for (int node : sched) items += ti.distinct[node];
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nt = items >= (uint64_t{1} << 17) ? std::min<unsigned>(hw, static_cast<unsigned>(sched.size())) : 1;
+    if (nt <= 1) {
+      for (int node : sched) prepare(node);
+    } else {
+      // nodes handed out largest first (one 10^5-item node is most of the work)
+      std::vector<int> order(sched.begin(), sched.end());
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return ti.distinct[x] > ti.distinct[y]; });
+      std::atomic<size_t> next{0};
+      std::exception_ptr err;
+      std::mutex err_mu;
+      std::vector<std::thread> th;
+      for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+          try {
+            for (size_t i; (i = next.fetch_add(1)) < order.size();) prepare(order[i]);
+          } catch (...) {
+            std::lock_guard<std::mutex> g(err_mu);
+            if (!err) err = std::current_exception();
+          }
+        });
+      for (auto& x : th) x.join();
+      if (err) std::rethrow_exception(err);
+    }
+  }
+  SectionTimer sec;
+  for (int node : sched) {
+    sec.start();
+    OpPrep& pr = prep[node];
+    const int l = p.node_left[node], r = p.node_right[node];
+    const std::vector<uint32_t> closed = std::move(pr.closed), fl = std::move(pr.fl), fr = std::move(pr.fr);
+
+    Op op;
+    op.node = node;
+    op.a_is_left = pr.a_is_left;
+    const bool ga_mode = pr.ga_mode;
+    op.child_a = op.a_is_left ? l : r;
+    op.child_b = op.a_is_left ? r : l;
+    const auto& fa_legs = op.a_is_left ? fl : fr;
+    const auto& fb_legs = op.a_is_left ? fr : fl;
+    op.fa = static_cast<int>(fa_legs.size());
+    op.fb = static_cast<int>(fb_legs.size());
+    op.kc = static_cast<int>(closed.size());
+    op.nb = ti.distinct[node];
+    op.root = node == p.root;
+    const auto& out_layout = layout[node];
+
+    // operand sources (per-item entries: prep)
+    auto setup_operand = [&](int child, bool& is_leaf, uint64_t& base, uint64_t& item) {
+      is_leaf = p.node_slot[child] >= 0;
+      if (is_leaf) {
+        const int slot = p.node_slot[child];
+        base = c.slot_base[slot];
+        item = c.slot_item[slot];
+      } else {
+        base = arena_off[child];
+        item = uint64_t{1} << legs[child].size();
+      }
+    };
+    setup_operand(op.child_a, op.a_leaf, op.a_base, op.a_item);
+    setup_operand(op.child_b, op.b_leaf, op.b_base, op.b_item);
+    op.ia = std::move(pr.ia);
+    op.ib = std::move(pr.ib);
+    sec.lap(0);
+    const auto& a_layout = layout[op.child_a];
+    const auto& b_layout = layout[op.child_b];
+    // m / n bit orders: free legs by increasing address in the output layout
+    auto by_out_addr = [&](std::vector<uint32_t> v) {
+      std::sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) {
+        return stride_in(out_layout, x) < stride_in(out_layout, y);
+      });
+      return v;
+    };
+    op.config = select_config(op.fa, op.fb, op.kc);
+    if (op.config == kGenericConfig && c.precision == MTCG_C64 && op.kc >= 6) op.config = kDotConfig;
+    std::vector<uint32_t> g_order = std::move(pr.g_order), g_start = std::move(pr.g_start),
+                          tg_start = std::move(pr.tg_start);
+    const uint32_t g_max = pr.g_max, tc_slots = pr.tc_slots;
     const bool grouped = tc_slots > 0;
     // Tensor-core path (complex64 only): dense, K-contiguous intermediate A,
     // shapes the 128 x (2N) x (2K) real tiles cover exactly.
@@ -1069,7 +1139,7 @@ Compiled compile_problem(const mtcg_problem& p, const mtcg_options& opt,
     const uint64_t d_open = uint64_t{1} << (op.fa + op.fb);
     op.mults = d_closed * d_open;
     op.adds = (d_closed - 1) * d_open;
-    op.rw = (uint64_t{1} << L.size()) + (uint64_t{1} << R.size()) + d_open;
+    op.rw = (uint64_t{1} << legs[l].size()) + (uint64_t{1} << legs[r].size()) + d_open;
     c.node_contractions[node] = static_cast<uint64_t>(op.nb) * c.n_slices;
     c.mults += op.mults * op.nb * c.n_slices;
     c.adds += op.adds * op.nb * c.n_slices;
