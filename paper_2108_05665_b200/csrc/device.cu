@@ -681,8 +681,10 @@ __device__ __forceinline__ void chain_step_any(int kc, int gb, const T* X, T* Y,
 // chunk's elements are loaded into registers while the current one is
 // contracted and stored (the load latency is the kernel's critical path; a
 // block per chunk left most blocks outside their load phase).
+constexpr int kChainThreads = 128;              // 16 elements per thread per 2048-element chunk
+constexpr int kChainTBits = 7;                  // log2 kChainThreads
 template <class R>
-__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
+__global__ void __launch_bounds__(kChainThreads, sizeof(R) == 4 ? 5 : 3)
     chain_kernel(const __grid_constant__ ChainDev<typename V2<R>::T> d) {
   using T = typename V2<R>::T;
   extern __shared__ __align__(16) uint8_t chain_smem[];
@@ -710,12 +712,12 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
   }
   const T* Aitem = d.a + uint64_t{__ldg(d.entries + item)} * d.a_item;
   T* Oitem = d.out + uint64_t{item} * d.out_item;
-  constexpr int kU = 8;  // elements per thread per chunk (2^(inner + |Q_in|) <= 2048)
-  // element e = threadIdx.x + 256 u of a map: bits 0-7 from the thread,
-  // bits 8-10 from u
+  constexpr int kU = 2048 / kChainThreads;  // elements per thread per chunk (2^(inner + |Q_in|) <= 2048)
+  // element e = threadIdx.x + kChainThreads u of a map: the low kChainTBits
+  // bits from the thread, bits kChainTBits-10 from u
   uint32_t lp = 0, lo = 0, sp = 0, so = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kChainTBits; ++i) {
     if (i < d.ld_bits && (threadIdx.x >> i & 1)) {
       lp += d.ld_p[i];
       lo += d.ld_o[i];
@@ -725,7 +727,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
       so += d.st_o[i];
     }
   }
-  // the per-u parts of the maps (bits 8-10, the same for every thread) live
+  // the per-u parts of the maps (bits >= kChainTBits, the same for every thread) live
   // in shared memory: [ld_o | ld_p | st_o | st_p][u] (registers for them
   // capped the kernel at 3 blocks per SM)
   uint32_t* hmap = tb + d.tbl_words;
@@ -734,8 +736,8 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
     const uint32_t* tab = t == 0 ? d.ld_o : t == 1 ? d.ld_p : t == 2 ? d.st_o : d.st_p;
     const int bits = t < 2 ? d.ld_bits : d.st_bits;
     uint32_t x = 0;
-    for (int i = 0; i < 3; ++i)
-      if (8 + i < bits && (u >> i & 1)) x += tab[8 + i];
+    for (int i = 0; i < 11 - kChainTBits; ++i)
+      if (kChainTBits + i < bits && (u >> i & 1)) x += tab[kChainTBits + i];
     hmap[threadIdx.x] = x;
   }
   __syncthreads();
@@ -748,7 +750,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
     const T* A = Aitem + d.tu_in(outer) + lo;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_ld) v[u] = A[hlo[u]];
+      if (threadIdx.x + kChainThreads * u < d.n_ld) v[u] = A[hlo[u]];
   };
   fetch(outer0);
   const int n_chunks = 1 << d.cpb_bits;
@@ -756,7 +758,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
     __syncthreads();  // the previous chunk's results are stored
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_ld) X0[lp + hlp[u]] = v[u];
+      if (threadIdx.x + kChainThreads * u < d.n_ld) X0[lp + hlp[u]] = v[u];
     if (k + 1 < n_chunks) fetch(outer0 + k + 1);  // in flight during the steps
     T* X = X0;
     T* Y = Y0;
@@ -772,7 +774,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 3 : 2)
     T* O = Oitem + d.tu_out(outer0 + k) + so;
 #pragma unroll
     for (int u = 0; u < kU; ++u)
-      if (threadIdx.x + 256 * u < d.n_st) O[hso[u]] = X[sp + hsp[u]];
+      if (threadIdx.x + kChainThreads * u < d.n_st) O[hso[u]] = X[sp + hsp[u]];
   }
 }
 
@@ -1336,7 +1338,7 @@ void launch_chain(DevicePlan& dp, const Chain& ch, cudaStream_t st) {
   }
   d.tbl_words = static_cast<int>(ch.steps.back().tbl_off + ch.steps.back().tbl.size() - ch.steps[0].tbl_off);
   const size_t smem = (2 * ((size_t{1} << d.q) + 1 << d.inner_bits) + 64 * ch.steps.size()) * sizeof(T) +
-                      4 * static_cast<size_t>(d.tbl_words) + 4 * 32;  // + the per-u map parts
+                      4 * static_cast<size_t>(d.tbl_words) + 4 * 4 * (2048 / kChainThreads);  // + the per-u map parts
   static size_t smem_set[kMaxDevices] = {};  // function attributes are per device
   const int dev = current_device();
   if (smem > 48 * 1024 && smem > smem_set[dev]) {
@@ -1349,7 +1351,7 @@ void launch_chain(DevicePlan& dp, const Chain& ch, cudaStream_t st) {
          (uint64_t{tail.nb} << (d.outer_bits - d.cpb_bits - 1)) >= 148 * 8)
     ++d.cpb_bits;
   const uint64_t blocks = uint64_t{tail.nb} << (d.outer_bits - d.cpb_bits);
-  chain_kernel<R><<<static_cast<unsigned>(blocks), 256, smem, st>>>(d);
+  chain_kernel<R><<<static_cast<unsigned>(blocks), kChainThreads, smem, st>>>(d);
 }
 
 template <class R>
