@@ -1978,6 +1978,58 @@ __global__ void build_bhat_i8_kernel(const BhatSrc src, uint64_t n_cols, int kr_
   }
 }
 
+// The same planes with one block per column pair (few columns, long K: a
+// warp per column left most SMs idle and each warp a long serial chain of
+// table-addressed loads): the column's k range is split over the block.
+__global__ void __launch_bounds__(256) build_bhat_i8_col_kernel(const BhatSrc src, uint64_t n_cols, int kr_pad,
+                                                                uint64_t plane_bytes, uint8_t* bhat,
+                                                                int8_t* sb_out) {
+  __shared__ float red[8];
+  const uint64_t K = uint64_t{1} << src.kc;
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const uint64_t b_slice = src.slice_offset();
+  for (uint64_t col = blockIdx.x; col < n_cols; col += gridDim.x) {
+    float mx = 0.f;
+    for (uint64_t k = threadIdx.x; k < K; k += blockDim.x) {
+      uint64_t kk, n, blk;
+      const float2 v = src.value(col * K + k, b_slice, kk, n, blk);
+      mx = fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[warp] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x / 32); ++w) mx = fmaxf(mx, red[w]);
+    __syncthreads();  // red is reused by the next column
+    const int sb = i8_scale_exp(mx);
+    const float sc = pow2f_wide(sb);
+    if (threadIdx.x == 0) sb_out[col] = static_cast<int8_t>(sb);
+    uint8_t* r0 = bhat + 2 * col * kr_pad;
+    uint8_t* r1 = r0 + kr_pad;
+    for (uint64_t k = threadIdx.x; 2 * k < static_cast<uint64_t>(kr_pad); k += blockDim.x) {
+      uint32_t q[4] = {0x808080u, 0x808080u, 0x808080u, 0x808080u};  // zero digits
+      if (k < K) {
+        uint64_t kk, n, blk;
+        const float2 v = src.value(col * K + k, b_slice, kk, n, blk);
+        q[0] = i8_biased(v.x, sc);
+        q[1] = i8_biased(-v.y, sc);
+        q[2] = i8_biased(v.y, sc);
+        q[3] = i8_biased(v.x, sc);
+      }
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl) {
+        const int sh = 8 * (2 - pl);
+        auto dig = [&](uint32_t x) { return ((x >> sh) & 0xFFu) ^ 0x80u; };
+        *reinterpret_cast<uint16_t*>(r0 + pl * plane_bytes + 2 * k) =
+            static_cast<uint16_t>(dig(q[0]) | (dig(q[1]) << 8));
+        *reinterpret_cast<uint16_t*>(r1 + pl * plane_bytes + 2 * k) =
+            static_cast<uint16_t>(dig(q[2]) | (dig(q[3]) << 8));
+      }
+    }
+  }
+}
+
 // In-place row quantization of the A table (split-integer path, K > 32
 // complex): each row of kr floats (VPL float4 per lane, one warp per row) ->
 // exponent sa_out[row] and digit planes [d0 | d1 | d2] in the row's first
@@ -2250,8 +2302,17 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   uint8_t* bplanes = reinterpret_cast<uint8_t*>(op.bhat_hi);
   {
     const uint64_t n_cols = b_rows / 2;
-    const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n_cols + 7) / 8, 148 * 16));
-    build_bhat_i8_kernel<<<blocks, 256, 0, st>>>(bhat_src(op), n_cols, kr_pad, plane_bytes, bplanes, op.col_exp);
+    // few columns with a long K: a block per column (MTCG_BHAT_COL=0|1 forces)
+    static const char* col_env = std::getenv("MTCG_BHAT_COL");
+    const bool per_block = col_env ? std::atoi(col_env) != 0 : (n_cols < 148 * 16 && Kr >= 512);
+    if (per_block) {
+      const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>(n_cols, 148 * 8));
+      build_bhat_i8_col_kernel<<<blocks, 256, 0, st>>>(bhat_src(op), n_cols, kr_pad, plane_bytes, bplanes,
+                                                       op.col_exp);
+    } else {
+      const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((n_cols + 7) / 8, 148 * 16));
+      build_bhat_i8_kernel<<<blocks, 256, 0, st>>>(bhat_src(op), n_cols, kr_pad, plane_bytes, bplanes, op.col_exp);
+    }
     ++launches;
   }
   DevAttr& da = dev_attr();
