@@ -358,8 +358,16 @@ constexpr int kTraceTiles = 256;
 __device__ __forceinline__ void trace(const TcParams& p, uint64_t it, int slot) {
   if (p.dbg && blockIdx.x == 0 && it < kTraceTiles) p.dbg[it * 8 + slot] = clock64();
 }
-// split-integer kernel: 16 slots per tile (the 8 above + finer marks)
+// split-integer kernel: 16 slots per tile (the 8 above + finer marks 8-12,
+// compiled in only with -DMTCG_TC_TRACE_FINE: they cost the hot role loops
+// instructions even when tracing is off)
+#ifdef MTCG_TC_TRACE_FINE
+constexpr bool kTraceFine = true;
+#else
+constexpr bool kTraceFine = false;
+#endif
 __device__ __forceinline__ void trace16(const TcParams& p, uint64_t it, int slot) {
+  if (!kTraceFine && slot >= 8) return;
   if (p.dbg && blockIdx.x == 0 && it < kTraceTiles) p.dbg[it * 16 + slot] = clock64();
 }
 
