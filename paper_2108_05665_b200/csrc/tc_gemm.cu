@@ -358,16 +358,16 @@ constexpr int kTraceTiles = 256;
 __device__ __forceinline__ void trace(const TcParams& p, uint64_t it, int slot) {
   if (p.dbg && blockIdx.x == 0 && it < kTraceTiles) p.dbg[it * 8 + slot] = clock64();
 }
-// split-integer kernel: 16 slots per tile (the 8 above + finer marks 8-12,
-// compiled in only with -DMTCG_TC_TRACE_FINE: they cost the hot role loops
-// instructions even when tracing is off)
-#ifdef MTCG_TC_TRACE_FINE
-constexpr bool kTraceFine = true;
+// split-integer kernel: 16 slots per tile (the 8 above + finer marks 8-12).
+// Compiled in only with -DMTCG_TC_TRACE_BUILD (make TRACE=1): the checks cost
+// the hot role loops instructions even when tracing is off (mode-C ops 2-5%).
+#ifdef MTCG_TC_TRACE_BUILD
+constexpr bool kTraceBuild = true;
 #else
-constexpr bool kTraceFine = false;
+constexpr bool kTraceBuild = false;
 #endif
 __device__ __forceinline__ void trace16(const TcParams& p, uint64_t it, int slot) {
-  if (!kTraceFine && slot >= 8) return;
+  if (!kTraceBuild) return;
   if (p.dbg && blockIdx.x == 0 && it < kTraceTiles) p.dbg[it * 16 + slot] = clock64();
 }
 
@@ -2393,7 +2393,12 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
                              : static_cast<unsigned>(std::min<uint64_t>(tiles, da.n_sms));
   const unsigned threads = 64 + 32 * n_conv + 128 * kEpiGroups;
   const char* tr = std::getenv("MTCG_TC_TRACE");
-  const bool tracing = tr && std::atoi(tr) == op.node;
+  const bool tracing = kTraceBuild && tr && std::atoi(tr) == op.node;
+  if (tr && !kTraceBuild) {
+    static bool warned = false;
+    if (!warned) std::fprintf(stderr, "[mtcg] MTCG_TC_TRACE needs a trace build (make -C csrc TRACE=1)\n");
+    warned = true;
+  }
   if (tracing) {
     TCK(cudaMalloc(&p.dbg, sizeof(unsigned long long) * kTraceTiles * 16));
     TCK(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned long long) * kTraceTiles * 16, st));
