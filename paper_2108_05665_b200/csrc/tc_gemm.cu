@@ -1234,7 +1234,7 @@ __device__ __forceinline__ int convert_row_i8(uint8_t* sp, int r, int n_conv) {
   return sa;
 }
 
-template <bool PAIR, bool QA>
+template <bool PAIR, bool QA, bool TR>
 __global__ void __launch_bounds__(kPThreads, 1)
     tc_i8_persistent(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                      const TcParams p, int n_stages) {
@@ -1267,7 +1267,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // the output row offset table (both halves) cached in shared memory when
   // small (p.tom_cache): the epilogue's per-tile row offsets are then shared
   // loads (global ones stalled the loop on the load's address registers)
-  uint32_t* tom_s = reinterpret_cast<uint32_t*>(stage_out + (p.transpose ? 4 * kEpiGroups * 32 * 33 : 0));
+  uint32_t* tom_s = reinterpret_cast<uint32_t*>(stage_out + (TR ? 4 * kEpiGroups * 32 * 33 : 0));
   const uint32_t tom_lo_n = 1u << p.tom.lo_bits;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1290,7 +1290,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   // acc0 columns and release acc1 / acc2 at once, (2) store the result — and
   // acc0 alternates between columns [0, bn) and [3 bn, 4 bn) by tile parity,
   // so the next tile's main loop runs while phase 2 drains.
-  const bool split = n_acc == 1;
+  const bool split = PAIR || n_acc == 1;  // pair tiles are 128 columns: always one accumulator set
   constexpr int n_epi = kEpiGroups;
   const bool ton_cached = n_item_cols <= kMaxTonCache;
   if (ton_cached)
@@ -1638,7 +1638,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
       }
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] *= cs[j / 2];
-      if (p.transpose) {
+      if constexpr (TR) {
         float* buf = stage_out + (warp - e0) * 32 * 33;
 #pragma unroll
         for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = v[j];
@@ -2382,9 +2382,13 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   static const char* blk_env = std::getenv("MTCG_TC_BLOCKED");
   p.blocked = blk_env ? std::atoi(blk_env) : (!ga && Nr <= static_cast<uint64_t>(bn) && units >= 2);
   p.dbg = nullptr;
-  const int slot = 4 + (pair ? 2 : 0) + (qa ? 1 : 0);
-  auto kern = pair ? (qa ? tc_i8_persistent<true, true> : tc_i8_persistent<true, false>)
-                   : (qa ? tc_i8_persistent<false, true> : tc_i8_persistent<false, false>);
+  // instances: the epilogue's store path (transposed through shared memory
+  // or row-per-lane) is a template parameter, so each instance carries one
+  // (pair tiles are 128 columns wide: never transposed)
+  const int slot = transpose ? 8 + (qa ? 1 : 0) : 4 + (pair ? 2 : 0) + (qa ? 1 : 0);
+  auto kern = pair ? (qa ? tc_i8_persistent<true, true, false> : tc_i8_persistent<true, false, false>)
+          : transpose ? (qa ? tc_i8_persistent<false, true, true> : tc_i8_persistent<false, false, true>)
+                      : (qa ? tc_i8_persistent<false, true, false> : tc_i8_persistent<false, false, false>);
   ensure_smem(da, slot, kern, smem, pair);
   const uint64_t tile_m = pair ? 2 * kBM : kBM;
   const uint64_t tiles = ga ? uint64_t{op.n_ga_tiles} * ((Nr + bn - 1) / bn)
