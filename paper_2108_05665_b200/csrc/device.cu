@@ -1491,6 +1491,7 @@ void launch_slice_ops(DevicePlan& dp, void* d_acc, cudaStream_t st_main, cudaEve
         // = ton(2j) + 1), not a contiguous n range
         t.n_contig = (op.ton.bits >= 1 && (op.ton.lo_bits >= 1 ? op.ton.lo[1] : op.ton.hi[1]) == 1) ? 1 : 0;
         t.m_contig = op.o_mcontig ? 1 : 0;
+        t.m_stride0 = op.tom.bits >= 1 ? (op.tom.lo_bits >= 1 ? op.tom.lo[1] : op.tom.hi[1]) : 1;
         dp.engine->launches += tc_contract(t, st);  // [absmax +] B̂ build + GEMM
         if (op_events) CK(cudaEventRecord(op_events[2 * oi + 1], st));
         if (dag) dag->end(oi);

@@ -1623,7 +1623,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     uint32_t tb = split ? 0u : static_cast<uint32_t>(it) % n_acc, tb_round = split ? 0u : static_cast<uint32_t>(it) / n_acc;
     uint32_t sa_slot = static_cast<uint32_t>(it), sa_round = 0;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const bool wide = p.Kr > 1024;
+    const bool wide = QA && p.Kr > 1024;  // whole-K (mode C) tiles: Kr <= 64
     // scatter one 32-column chunk (16 complex columns from cc) of this lane's
     // row, scaled, to the output
     auto store_chunk = [&](float (&v)[32], int cc, float rs) {
@@ -2328,7 +2328,13 @@ int tc_contract_i8(const TcOp& op, cudaStream_t st) {
   const bool pair = !ga && bn == 128 && M >= 256 && da.n_sms >= 2 &&
                     !(std::getenv("MTCG_TC_PAIR") && std::atoi(std::getenv("MTCG_TC_PAIR")) == 0);
   const int bn_cta = pair ? bn / 2 : bn;
-  const bool transpose = !op.m_contig && bn <= 64;
+  // transposed stores (through shared memory) only for widely spaced rows:
+  // with m bit 0 at stride <= 4 the rows' column runs pack into whole sectors
+  // and the row-per-lane stores were faster on every such op of cfg2 / cfg3
+  // (node 618: 9.8 → 8.7 ms); MTCG_TC_TRANSPOSE=0|1 forces
+  static const char* tr_env = std::getenv("MTCG_TC_TRANSPOSE");
+  const bool transpose =
+      bn <= 64 && !pair && (tr_env ? std::atoi(tr_env) != 0 : !op.m_contig && op.m_stride0 >= 8);
   const int n_conv = qa ? (pair ? 1 : 0) : 4;  // QA pair: one relay warp
   const int extra0 = 1024 + 8 * (3 * kMaxStages + 2 * kMaxAcc + 2 + kSaRing) + 16 +
                     4 * static_cast<int>(std::min<uint64_t>(N, kMaxTonCache)) + 16 + 8 * kEpiGroups * (kMaxBn / 2) +

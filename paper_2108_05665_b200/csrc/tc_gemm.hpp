@@ -37,6 +37,7 @@ struct TcOp {
   int tom_bits, ton_bits;
   int n_contig;                   // output n index contiguous (vector epilogue stores)
   int m_contig;                   // output m index contiguous (row-per-lane stores coalesce)
+  uint64_t m_stride0;             // output stride of m bit 0 (complex elements)
   // Grouped mode (slots > 0): items sharing an A entry are one GEMM whose N
   // is the concatenation of `slots` item B blocks (padded with zero blocks).
   const uint32_t* grp_items;      // items ordered by A entry
