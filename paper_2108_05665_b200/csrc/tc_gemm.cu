@@ -1131,11 +1131,12 @@ __device__ __forceinline__ void i8_load_combine(uint32_t t0, uint32_t t1, uint32
 // plane 0; planes are pa / pb bytes apart (>> 4 in the descriptor).
 template <bool PAIR>
 __device__ __forceinline__ void mma_stage_i8(uint32_t d, uint32_t d1, uint32_t d2, uint64_t a, uint64_t b,
-                                             uint32_t pa, uint32_t pb, uint32_t idesc, uint32_t acc) {
+                                             uint32_t pa, uint32_t pb, uint32_t idesc, uint32_t acc, int n_ks = 2) {
   const uint64_t a1 = a + (pa >> 4), a2 = a + 2 * (pa >> 4);
   const uint64_t b1 = b + (pb >> 4), b2 = b + 2 * (pb >> 4);
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks) {
+    if (ks >= n_ks) break;  // K = 16 complex: the second k-step would multiply zero padding
     const uint64_t o = 2 * ks;  // 32 bytes further along the swizzled row
     const uint32_t f = ks ? 1u : acc;
     if constexpr (PAIR) {
@@ -1212,19 +1213,16 @@ __device__ __forceinline__ int convert_row_i8(uint8_t* sp, int r, int n_conv) {
   const int sa = i8_scale_exp(m[0]);
   const float sc = pow2f_wide(sa);
   asm volatile("bar.sync 3, %0;" ::"r"(32 * n_conv) : "memory");  // every raw read done (in place)
+  // K = 16 complex (!TWO): chunks 2-3 (the second 32-byte k-step) are never
+  // read — the MMA issues one k-step for these tiles — so they are not written
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {  // 16-byte chunk j of each plane row = elements 16j .. 16j + 15
+  for (int j = 0; j < (TWO ? 4 : 2); ++j) {  // 16-byte chunk j of each plane row = elements 16j .. 16j + 15
     uint32_t w[3][4];
-    if (TWO || j < 2) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float4 x = v[(4 * j + q) % NC];
-        i8_pack4(i8_biased(x.x, sc), i8_biased(x.y, sc), i8_biased(x.z, sc), i8_biased(x.w, sc), w[0][q], w[1][q],
-                 w[2][q]);
-      }
-    } else {  // zero padding: every digit 0
-#pragma unroll
-      for (int q = 0; q < 4; ++q) w[0][q] = w[1][q] = w[2][q] = 0u;
+    for (int q = 0; q < 4; ++q) {
+      const float4 x = v[(4 * j + q) % NC];
+      i8_pack4(i8_biased(x.x, sc), i8_biased(x.y, sc), i8_biased(x.z, sc), i8_biased(x.w, sc), w[0][q], w[1][q],
+               w[2][q]);
     }
     const int off = r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
 #pragma unroll
@@ -1283,6 +1281,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const uint64_t t_last = p.blocked ? tiles * (cta0 + 1) / ncta : tiles;
   const uint64_t t_stride = p.blocked ? 1 : ncta;
   const int k_stages = QA ? p.Kr / kI8Kb : 1;
+  const int n_ks = QA || p.Kr > 32 ? 2 : 1;  // 32-byte k-steps per stage (K = 16 complex: one)
   const uint32_t buf_cols = 3 * p.bn;
   const uint32_t n_acc = min(static_cast<uint32_t>(kMaxAcc), 512u / buf_cols);
   // One 3 x bn accumulator set (bn = 128): both epilogue groups drain every
@@ -1481,7 +1480,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sp = smem_u32(base + st * stage_bytes);
         mma_stage_i8<PAIR>(dacc, d1, d2, sw_desc<16>(sp), sw_desc<16>(sp + a_span), kPlaneA,
-                           static_cast<uint32_t>(plane_b), idesc, s > 0 ? 1u : 0u);
+                           static_cast<uint32_t>(plane_b), idesc, s > 0 ? 1u : 0u, n_ks);
         if constexpr (PAIR)
           mma_commit_pair_elect(&empty[st]);
         else
